@@ -1,0 +1,212 @@
+/*
+ * cbx.h -- C-ABI of the B200-native CBinfer change-based inference path.
+ *
+ * This is the drop-in boundary: plain C types, POD descriptors, int status
+ * codes, no torch or C++ types. It replaces the per-frame network-evaluation
+ * API of the reference (namespace cbinfer, /root/reference/proj):
+ *
+ *   cbx_create + cbx_load_layer  <- load_network            core/include/cbinfer/network.hpp:88
+ *                                   (+ read_weights_f32le   core/include/cbinfer/io.hpp:29)
+ *   cbx_forward / _device        <- forward_frame           core/include/cbinfer/network.hpp:93-94
+ *   cbx_reset                    <- reset_state             core/include/cbinfer/network.hpp:97
+ *   cbx_set_thresholds           <- Network::set_thresholds core/include/cbinfer/network.hpp:67
+ *   cbx_get_thresholds           <- Network::thresholds     core/include/cbinfer/network.hpp:66
+ *   cbx_chain_dims               <- chain_dims              core/include/cbinfer/network.hpp:45
+ *   cbx_get_trace / _activation  <- ForwardTrace/CBConvTrace network.hpp:80-83, cbconv.hpp:82-85
+ *   cbx_op_*                     <- detect_changes / dilate_changes / extract_indexes /
+ *                                   maxpool / argmax_classify (cbconv.hpp:87-106,
+ *                                   baseline.hpp:69-79), on device pointers
+ *   cbx_random_filters           <- random_filters          core/include/cbinfer/synth.hpp:80
+ *   cbx_synth_frame              <- synth_frame             core/include/cbinfer/synth.hpp:46
+ *
+ * Status codes map 1:1 onto the reference exception hierarchy
+ * (core/include/cbinfer/error.hpp:9-42); the message of the last failure on a
+ * context is returned by cbx_last_error(ctx) (or cbx_last_error(NULL) for
+ * context-free calls, per thread).
+ *
+ * Threading: a context is one Network (a batch of S independent camera
+ * streams) on one device. It is stream-affine and not thread-safe, mirroring
+ * "one Network processes one frame at a time"; distinct
+ * contexts may run concurrently.
+ */
+#ifndef CBX_H
+#define CBX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CBX_API __attribute__((visibility("default")))
+
+typedef enum {
+    CBX_OK = 0,
+    CBX_E_SHAPE = 1,    /* shape_error    */
+    CBX_E_GEOMETRY = 2, /* geometry_error */
+    CBX_E_BOUNDS = 3,   /* bounds_error   */
+    CBX_E_IO = 4,       /* io_error       */
+    CBX_E_SPEC = 5,     /* spec_error     */
+    CBX_E_CUDA = 6,     /* CUDA runtime / device failure (no CPU fallback exists) */
+    CBX_E_ARG = 7       /* invalid argument (null pointer, bad enum) */
+} cbx_status;
+
+/* LayerKind, network.hpp:12 */
+typedef enum { CBX_CBCONV = 0, CBX_CONV = 1, CBX_RELU = 2, CBX_MAXPOOL = 3, CBX_CLASSIFY = 4 } cbx_layer_kind;
+
+/* Engine, network.hpp:70 */
+typedef enum { CBX_ENGINE_BASELINE = 0, CBX_ENGINE_CBINFER = 1 } cbx_engine;
+
+/* Arithmetic of the convolution contraction. EXACT reproduces the reference
+ * fp32 accumulation order bit for bit (bias first, ascending (c,kj,ki), one
+ * rounding per multiply and per add). TF32 runs layers with channels-last
+ * inputs on tcgen05 tensor cores (tf32 operands, fp32 accumulate). */
+typedef enum { CBX_PREC_EXACT = 0, CBX_PREC_TF32 = 1 } cbx_precision;
+
+/* ConvGeometry, geometry.hpp:12-49 */
+typedef struct {
+    int kernelH, kernelW, strideH, strideW, padH, padW, inChannels, outChannels;
+} cbx_geom;
+
+/* LayerSpec, network.hpp:17-27 (weights are passed separately) */
+typedef struct {
+    int kind;       /* cbx_layer_kind */
+    cbx_geom geom;  /* conv kinds; inChannels is filled by cbx_chain_dims/cbx_create */
+    int window;     /* MAXPOOL */
+    int stride;     /* MAXPOOL */
+    float threshold;/* CBCONV, >= 0 */
+    int fuseRelu;   /* CBCONV */
+} cbx_layer_desc;
+
+/* NetworkSpec, network.hpp:29-35 */
+typedef struct {
+    int inputChannels, inputHeight, inputWidth, numClasses;
+    int numLayers;
+    const cbx_layer_desc* layers;
+} cbx_net_desc;
+
+/* LayerStats, cbconv.hpp:55-60 (timings are measured with CUDA events by the caller) */
+typedef struct {
+    int64_t changedInputPixels;
+    int64_t changedOutputPixels;
+    uint64_t gemmMacs;
+} cbx_layer_stats;
+
+typedef struct cbx_ctx cbx_ctx;
+
+CBX_API const char* cbx_last_error(const cbx_ctx* ctx);
+CBX_API const char* cbx_version(void);
+
+/* chain_dims: validates the chain, fills layers[k].geom.inChannels and writes
+ * per-layer in/out dims (dims[6k..6k+5] = inC,inH,inW,outC,outH,outW). */
+CBX_API int cbx_chain_dims(const cbx_net_desc* net, cbx_layer_desc* layers_out, int* dims);
+
+/* Create a network context on `device` serving `num_streams` independent
+ * camera streams (each with its own change-based state). */
+CBX_API int cbx_create(const cbx_net_desc* net, int device, int num_streams, int precision,
+                       cbx_ctx** out);
+CBX_API void cbx_destroy(cbx_ctx* ctx);
+
+/* Install the filters of conv layer `layer` (0-based index in the layer
+ * list) in the reference layout: K row-major [outC][inC*kH*kW] with columns in
+ * (c, kj, ki) order (baseline.hpp:11-12), then outC biases. Host memory. */
+CBX_API int cbx_load_layer(cbx_ctx* ctx, int layer, const float* K, const float* bias);
+
+CBX_API int cbx_set_thresholds(cbx_ctx* ctx, const float* taus, int n);
+CBX_API int cbx_get_thresholds(const cbx_ctx* ctx, float* taus, int n);
+
+/* Drops all change-based state of every stream: the next frame is a full
+ * evaluation (reset_state, network.cpp:317-320). */
+CBX_API int cbx_reset(cbx_ctx* ctx);
+
+/* One frame for each of the S streams, HOST buffers:
+ *   frames: S planar CHW fp32 frames back to back (S*C*H*W floats)
+ *   labels: S label maps (uint16, row-major), may be NULL
+ *   stats : S*numLayers entries (stream-major), may be NULL
+ *   macs  : S entries (macsTotal per stream), may be NULL
+ * Synchronous: returns after labels/stats are in host memory. The
+ * Baseline engine evaluates every layer full-frame and leaves the
+ * change-based state untouched (network.cpp:278-285). */
+CBX_API int cbx_forward(cbx_ctx* ctx, int engine, const float* frames, uint16_t* labels,
+                        cbx_layer_stats* stats, uint64_t* macs);
+
+/* Device-resident variant for clips already in HBM: frames_dev[s] points to
+ * stream s's planar frame on the context's device. The previous call's frame
+ * buffers must stay valid until this call returns (they are the detection
+ * reference, i.e. prevInput of the first CBCONV). Asynchronous on the context
+ * stream; use cbx_sync / cbx_read_* afterwards. */
+CBX_API int cbx_forward_device(cbx_ctx* ctx, int engine, const float* const* frames_dev);
+CBX_API int cbx_sync(cbx_ctx* ctx);
+CBX_API int cbx_read_labels(cbx_ctx* ctx, int engine, uint16_t* labels);
+CBX_API int cbx_read_stats(cbx_ctx* ctx, int engine, cbx_layer_stats* stats, uint64_t* macs);
+CBX_API int cbx_labels_device(cbx_ctx* ctx, int engine, const uint16_t** labels_dev);
+
+/* Context stream as a cudaStream_t (void* here). */
+CBX_API void* cbx_stream(cbx_ctx* ctx);
+/* Number of kernel launches (graph kernel nodes) issued by the last forward. */
+CBX_API int cbx_last_launch_count(const cbx_ctx* ctx);
+
+/* Per-kernel device time of one forward: the frame is run WITHOUT the CUDA
+ * graph, every kernel bracketed by CUDA events on the context stream. The
+ * state advances exactly as with cbx_forward_device. */
+typedef struct {
+    char name[32];
+    int layer;
+    float ms;
+} cbx_kernel_time;
+CBX_API int cbx_profile_forward(cbx_ctx* ctx, int engine, const float* const* frames_dev,
+                                cbx_kernel_time* out, int cap, int* n);
+
+/* Trace access for parity checks (CBConvTrace / ForwardTrace):
+ *   cbx_get_activation: output of layer `layer` for stream s, planar CHW, host
+ *   cbx_get_trace: CBCONV ordinal `cb`, stream s: detected input-grid mask
+ *   (uint8 H*W, zeroed on the first frame) and the ascending updated index list
+ *   (int32, capacity Ho*Wo); *n receives the count; *first is set to 1 when
+ *   the last frame was a full evaluation (the reference's empty `detected`). */
+CBX_API int cbx_get_activation(cbx_ctx* ctx, int engine, int layer, int s, float* out);
+CBX_API int cbx_get_trace(cbx_ctx* ctx, int cb, int s, uint8_t* detected, int32_t* updated,
+                          int64_t* n, int* first);
+
+/* ---- op level, device pointers, asynchronous on `stream` (cudaStream_t) ---- */
+CBX_API int cbx_op_detect(const float* cur, const float* prev, int C, int H, int W, float tau,
+                          uint8_t* mask, unsigned long long* count_dev, void* stream);
+CBX_API int cbx_op_dilate(const uint8_t* mask, int H, int W, const cbx_geom* geom, uint8_t* out,
+                          void* stream);
+/* Workspace bytes for cbx_op_extract over n mask bytes. */
+CBX_API size_t cbx_op_extract_workspace(int64_t n);
+CBX_API int cbx_op_extract(const uint8_t* mask, int64_t n, int32_t* idx, int* count_dev,
+                           void* workspace, void* stream);
+CBX_API int cbx_op_maxpool(const float* in, int C, int H, int W, int window, int stride,
+                           float* out, void* stream);
+CBX_API int cbx_op_argmax(const float* t, int C, int H, int W, uint16_t* labels, void* stream);
+/* Reduced conv over an index list (gen_x_reduced + gemm + update_output,
+ * cbconv.cpp:115-155), planar CHW in/out, exact fp32 order; out is updated in
+ * place at the listed output pixels. */
+CBX_API int cbx_op_cbconv_update(const float* in, int C, int H, int W, const float* K,
+                                 const float* bias, const cbx_geom* geom, const int32_t* idx,
+                                 int n, int fuseRelu, float* out, void* stream);
+
+/* ---- input fixtures (synth.hpp) ---- */
+CBX_API int cbx_random_filters(const cbx_geom* geom, uint32_t seed, float* K, float* bias);
+typedef struct {
+    int size, velocity;
+    float intensity;
+} cbx_sprite;
+typedef struct {
+    int channels, height, width, frames;
+    int numSprites;
+    const cbx_sprite* sprites;
+    float noiseAmplitude;
+    uint32_t seed;
+} cbx_synth_cfg;
+/* Host frame (noise supported). */
+CBX_API int cbx_synth_frame(const cbx_synth_cfg* cfg, int f, float* out);
+/* Device frame (noise-free clips only; noise needs the sequential mt19937). */
+CBX_API int cbx_synth_frame_device(const cbx_synth_cfg* cfg, int f, float* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CBX_H */

@@ -1,0 +1,56 @@
+// common.cuh -- shared device/host definitions of the cbx engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cbx {
+
+constexpr int kNumSMs = 148;  // B200
+
+// Activation tensor on the device. All intermediate activations are
+// channels-last (HWC) with the channel stride padded to a multiple of 4
+// floats (one 16-byte chunk) and a zero halo of `hh`/`hw` pixels so that the
+// consumer's zero padding is free. Layout per stream: [Hp][Wp][Cp]; streams
+// are `ss` floats apart. The network input (the camera frame) is the only
+// planar (CHW) tensor; it is addressed through a per-stream pointer table.
+struct TensorView {
+    float* d;
+    int C, H, W;     // logical
+    int Cp, Hp, Wp;  // padded
+    int hh, hw;      // halo
+    int64_t ss;      // floats per stream
+};
+
+// Byte mask on a pixel grid: [S][stride], pixel p = y*W + x.
+struct MaskView {
+    uint8_t* d;
+    int H, W;
+    int64_t stride;
+};
+
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// Reference ReLU: std::max(0.0f, v) == (0.0f < v) ? v : 0.0f (baseline.cpp:115).
+__device__ __forceinline__ float ref_relu(float v) { return (0.0f < v) ? v : 0.0f; }
+// Reference max: std::max(m, v) == (m < v) ? v : m (baseline.cpp:138).
+__device__ __forceinline__ float ref_max(float m, float v) { return (m < v) ? v : m; }
+// Reference change test (cbconv.cpp:66-67): strict on both signs.
+__device__ __forceinline__ bool ref_changed(float now, float before, float tau) {
+    const float d = __fsub_rn(now, before);
+    return d > tau || -d > tau;
+}
+
+// Adds `flag` into counters[s*stride] with one atomic per (warp, stream).
+__device__ __forceinline__ void warp_count_add(unsigned long long* counters, int stride, int s,
+                                               bool flag, bool active) {
+    const unsigned act = __ballot_sync(0xffffffffu, active);
+    if (!active) return;
+    const unsigned same = __match_any_sync(act, s);
+    const unsigned hits = __ballot_sync(act, flag) & same;
+    const int leader = __ffs(same) - 1;
+    if ((int)(threadIdx.x & 31) == leader && hits)
+        atomicAdd(counters + (int64_t)s * stride, (unsigned long long)__popc(hits));
+}
+
+}  // namespace cbx

@@ -1,0 +1,791 @@
+// engine.cu -- device runtime of one change-based network (see engine.hpp).
+//
+// Frame recipe (reference: forward_frame network.cpp:252-315, cbconv_forward
+// cbconv.cpp:157-228). Tensor t is the input of layer t (t = 0: the camera
+// frame, planar, addressed through a per-stream pointer table).
+//
+//   steady frame, for each layer k
+//     CBCONV  : U_k = dilate(chg_k)              (K3)   cbconv.cpp:73-82
+//               idx_k = compact(U_k)             (K2)   cbconv.cpp:99-113
+//               T_{k+1}[idx_k] = conv(T_k)       (K4)   cbconv.cpp:115-155
+//               + chg_{k+1} by compare-before-write when layer k+1 is CBCONV
+//     MAXPOOL : recompute windows touched by upd_k, compare-before-write
+//     RELU    : recompute pixels in upd_k, compare-before-write
+//     CONV    : recompute dilate(upd_k) (== upd_k for 1x1), reusing idx lists
+//     CLASSIFY: argmax over upd_k
+//   chg_0 = detect(frame_t, frame_{t-1}) (K1) cbconv.cpp:57-71
+//
+// chg_t ("changed by more than the consumer's tau") equals the reference's
+// detect_changes(input, prevInput) because the tensor is updated in place:
+// pixels outside the producer's updated set are bitwise unchanged and the
+// writer compares the new value with the one it overwrites.
+//
+// First frame after reset and the Baseline engine run the same kernels in
+// "full" mode: no masks, every output pixel evaluated.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "engine.hpp"
+#include "kernels.hpp"
+#include "conv_tc.hpp"
+
+namespace cbx {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Error(CBX_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+int fdiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+bool is_conv(int kind) { return kind == CBX_CBCONV || kind == CBX_CONV; }
+
+bool identity_geom(const cbx_geom& g) {
+    return g.kernelH == 1 && g.kernelW == 1 && g.strideH == 1 && g.strideW == 1 && g.padH == 0 &&
+           g.padW == 0;
+}
+
+std::string where(int k, int kind) {
+    static const char* names[] = {"CBCONV", "CONV", "RELU", "MAXPOOL", "CLASSIFY"};
+    return "layer " + std::to_string(k + 1) + " (" + (kind >= 0 && kind < 5 ? names[kind] : "?") + ")";
+}
+
+template <class T>
+T* dmalloc(size_t n) {
+    void* p = nullptr;
+    CBX_CUDA(cudaMalloc(&p, n * sizeof(T) + 16));
+    CBX_CUDA(cudaMemset(p, 0, n * sizeof(T) + 16));
+    return static_cast<T*>(p);
+}
+
+}  // namespace
+
+// chain_dims, network.cpp:128-188
+std::vector<int> chain_dims(const cbx_net_desc& net, std::vector<cbx_layer_desc>& L) {
+    if (net.numLayers < 1 || !net.layers) throw Error(CBX_E_SPEC, "network spec has no layers");
+    if (net.inputChannels < 1 || net.inputHeight < 1 || net.inputWidth < 1)
+        throw Error(CBX_E_SPEC, "network spec has invalid input dimensions");
+    if (net.numClasses < 1) throw Error(CBX_E_SPEC, "network spec has invalid class count");
+    L.assign(net.layers, net.layers + net.numLayers);
+    std::vector<int> dims(6 * L.size());
+    int c = net.inputChannels, h = net.inputHeight, w = net.inputWidth;
+    for (size_t k = 0; k < L.size(); ++k) {
+        cbx_layer_desc& l = L[k];
+        int oc = c, oh = h, ow = w;
+        dims[6 * k + 0] = c;
+        dims[6 * k + 1] = h;
+        dims[6 * k + 2] = w;
+        switch (l.kind) {
+            case CBX_CBCONV:
+            case CBX_CONV: {
+                cbx_geom& g = l.geom;
+                g.inChannels = c;
+                if (g.kernelH < 1 || g.kernelW < 1 || g.strideH < 1 || g.strideW < 1 || g.padH < 0 || g.padW < 0)
+                    throw Error(CBX_E_GEOMETRY, where((int)k, l.kind) + ": invalid convolution geometry");
+                if (h + 2 * g.padH < g.kernelH || w + 2 * g.padW < g.kernelW)
+                    throw Error(CBX_E_GEOMETRY, where((int)k, l.kind) + ": convolution output would be empty");
+                if (g.outChannels < 1) throw Error(CBX_E_SPEC, where((int)k, l.kind) + ": invalid outChannels");
+                if (l.kind == CBX_CBCONV && l.threshold < 0.0f)
+                    throw Error(CBX_E_SPEC, "network spec: negative threshold");
+                oc = g.outChannels;
+                oh = (h + 2 * g.padH - g.kernelH) / g.strideH + 1;
+                ow = (w + 2 * g.padW - g.kernelW) / g.strideW + 1;
+                break;
+            }
+            case CBX_RELU:
+                break;
+            case CBX_MAXPOOL:
+                if (l.window < 1 || l.stride < 1 || l.window > h || l.window > w)
+                    throw Error(CBX_E_GEOMETRY, where((int)k, l.kind) + ": invalid pooling window");
+                oh = (h - l.window) / l.stride + 1;
+                ow = (w - l.window) / l.stride + 1;
+                break;
+            case CBX_CLASSIFY:
+                if (k + 1 != L.size()) throw Error(CBX_E_SPEC, where((int)k, l.kind) + ": CLASSIFY must be the last layer");
+                if (c != net.numClasses)
+                    throw Error(CBX_E_SPEC, where((int)k, l.kind) + ": classification input has " + std::to_string(c) +
+                                                " channels, expected " + std::to_string(net.numClasses) + " classes");
+                oc = 1;
+                break;
+            default:
+                throw Error(CBX_E_SPEC, "unknown layer kind");
+        }
+        dims[6 * k + 3] = oc;
+        dims[6 * k + 4] = oh;
+        dims[6 * k + 5] = ow;
+        c = oc;
+        h = oh;
+        w = ow;
+    }
+    const bool hasClassify = L.back().kind == CBX_CLASSIFY;
+    const int finalC = hasClassify ? dims[6 * (L.size() - 1)] : dims[6 * (L.size() - 1) + 3];
+    if (finalC != net.numClasses)
+        throw Error(CBX_E_SPEC, "network produces " + std::to_string(finalC) + " channels, expected " +
+                                    std::to_string(net.numClasses) + " classes");
+    return dims;
+}
+
+struct Engine::Plan {
+    bool baseline = false;
+    std::vector<TensorView> T;      // nl+1; T[0] = frame (planar) unless ingested
+    bool ingest = false;            // first layer is not a conv: frame copied to HWC T[0]
+    std::vector<MaskView> chg;      // nl+1
+    std::vector<bool> chg_by_conv;  // chg written with 1s only -> cleared per frame
+    std::vector<MaskView> upd;      // nl+1 (aliases)
+    std::vector<int> upd_owner;     // producing layer of upd[t] (-1 detect, -2 none)
+    std::vector<MaskView> U;        // nl (owned)
+    std::vector<int32_t*> idx;
+    std::vector<int*> cnt;
+    std::vector<int> idx_src;       // conv layer whose list is reused (-1: own)
+    std::vector<void*> allocs;
+    void* ws = nullptr;
+    uint16_t* labels = nullptr;
+    unsigned long long* stats = nullptr;  // [nl][S][2]
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    int launches[2] = {0, 0};
+    bool dirty = true;
+
+    ~Plan() {
+        for (auto& g : gexec)
+            if (g) cudaGraphExecDestroy(g);
+        for (void* p : allocs) cudaFree(p);
+    }
+    template <class T>
+    T* alloc(size_t n) {
+        T* p = dmalloc<T>(n);
+        allocs.push_back(p);
+        return p;
+    }
+    MaskView mask(int S, int H, int W) {
+        MaskView m{nullptr, H, W, round_up((int64_t)H * W, 16)};
+        m.d = alloc<uint8_t>((size_t)(m.stride * S));
+        return m;
+    }
+};
+
+Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
+    : device_(device), S_(S), precision_(precision) {
+    if (S < 1) throw Error(CBX_E_ARG, "num_streams must be >= 1");
+    if (precision != CBX_PREC_EXACT && precision != CBX_PREC_TF32) throw Error(CBX_E_ARG, "bad precision");
+    dims_ = chain_dims(net, layers_);
+    net_ = net;
+    net_.layers = layers_.data();
+    CBX_CUDA(cudaSetDevice(device));
+    int ndev = 0;
+    CBX_CUDA(cudaGetDeviceCount(&ndev));
+    CBX_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    const int nl = (int)layers_.size();
+    dK_.assign(nl, nullptr);
+    dBias_.assign(nl, nullptr);
+    tc_.resize(nl);
+    for (int k = 0; k < nl; ++k) {
+        if (layers_[k].kind == CBX_CBCONV) cb_layers_.push_back(k);
+        if (is_conv(layers_[k].kind)) {
+            const cbx_geom& g = layers_[k].geom;
+            const size_t kd = (size_t)g.inChannels * g.kernelH * g.kernelW;
+            dK_[k] = dmalloc<float>(kd * g.outChannels);
+            dBias_[k] = dmalloc<float>(g.outChannels);
+            // tcgen05 for channels-last inputs in TF32 mode (every conv but a
+            // first layer reading the planar frame).
+            if (precision_ == CBX_PREC_TF32 && k > 0 && tc_supported(g)) tc_[k] = make_tc_layer(g);
+        }
+    }
+    const bool hasClassify = layers_.back().kind == CBX_CLASSIFY;
+    const int fl = nl - 1;
+    lh_ = hasClassify ? dims_[6 * fl + 1] : dims_[6 * fl + 4];
+    lw_ = hasClassify ? dims_[6 * fl + 2] : dims_[6 * fl + 5];
+    const float** tbl = dmalloc<const float*>(2 * (size_t)S);
+    d_cur_ = tbl;
+    d_prev_ = tbl + S;
+    const size_t frame = (size_t)net.inputChannels * net.inputHeight * net.inputWidth * S;
+    for (auto& s : slots_) s = dmalloc<float>(frame);
+    CBX_CUDA(cudaMallocHost(&h_stats_, sizeof(unsigned long long) * 4 * S * nl + 16));
+    last_cb_frames_.assign(S, nullptr);
+    for (int e = 0; e < 2; ++e) {
+        last_stats_[e].assign((size_t)S * nl, cbx_layer_stats{0, 0, 0});
+        last_macs_[e].assign(S, 0);
+    }
+    cb_.reset(new Plan);
+    build_plan(*cb_, false);
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    cb_.reset();
+    base_.reset();
+    tc_.clear();
+    for (float* p : dK_) cudaFree(p);
+    for (float* p : dBias_) cudaFree(p);
+    cudaFree(d_cur_);
+    for (auto& s : slots_) cudaFree(s);
+    cudaFreeHost(h_stats_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+Engine::Plan& Engine::plan(int engine) {
+    if (engine == CBX_ENGINE_CBINFER) return *cb_;
+    if (!base_) {
+        base_.reset(new Plan);
+        build_plan(*base_, true);
+    }
+    return *base_;
+}
+
+void Engine::build_plan(Plan& p, bool baseline) {
+    const int nl = (int)layers_.size(), S = S_;
+    p.baseline = baseline;
+    p.T.assign(nl + 1, TensorView{});
+    p.chg.assign(nl + 1, MaskView{nullptr, 0, 0, 0});
+    p.chg_by_conv.assign(nl + 1, false);
+    p.upd.assign(nl + 1, MaskView{nullptr, 0, 0, 0});
+    p.upd_owner.assign(nl + 1, -2);
+    p.U.assign(nl, MaskView{nullptr, 0, 0, 0});
+    p.idx.assign(nl, nullptr);
+    p.cnt.assign(nl, nullptr);
+    p.idx_src.assign(nl, -1);
+    const bool hasClassify = layers_.back().kind == CBX_CLASSIFY;
+
+    auto consumer_kind = [&](int t) -> int {  // kind of the layer reading tensor t; 4 = final argmax
+        if (t < nl) return layers_[t].kind;
+        return CBX_CLASSIFY;
+    };
+    auto tensor_dims = [&](int t, int& c, int& h, int& w) {
+        if (t == 0) {
+            c = net_.inputChannels;
+            h = net_.inputHeight;
+            w = net_.inputWidth;
+        } else {
+            c = dims_[6 * (t - 1) + 3];
+            h = dims_[6 * (t - 1) + 4];
+            w = dims_[6 * (t - 1) + 5];
+        }
+    };
+    auto alloc_tensor = [&](int t) {
+        int c, h, w;
+        tensor_dims(t, c, h, w);
+        TensorView v{};
+        v.C = c;
+        v.H = h;
+        v.W = w;
+        v.Cp = (int)round_up(c, 4);
+        if (t < nl && is_conv(layers_[t].kind)) {
+            v.hh = layers_[t].geom.padH;
+            v.hw = layers_[t].geom.padW;
+        }
+        v.Hp = h + 2 * v.hh;
+        v.Wp = w + 2 * v.hw;
+        v.ss = round_up((int64_t)v.Hp * v.Wp * v.Cp, 64);
+        v.d = p.alloc<float>((size_t)(v.ss * S));
+        p.T[t] = v;
+    };
+
+    // tensors
+    p.ingest = !is_conv(layers_[0].kind);
+    if (p.ingest) alloc_tensor(0);
+    for (int k = 0; k < nl; ++k) {
+        if (layers_[k].kind == CBX_CLASSIFY) {
+            p.T[k + 1] = p.T[k];
+            continue;
+        }
+        alloc_tensor(k + 1);
+    }
+    if (p.T[0].d == nullptr) {
+        int c, h, w;
+        tensor_dims(0, c, h, w);
+        p.T[0] = TensorView{nullptr, c, h, w, c, h, w, 0, 0, (int64_t)c * h * w};
+    }
+    p.labels = p.alloc<uint16_t>((size_t)S * lh_ * lw_);
+    p.stats = p.alloc<unsigned long long>((size_t)2 * S * nl);
+    if (baseline) return;  // full mode only: no masks, no lists
+
+    // change masks (inputs of CBCONV layers) and updated masks
+    const int nt = hasClassify ? nl : nl + 1;
+    size_t ws = 0;
+    for (int t = 0; t < nt; ++t) {
+        int c, h, w;
+        tensor_dims(t, c, h, w);
+        const int ck = consumer_kind(t);
+        if (ck == CBX_CBCONV) {
+            p.chg[t] = p.mask(S, h, w);
+            p.chg_by_conv[t] = t > 0 && is_conv(layers_[t - 1].kind);
+        } else {
+            if (t == 0) {
+                p.upd[0] = p.mask(S, h, w);
+                p.upd_owner[0] = -1;
+            } else {
+                const int pk = layers_[t - 1].kind;
+                if (is_conv(pk) || pk == CBX_MAXPOOL) {
+                    p.upd_owner[t] = t - 1;
+                } else if (pk == CBX_RELU) {
+                    p.upd_owner[t] = -3;  // alias of the RELU input, resolved below
+                }
+            }
+        }
+    }
+    for (int k = 0; k < nl; ++k) {
+        const auto& l = layers_[k];
+        const int Ho = dims_[6 * k + 4], Wo = dims_[6 * k + 5];
+        if (l.kind == CBX_CBCONV) {
+            p.U[k] = p.mask(S, Ho, Wo);
+        } else if (l.kind == CBX_CONV) {
+            if (!identity_geom(l.geom)) p.U[k] = p.mask(S, Ho, Wo);
+        } else if (l.kind == CBX_MAXPOOL) {
+            if (p.upd_owner[k + 1] == k) p.U[k] = p.mask(S, Ho, Wo);
+        }
+    }
+    // resolve upd aliases in layer order (upd[t] of a RELU output = upd of its input)
+    for (int t = 1; t <= nl; ++t) {
+        if (p.upd_owner[t] == -3) {
+            p.upd_owner[t] = p.upd_owner[t - 1];
+            p.upd[t] = p.upd[t - 1];
+        } else if (p.upd_owner[t] >= 0) {
+            const int k = p.upd_owner[t];
+            if (layers_[k].kind == CBX_CONV && identity_geom(layers_[k].geom)) {
+                p.upd[t] = p.upd[k];  // U of an identity conv is its input's upd
+                p.upd_owner[t] = p.upd_owner[k];
+            } else {
+                p.upd[t] = p.U[k];
+            }
+        }
+    }
+    // index lists
+    for (int k = 0; k < nl; ++k) {
+        const auto& l = layers_[k];
+        if (!is_conv(l.kind)) continue;
+        const int Ho = dims_[6 * k + 4], Wo = dims_[6 * k + 5];
+        if (l.kind == CBX_CONV && identity_geom(l.geom) && p.upd_owner[k] >= 0 &&
+            is_conv(layers_[p.upd_owner[k]].kind)) {
+            const int j = p.upd_owner[k];
+            p.idx_src[k] = p.idx_src[j] >= 0 ? p.idx_src[j] : j;
+            continue;
+        }
+        p.idx[k] = p.alloc<int32_t>((size_t)S * Ho * Wo);
+        p.cnt[k] = p.alloc<int>(1);
+        ws = std::max(ws, compact_workspace_bytes(S, (int64_t)Ho * Wo));
+    }
+    if (ws) p.ws = p.alloc<uint8_t>(ws);
+}
+
+void Engine::record(Plan& p, bool full) {
+    const int nl = (int)layers_.size(), S = S_;
+    cudaStream_t st = stream_;
+    auto stats_of = [&](int layer, int field) { return p.stats + (size_t)layer * S * 2 + field; };
+    if (!full) {
+        CBX_CUDA(cudaMemsetAsync(p.stats, 0, sizeof(unsigned long long) * 2 * S * nl, st));
+        for (int t = 0; t <= nl; ++t)
+            if (p.chg_by_conv[t] && p.chg[t].d)
+                CBX_CUDA(cudaMemsetAsync(p.chg[t].d, 0, (size_t)(p.chg[t].stride * S), st));
+    }
+    // K1: detection on the raw frames
+    if (!full) {
+        const auto& in = p.T[0];
+        if (p.chg[0].d)
+            launch_detect_planar(d_cur_, d_prev_, S, in.C, in.H, in.W, layers_[0].threshold, 0, p.chg[0],
+                                 stats_of(0, 0), 2, st); mark("detect", 0);
+        if (p.upd[0].d && p.upd_owner[0] == -1)
+            launch_detect_planar(d_cur_, d_prev_, S, in.C, in.H, in.W, 0.0f, 1, p.upd[0], nullptr, 2, st); mark("detect_bitwise", 0);
+    }
+    if (p.ingest) {
+        launch_ingest(d_cur_, p.T[0], S, st);
+        mark("ingest", 0);
+    }
+    for (int k = 0; k < nl; ++k) {
+        const auto& l = layers_[k];
+        const bool has_next = k + 1 < nl;
+        MaskView chg_next = (!full && has_next) ? p.chg[k + 1] : MaskView{nullptr, 0, 0, 0};
+        const float tau_next = has_next ? layers_[k + 1].threshold : 0.0f;
+        unsigned long long* cnt_next = has_next ? stats_of(k + 1, 0) : nullptr;
+        switch (l.kind) {
+            case CBX_CBCONV:
+            case CBX_CONV: {
+                const cbx_geom& g = l.geom;
+                const int32_t* idx = nullptr;
+                const int* count = nullptr;
+                if (!full) {
+                    if (l.kind == CBX_CBCONV) {
+                        launch_dilate(p.chg[k], p.U[k], S, g.kernelH, g.kernelW, g.strideH, g.strideW, g.padH, g.padW, st); mark("dilate", k);
+                        launch_compact(p.U[k], S, p.idx[k], p.cnt[k], p.ws, stats_of(k, 1), 2, st); mark("compact", k);
+                    } else if (p.idx_src[k] < 0) {
+                        if (identity_geom(g)) {
+                            launch_compact(p.upd[k], S, p.idx[k], p.cnt[k], p.ws, nullptr, 2, st); mark("compact", k);
+                        } else {
+                            launch_dilate(p.upd[k], p.U[k], S, g.kernelH, g.kernelW, g.strideH, g.strideW, g.padH, g.padW, st); mark("dilate", k);
+                            launch_compact(p.U[k], S, p.idx[k], p.cnt[k], p.ws, nullptr, 2, st); mark("compact", k);
+                        }
+                    }
+                    const int src = p.idx_src[k] >= 0 ? p.idx_src[k] : k;
+                    idx = p.idx[src];
+                    count = p.cnt[src];
+                }
+                const bool planar_in = (k == 0 && !p.ingest);
+                const bool relu = l.kind == CBX_CBCONV && l.fuseRelu;
+                const int64_t full_count = (int64_t)S * dims_[6 * k + 4] * dims_[6 * k + 5];
+                if (tc_[k] && !planar_in) {
+                    launch_conv_tc(*tc_[k], p.T[k], p.T[k + 1], dBias_[k], idx, count, full_count, relu,
+                                   chg_next, tau_next, cnt_next, 2, S, st);
+                    mark("conv_tc", k);
+                } else {
+                    ConvArgs a{};
+                    a.in = p.T[k];
+                    a.in_ptrs = planar_in ? d_cur_ : nullptr;
+                    a.out = p.T[k + 1];
+                    a.K = dK_[k];
+                    a.bias = dBias_[k];
+                    a.kh = g.kernelH;
+                    a.kw = g.kernelW;
+                    a.sh = g.strideH;
+                    a.sw = g.strideW;
+                    a.ph = g.padH;
+                    a.pw = g.padW;
+                    a.idx = idx;
+                    a.count = count;
+                    a.full_count = full_count;
+                    a.relu = relu;
+                    a.chg = chg_next;
+                    a.tau = tau_next;
+                    a.chg_cnt = cnt_next;
+                    a.cnt_stride = 2;
+                    a.S = S;
+                    launch_conv_exact(a, st); mark("conv_exact", k);
+                }
+                break;
+            }
+            case CBX_RELU: {
+                PointArgs a{};
+                a.in = p.T[k];
+                a.out = p.T[k + 1];
+                a.upd = full ? nullptr : p.upd[k].d;
+                a.upd_stride = p.upd[k].stride;
+                a.chg = chg_next;
+                a.tau = tau_next;
+                a.chg_cnt = cnt_next;
+                a.cnt_stride = 2;
+                a.S = S;
+                launch_relu(a, st); mark("relu", k);
+                break;
+            }
+            case CBX_MAXPOOL: {
+                PoolArgs a{};
+                a.in = p.T[k];
+                a.out = p.T[k + 1];
+                a.window = l.window;
+                a.stride = l.stride;
+                a.upd_in = full ? nullptr : p.upd[k].d;
+                a.upd_in_stride = p.upd[k].stride;
+                a.upd_out = full ? nullptr : p.U[k].d;
+                a.upd_out_stride = p.U[k].stride;
+                a.chg = chg_next;
+                a.tau = tau_next;
+                a.chg_cnt = cnt_next;
+                a.cnt_stride = 2;
+                a.S = S;
+                launch_pool(a, st); mark("pool", k);
+                break;
+            }
+            case CBX_CLASSIFY: {
+                PointArgs a{};
+                a.in = p.T[k];
+                a.upd = full ? nullptr : p.upd[k].d;
+                a.upd_stride = p.upd[k].stride;
+                a.labels = p.labels;
+                a.S = S;
+                launch_classify(a, st);
+                mark("classify", k);
+                break;
+            }
+        }
+    }
+    if (layers_.back().kind != CBX_CLASSIFY) {
+        PointArgs a{};
+        a.in = p.T[nl];
+        a.upd = full ? nullptr : p.upd[nl].d;
+        a.upd_stride = p.upd[nl].stride;
+        a.labels = p.labels;
+        a.S = S;
+        launch_classify(a, st);
+        mark("classify", nl);
+    }
+    CBX_CUDA(cudaGetLastError());
+}
+
+void Engine::launch(Plan& p, bool full) {
+    const int m = full ? 1 : 0;
+    if (p.dirty) {
+        for (auto& g : p.gexec)
+            if (g) {
+                cudaGraphExecDestroy(g);
+                g = nullptr;
+            }
+        p.dirty = false;
+    }
+    if (!p.gexec[m]) {
+        cudaGraph_t graph = nullptr;
+        CBX_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+        try {
+            record(p, full);
+        } catch (...) {
+            cudaStreamEndCapture(stream_, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        CBX_CUDA(cudaStreamEndCapture(stream_, &graph));
+        size_t n = 0;
+        CBX_CUDA(cudaGraphGetNodes(graph, nullptr, &n));
+        std::vector<cudaGraphNode_t> nodes(n);
+        if (n) CBX_CUDA(cudaGraphGetNodes(graph, nodes.data(), &n));
+        int kernels = 0;
+        for (auto nd : nodes) {
+            cudaGraphNodeType t;
+            CBX_CUDA(cudaGraphNodeGetType(nd, &t));
+            kernels += t == cudaGraphNodeTypeKernel;
+        }
+        p.launches[m] = kernels;
+        CBX_CUDA(cudaGraphInstantiate(&p.gexec[m], graph, 0));
+        cudaGraphDestroy(graph);
+    }
+    CBX_CUDA(cudaGraphLaunch(p.gexec[m], stream_));
+    last_launches_ = p.launches[m];
+}
+
+void Engine::stage_frame_pointers(int engine, const float* const* cur, const float* const* prev) {
+    (void)engine;
+    std::vector<const float*> tbl(2 * (size_t)S_);
+    for (int s = 0; s < S_; ++s) {
+        tbl[s] = cur[s];
+        tbl[S_ + s] = prev ? prev[s] : cur[s];
+    }
+    // pageable source: staged by the driver before return, safe to reuse
+    CBX_CUDA(cudaMemcpyAsync(d_cur_, tbl.data(), sizeof(const float*) * 2 * S_, cudaMemcpyHostToDevice, stream_));
+}
+
+void Engine::forward_host(int engine, const float* frames, uint16_t* labels, cbx_layer_stats* stats,
+                          uint64_t* macs) {
+    if (!frames) throw Error(CBX_E_ARG, "frames is null");
+    CBX_CUDA(cudaSetDevice(device_));
+    const size_t per = (size_t)net_.inputChannels * net_.inputHeight * net_.inputWidth;
+    float* slot = engine == CBX_ENGINE_CBINFER ? slots_[parity_] : slots_[2];
+    CBX_CUDA(cudaMemcpyAsync(slot, frames, per * S_ * sizeof(float), cudaMemcpyHostToDevice, stream_));
+    std::vector<const float*> cur(S_);
+    for (int s = 0; s < S_; ++s) cur[s] = slot + per * s;
+    forward_device(engine, cur.data());
+    if (engine == CBX_ENGINE_CBINFER) parity_ ^= 1;
+    if (labels) read_labels(engine, labels);
+    read_stats(engine, stats, macs);
+}
+
+void Engine::forward_device(int engine, const float* const* frames_dev) {
+    if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
+    if (!frames_dev) throw Error(CBX_E_ARG, "frames is null");
+    CBX_CUDA(cudaSetDevice(device_));
+    Plan& p = plan(engine);
+    const bool full = engine == CBX_ENGINE_BASELINE || !has_history_;
+    stage_frame_pointers(engine, frames_dev, engine == CBX_ENGINE_CBINFER && has_history_ ? last_cb_frames_.data() : nullptr);
+    launch(p, full);
+    const int nl = (int)layers_.size();
+    CBX_CUDA(cudaMemcpyAsync(h_stats_ + (size_t)engine * 2 * S_ * nl, p.stats, sizeof(unsigned long long) * 2 * S_ * nl,
+                             cudaMemcpyDeviceToHost, stream_));
+    last_full_[engine] = full;
+    if (engine == CBX_ENGINE_CBINFER) {
+        has_history_ = true;
+        last_cb_frames_.assign(frames_dev, frames_dev + S_);
+    }
+    pending_engine_ = engine;
+}
+
+void Engine::sync() { CBX_CUDA(cudaStreamSynchronize(stream_)); }
+
+void Engine::finish_stats(Plan& p, bool full, int engine) {
+    (void)p;
+    const int nl = (int)layers_.size();
+    const unsigned long long* hs = h_stats_ + (size_t)engine * 2 * S_ * nl;
+    auto& out = last_stats_[engine];
+    auto& macs = last_macs_[engine];
+    for (int s = 0; s < S_; ++s) {
+        uint64_t total = 0;
+        for (int k = 0; k < nl; ++k) {
+            const auto& l = layers_[k];
+            cbx_layer_stats st{0, 0, 0};
+            const int64_t inHW = (int64_t)dims_[6 * k + 1] * dims_[6 * k + 2];
+            const int64_t outHW = (int64_t)dims_[6 * k + 4] * dims_[6 * k + 5];
+            if (is_conv(l.kind)) {
+                const uint64_t rc = (uint64_t)l.geom.outChannels * l.geom.inChannels * l.geom.kernelH * l.geom.kernelW;
+                if (l.kind == CBX_CBCONV && engine == CBX_ENGINE_CBINFER) {
+                    if (full) {
+                        st.changedInputPixels = inHW;
+                        st.changedOutputPixels = outHW;
+                    } else {
+                        st.changedInputPixels = (int64_t)hs[((size_t)k * S_ + s) * 2 + 0];
+                        st.changedOutputPixels = (int64_t)hs[((size_t)k * S_ + s) * 2 + 1];
+                    }
+                    st.gemmMacs = rc * (uint64_t)st.changedOutputPixels;
+                } else {
+                    st.changedOutputPixels = outHW;
+                    st.gemmMacs = rc * (uint64_t)outHW;
+                }
+            }
+            out[(size_t)s * nl + k] = st;
+            total += st.gemmMacs;
+        }
+        macs[s] = total;
+    }
+}
+
+void Engine::read_stats(int engine, cbx_layer_stats* stats, uint64_t* macs) {
+    sync();
+    if (pending_engine_ == engine) {
+        finish_stats(plan(engine), last_full_[engine], engine);
+        pending_engine_ = -1;
+    }
+    const int nl = (int)layers_.size();
+    if (stats) std::memcpy(stats, last_stats_[engine].data(), sizeof(cbx_layer_stats) * S_ * nl);
+    if (macs) std::memcpy(macs, last_macs_[engine].data(), sizeof(uint64_t) * S_);
+}
+
+void Engine::read_labels(int engine, uint16_t* labels) {
+    Plan& p = plan(engine);
+    CBX_CUDA(cudaMemcpyAsync(labels, p.labels, sizeof(uint16_t) * S_ * lh_ * lw_, cudaMemcpyDeviceToHost, stream_));
+    sync();
+}
+
+const uint16_t* Engine::labels_device(int engine) { return plan(engine).labels; }
+
+void Engine::load_layer(int layer, const float* K, const float* bias) {
+    if (layer < 0 || layer >= (int)layers_.size() || !is_conv(layers_[layer].kind))
+        throw Error(CBX_E_SPEC, "layer " + std::to_string(layer + 1) + " has no filters");
+    if (!K || !bias) throw Error(CBX_E_ARG, "null weights");
+    const cbx_geom& g = layers_[layer].geom;
+    const size_t kd = (size_t)g.inChannels * g.kernelH * g.kernelW;
+    for (size_t i = 0; i < kd * g.outChannels; ++i)
+        if (!std::isfinite(K[i])) throw Error(CBX_E_IO, where(layer, layers_[layer].kind) + ": non-finite weight");
+    for (int i = 0; i < g.outChannels; ++i)
+        if (!std::isfinite(bias[i])) throw Error(CBX_E_IO, where(layer, layers_[layer].kind) + ": non-finite bias");
+    CBX_CUDA(cudaSetDevice(device_));
+    CBX_CUDA(cudaMemcpy(dK_[layer], K, kd * g.outChannels * sizeof(float), cudaMemcpyHostToDevice));
+    CBX_CUDA(cudaMemcpy(dBias_[layer], bias, g.outChannels * sizeof(float), cudaMemcpyHostToDevice));
+    if (tc_[layer]) tc_load_weights(*tc_[layer], K, stream_);
+    CBX_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::set_thresholds(const float* taus, int n) {
+    if (n != (int)cb_layers_.size())
+        throw Error(CBX_E_SPEC, "expected " + std::to_string(cb_layers_.size()) + " thresholds, got " + std::to_string(n));
+    for (int k = 0; k < n; ++k)
+        if (!(taus[k] >= 0.0f)) throw Error(CBX_E_SPEC, "negative threshold");
+    for (int k = 0; k < n; ++k) layers_[cb_layers_[k]].threshold = taus[k];
+    cb_->dirty = true;
+}
+
+void Engine::get_thresholds(float* taus, int n) const {
+    for (int k = 0; k < n && k < (int)cb_layers_.size(); ++k) taus[k] = layers_[cb_layers_[k]].threshold;
+}
+
+void Engine::reset() { has_history_ = false; }
+
+void Engine::get_activation(int engine, int layer, int s, float* out) {
+    if (layer < 0 || layer >= (int)layers_.size() || s < 0 || s >= S_) throw Error(CBX_E_BOUNDS, "layer/stream out of range");
+    if (layers_[layer].kind == CBX_CLASSIFY) throw Error(CBX_E_SPEC, "CLASSIFY produces labels, not an activation");
+    Plan& p = plan(engine);
+    const TensorView& t = p.T[layer + 1];
+    const size_t n = (size_t)t.C * t.H * t.W;
+    float* tmp = nullptr;
+    CBX_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), stream_));
+    launch_hwc_to_chw(t, s, tmp, stream_);
+    CBX_CUDA(cudaMemcpyAsync(out, tmp, n * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+    CBX_CUDA(cudaFreeAsync(tmp, stream_));
+    sync();
+}
+
+void Engine::get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64_t* n, int* first) {
+    if (cb < 0 || cb >= (int)cb_layers_.size() || s < 0 || s >= S_) throw Error(CBX_E_BOUNDS, "trace index out of range");
+    const int k = cb_layers_[cb];
+    Plan& p = *cb_;
+    const int H = dims_[6 * k + 1], W = dims_[6 * k + 2];
+    const int64_t N = (int64_t)dims_[6 * k + 4] * dims_[6 * k + 5];
+    sync();
+    const bool full = last_full_[CBX_ENGINE_CBINFER];
+    if (first) *first = full;
+    if (detected) {
+        if (full)
+            std::memset(detected, 0, (size_t)H * W);
+        else
+            CBX_CUDA(cudaMemcpy(detected, p.chg[k].d + (int64_t)s * p.chg[k].stride, (size_t)H * W, cudaMemcpyDeviceToHost));
+    }
+    if (full) {
+        if (updated)
+            for (int64_t i = 0; i < N; ++i) updated[i] = (int32_t)i;
+        if (n) *n = N;
+        return;
+    }
+    int total = 0;
+    CBX_CUDA(cudaMemcpy(&total, p.cnt[k], sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> all(total);
+    if (total) CBX_CUDA(cudaMemcpy(all.data(), p.idx[k], sizeof(int32_t) * total, cudaMemcpyDeviceToHost));
+    int64_t m = 0;
+    for (int32_t g : all)
+        if (g >= s * N && g < (s + 1) * N) {
+            if (updated) updated[m] = (int32_t)(g - s * N);
+            ++m;
+        }
+    if (n) *n = m;
+}
+
+}  // namespace cbx
+
+namespace cbx {
+
+void Engine::mark(const char* name, int layer) {
+    if (!prof_) return;
+    cudaEvent_t e;
+    CBX_CUDA(cudaEventCreate(&e));
+    CBX_CUDA(cudaEventRecord(e, stream_));
+    prof_->push_back(ProfMark{name, layer, e});
+}
+
+// One forward without the graph, each kernel bracketed by CUDA events on the
+// context stream (the stream every kernel is launched on). Advances the state
+// exactly like forward_device.
+void Engine::profile(int engine, const float* const* frames_dev, std::vector<cbx_kernel_time>& out) {
+    if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
+    CBX_CUDA(cudaSetDevice(device_));
+    Plan& p = plan(engine);
+    const bool full = engine == CBX_ENGINE_BASELINE || !has_history_;
+    stage_frame_pointers(engine, frames_dev, engine == CBX_ENGINE_CBINFER && has_history_ ? last_cb_frames_.data() : nullptr);
+    std::vector<ProfMark> marks;
+    prof_ = &marks;
+    try {
+        mark("start", -1);
+        record(p, full);
+    } catch (...) {
+        prof_ = nullptr;
+        throw;
+    }
+    prof_ = nullptr;
+    const int nl = (int)layers_.size();
+    CBX_CUDA(cudaMemcpyAsync(h_stats_ + (size_t)engine * 2 * S_ * nl, p.stats, sizeof(unsigned long long) * 2 * S_ * nl,
+                             cudaMemcpyDeviceToHost, stream_));
+    sync();
+    out.clear();
+    for (size_t i = 1; i < marks.size(); ++i) {
+        float ms = 0;
+        CBX_CUDA(cudaEventElapsedTime(&ms, marks[i - 1].ev, marks[i].ev));
+        cbx_kernel_time t{};
+        std::snprintf(t.name, sizeof(t.name), "%s", marks[i].name.c_str());
+        t.layer = marks[i].layer;
+        t.ms = ms;
+        out.push_back(t);
+    }
+    for (auto& m : marks) cudaEventDestroy(m.ev);
+    last_full_[engine] = full;
+    pending_engine_ = engine;
+    if (engine == CBX_ENGINE_CBINFER) {
+        has_history_ = true;
+        last_cb_frames_.assign(frames_dev, frames_dev + S_);
+    }
+}
+
+}  // namespace cbx

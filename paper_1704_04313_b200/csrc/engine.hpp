@@ -1,0 +1,118 @@
+// engine.hpp -- per-network device runtime behind the C-ABI (include/cbx.h).
+//
+// One Engine = one reference `Network` (network.hpp:54-68) replicated over S
+// independent camera streams on one device. It owns the persistent per-layer
+// state (channels-last activations with zero halos, change masks, index
+// lists), captures the whole frame as a CUDA graph, and reproduces
+// forward_frame (network.cpp:252-315) with every CBCONV evaluated by the
+// change-based pipeline and every other layer updated incrementally over the
+// pixels its input actually changed (exact: unchanged inputs give bitwise
+// unchanged outputs, so the full-frame recomputation of the reference is
+// reproduced without re-running it).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cbx.h"
+#include "common.cuh"
+#include "conv_tc.hpp"
+
+namespace cbx {
+
+// Error carrying a cbx_status (mapped 1:1 to the reference exceptions).
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define CBX_CUDA(x) ::cbx::cuda_check((x), #x)
+
+
+// chain_dims (network.cpp:128-188)
+std::vector<int> chain_dims(const cbx_net_desc& net, std::vector<cbx_layer_desc>& layers);
+
+class Engine {
+public:
+    Engine(const cbx_net_desc& net, int device, int S, int precision);
+    ~Engine();
+
+    void load_layer(int layer, const float* K, const float* bias);
+    void set_thresholds(const float* taus, int n);
+    void get_thresholds(float* taus, int n) const;
+    void reset();
+
+    // frames: host S*C*H*W floats (pinned or pageable)
+    void forward_host(int engine, const float* frames, uint16_t* labels, cbx_layer_stats* stats,
+                      uint64_t* macs);
+    void forward_device(int engine, const float* const* frames_dev);
+    void sync();
+    void read_labels(int engine, uint16_t* labels);
+    void read_stats(int engine, cbx_layer_stats* stats, uint64_t* macs);
+    const uint16_t* labels_device(int engine);
+    void get_activation(int engine, int layer, int s, float* out);
+    void get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64_t* n, int* first);
+
+    void profile(int engine, const float* const* frames_dev, std::vector<cbx_kernel_time>& out);
+
+    cudaStream_t stream() const { return stream_; }
+    int last_launch_count() const { return last_launches_; }
+    int num_layers() const { return (int)layers_.size(); }
+    int label_h() const { return lh_; }
+    int label_w() const { return lw_; }
+
+private:
+    struct Plan;
+    Plan& plan(int engine);
+    void build_plan(Plan& p, bool baseline);
+    void record(Plan& p, bool full);
+    void launch(Plan& p, bool full);
+    void stage_frame_pointers(int engine, const float* const* cur, const float* const* prev);
+    void finish_stats(Plan& p, bool full, int engine);
+    void mark(const char* name, int layer);
+
+    struct ProfMark {
+        std::string name;
+        int layer;
+        cudaEvent_t ev;
+    };
+    std::vector<ProfMark>* prof_ = nullptr;
+
+    int device_, S_, precision_;
+    cbx_net_desc net_{};
+    std::vector<cbx_layer_desc> layers_;
+    std::vector<int> dims_;  // 6 per layer
+    std::vector<int> cb_layers_;
+    int lh_ = 0, lw_ = 0;
+    cudaStream_t stream_ = nullptr;
+
+    // weights (reference layout), per layer
+    std::vector<float*> dK_, dBias_;
+    std::vector<std::unique_ptr<TcLayer, TcLayerDeleter>> tc_;
+
+    std::unique_ptr<Plan> cb_, base_;
+    bool has_history_ = false;
+
+    // frame pointer tables (device) and host copies
+    const float** d_cur_ = nullptr;
+    const float** d_prev_ = nullptr;
+    std::vector<const float*> last_cb_frames_;
+    // host-input staging slots: CB ping-pong + baseline
+    float* slots_[3] = {nullptr, nullptr, nullptr};
+    int parity_ = 0;
+
+    // host stats of the last forward, per engine
+    std::vector<cbx_layer_stats> last_stats_[2];
+    std::vector<uint64_t> last_macs_[2];
+    unsigned long long* h_stats_ = nullptr;  // pinned mirror, [engine][nl][S][2]
+    int pending_engine_ = -1;
+    int last_launches_ = 0;
+    bool last_full_[2] = {true, true};
+};
+
+}  // namespace cbx

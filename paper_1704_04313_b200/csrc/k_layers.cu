@@ -1,0 +1,319 @@
+// k_layers.cu -- exact-fp32 gathered convolution, incremental max-pool /
+// ReLU / classification updates over the updated-pixel sets, layout helpers.
+//
+//   conv_exact  <- gen_x_reduced + gemm + update_output
+//                  (/root/reference/proj/core/src/cbconv.cpp:115-155,
+//                   baseline.cpp:9-31,47-63): accumulator starts at the bias,
+//                  adds K(o,r)*x(r) for ascending r in (c,kj,ki) order with one
+//                  rounding per multiply and per add -> bitwise equal to the
+//                  reference. Used for the planar first layer in every mode
+//                  and for every layer in CBX_PREC_EXACT.
+//   pool        <- maxpool (baseline.cpp:119-145), recomputed only for windows
+//                  touched by the producer's updated set, fused with the
+//                  consumer's change detection (detect_changes, cbconv.cpp:57-71)
+//                  by comparing against the value it overwrites.
+//   relu        <- relu (baseline.cpp:113-117), same in-place scheme.
+//   classify    <- argmax_classify (baseline.cpp:147-163).
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace cbx {
+
+constexpr int kConvThreads = 128, kConvOC = 16, kConvKC = 128;
+
+template <bool PLANAR>
+__global__ void __launch_bounds__(kConvThreads) conv_exact_kernel(ConvArgs a) {
+    __shared__ float sW[kConvOC][kConvKC];
+    const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
+    const int64_t ntiles = (total + kConvThreads - 1) / kConvThreads;
+    const int Ho = a.out.H, Wo = a.out.W, O = a.out.C;
+    const int64_t HoWo = (int64_t)Ho * Wo;
+    const int khw = a.kh * a.kw;
+    const int Kdim = a.in.C * khw;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t n = tile * kConvThreads + threadIdx.x;
+        const bool valid = n < total;
+        const int64_t g = valid ? (a.idx ? (int64_t)a.idx[n] : n) : 0;
+        const int s = (int)(g / HoWo);
+        const int p = (int)(g - (int64_t)s * HoWo);
+        const int y = p / Wo, x = p - (p / Wo) * Wo;
+        const int y0 = y * a.sh - a.ph, x0 = x * a.sw - a.pw;
+        const float* src;
+        if (PLANAR) {
+            src = a.in_ptrs[s];
+        } else {
+            src = a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y0 + a.in.hh) * a.in.Wp + (x0 + a.in.hw)) * a.in.Cp;
+        }
+        float* dst = a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + (x + a.out.hw)) * a.out.Cp;
+        bool changed = false;
+        for (int o0 = 0; o0 < O; o0 += kConvOC) {
+            float acc[kConvOC];
+#pragma unroll
+            for (int j = 0; j < kConvOC; ++j) acc[j] = (o0 + j < O) ? a.bias[o0 + j] : 0.0f;
+            for (int r0 = 0; r0 < Kdim; r0 += kConvKC) {
+                __syncthreads();
+                for (int t = threadIdx.x; t < kConvOC * kConvKC; t += kConvThreads) {
+                    const int j = t / kConvKC, r = t - j * kConvKC;
+                    sW[j][r] = (o0 + j < O && r0 + r < Kdim) ? a.K[(int64_t)(o0 + j) * Kdim + r0 + r] : 0.0f;
+                }
+                __syncthreads();
+                if (!valid) continue;
+                const int r1 = min(r0 + kConvKC, Kdim);
+                int c = r0 / khw;
+                int rem = r0 - c * khw;
+                int kj = rem / a.kw;
+                int ki = rem - kj * a.kw;
+                for (int r = r0; r < r1; ++r) {
+                    float v;
+                    if (PLANAR) {
+                        const int yy = y0 + kj, xx = x0 + ki;
+                        v = (yy >= 0 && yy < a.in.H && xx >= 0 && xx < a.in.W)
+                                ? __ldg(src + ((int64_t)c * a.in.H + yy) * a.in.W + xx)
+                                : 0.0f;
+                    } else {
+                        v = __ldg(src + ((int64_t)kj * a.in.Wp + ki) * a.in.Cp + c);
+                    }
+#pragma unroll
+                    for (int j = 0; j < kConvOC; ++j) acc[j] = __fadd_rn(acc[j], __fmul_rn(sW[j][r - r0], v));
+                    if (++ki == a.kw) {
+                        ki = 0;
+                        if (++kj == a.kh) {
+                            kj = 0;
+                            ++c;
+                        }
+                    }
+                }
+            }
+            if (valid) {
+#pragma unroll
+                for (int j = 0; j < kConvOC; ++j) {
+                    if (o0 + j >= O) break;
+                    const float v = a.relu ? ref_relu(acc[j]) : acc[j];
+                    if (a.chg.d) changed |= ref_changed(v, dst[o0 + j], a.tau);
+                    dst[o0 + j] = v;
+                }
+            }
+        }
+        if (a.chg.d) {
+            if (valid && changed) a.chg.d[(int64_t)s * a.chg.stride + p] = 1;
+            if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
+        }
+    }
+}
+
+void launch_conv_exact(const ConvArgs& a, cudaStream_t st) {
+    const int64_t max_tiles = (a.full_count + kConvThreads - 1) / kConvThreads;
+    int grid = (int)std::min<int64_t>(max_tiles, (int64_t)kNumSMs * 8);
+    if (grid < 1) grid = 1;
+    if (a.in_ptrs)
+        conv_exact_kernel<true><<<grid, kConvThreads, 0, st>>>(a);
+    else
+        conv_exact_kernel<false><<<grid, kConvThreads, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float4 max4(float4 m, float4 v) {
+    return make_float4(ref_max(m.x, v.x), ref_max(m.y, v.y), ref_max(m.z, v.z), ref_max(m.w, v.w));
+}
+__device__ __forceinline__ bool changed4(float4 a, float4 b, float tau) {
+    return ref_changed(a.x, b.x, tau) | ref_changed(a.y, b.y, tau) | ref_changed(a.z, b.z, tau) |
+           ref_changed(a.w, b.w, tau);
+}
+
+__global__ void __launch_bounds__(256) pool_kernel(PoolArgs a) {
+    const int Ho = a.out.H, Wo = a.out.W, W = a.in.W;
+    const int64_t HoWo = (int64_t)Ho * Wo, total = HoWo * a.S;
+    const int c4n = a.in.Cp / 4;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const bool act = i < total;
+        int s = 0, p = 0;
+        bool touched = false, changed = false;
+        if (act) {
+            s = (int)(i / HoWo);
+            p = (int)(i - (int64_t)s * HoWo);
+            const int y = p / Wo, x = p - (p / Wo) * Wo;
+            if (a.upd_in) {
+                const uint8_t* u = a.upd_in + (int64_t)s * a.upd_in_stride;
+                for (int kj = 0; kj < a.window && !touched; ++kj)
+                    for (int ki = 0; ki < a.window; ++ki)
+                        if (u[(int64_t)(y * a.stride + kj) * W + x * a.stride + ki]) {
+                            touched = true;
+                            break;
+                        }
+            } else {
+                touched = true;
+            }
+            if (touched) {
+                const float4* src = reinterpret_cast<const float4*>(
+                    a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp);
+                float4* dst = reinterpret_cast<float4*>(
+                    a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp);
+                const int rowq = a.in.Wp * c4n;
+                for (int c4 = 0; c4 < c4n; ++c4) {
+                    float4 m = src[c4];
+                    for (int kj = 0; kj < a.window; ++kj)
+                        for (int ki = 0; ki < a.window; ++ki) m = max4(m, src[kj * rowq + ki * c4n + c4]);
+                    if (a.chg.d) changed |= changed4(m, dst[c4], a.tau);
+                    dst[c4] = m;
+                }
+            }
+            if (a.upd_out) a.upd_out[(int64_t)s * a.upd_out_stride + p] = touched;
+            if (a.chg.d) a.chg.d[(int64_t)s * a.chg.stride + p] = changed;
+        }
+        if (a.chg.d && a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, act);
+    }
+}
+
+void launch_pool(const PoolArgs& a, cudaStream_t st) {
+    const int64_t total = (int64_t)a.out.H * a.out.W * a.S;
+    int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
+    pool_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(a);
+}
+
+__global__ void __launch_bounds__(256) relu_kernel(PointArgs a) {
+    const int H = a.in.H, W = a.in.W;
+    const int64_t HW = (int64_t)H * W, total = HW * a.S;
+    const int c4n = a.in.Cp / 4;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const bool act = i < total;
+        int s = 0;
+        bool changed = false;
+        if (act) {
+            s = (int)(i / HW);
+            const int p = (int)(i - (int64_t)s * HW);
+            const bool u = a.upd ? a.upd[(int64_t)s * a.upd_stride + p] != 0 : true;
+            if (u) {
+                const int y = p / W, x = p - (p / W) * W;
+                const float4* src = reinterpret_cast<const float4*>(
+                    a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y + a.in.hh) * a.in.Wp + x + a.in.hw) * a.in.Cp);
+                float4* dst = reinterpret_cast<float4*>(
+                    a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp);
+                for (int c4 = 0; c4 < c4n; ++c4) {
+                    const float4 v = src[c4];
+                    const float4 r = make_float4(ref_relu(v.x), ref_relu(v.y), ref_relu(v.z), ref_relu(v.w));
+                    if (a.chg.d) changed |= changed4(r, dst[c4], a.tau);
+                    dst[c4] = r;
+                }
+            }
+            if (a.chg.d) a.chg.d[(int64_t)s * a.chg.stride + p] = changed;
+        }
+        if (a.chg.d && a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, act);
+    }
+}
+
+void launch_relu(const PointArgs& a, cudaStream_t st) {
+    const int64_t total = (int64_t)a.in.H * a.in.W * a.S;
+    int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
+    relu_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(a);
+}
+
+__global__ void __launch_bounds__(256) classify_kernel(PointArgs a) {
+    const int H = a.in.H, W = a.in.W;
+    const int64_t HW = (int64_t)H * W, total = HW * a.S;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(i / HW);
+        const int p = (int)(i - (int64_t)s * HW);
+        if (a.upd && !a.upd[(int64_t)s * a.upd_stride + p]) continue;
+        const int y = p / W, x = p - (p / W) * W;
+        const float* src = a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y + a.in.hh) * a.in.Wp + x + a.in.hw) * a.in.Cp;
+        int best = 0;
+        float bv = src[0];
+        for (int c = 1; c < a.in.C; ++c) {
+            const float v = src[c];
+            if (v > bv) {
+                bv = v;
+                best = c;
+            }
+        }
+        a.labels[i] = (uint16_t)best;
+    }
+}
+
+void launch_classify(const PointArgs& a, cudaStream_t st) {
+    const int64_t total = (int64_t)a.in.H * a.in.W * a.S;
+    int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
+    classify_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void hwc_to_chw_kernel(TensorView t, int s, float* out) {
+    const int64_t n = (int64_t)t.C * t.H * t.W;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i / ((int64_t)t.H * t.W));
+        const int64_t p = i - (int64_t)c * t.H * t.W;
+        const int y = (int)(p / t.W), x = (int)(p - (p / t.W) * t.W);
+        out[i] = t.d[(int64_t)s * t.ss + ((int64_t)(y + t.hh) * t.Wp + x + t.hw) * t.Cp + c];
+    }
+}
+
+void launch_hwc_to_chw(TensorView t, int s, float* out, cudaStream_t st) {
+    const int64_t n = (int64_t)t.C * t.H * t.W;
+    int grid = (int)std::min<int64_t>((n + 255) / 256, 4096);
+    hwc_to_chw_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(t, s, out);
+}
+
+__global__ void chw_to_hwc_kernel(const float* in, TensorView t, int s) {
+    const int64_t n = (int64_t)t.C * t.H * t.W;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i / ((int64_t)t.H * t.W));
+        const int64_t p = i - (int64_t)c * t.H * t.W;
+        const int y = (int)(p / t.W), x = (int)(p - (p / t.W) * t.W);
+        t.d[(int64_t)s * t.ss + ((int64_t)(y + t.hh) * t.Wp + x + t.hw) * t.Cp + c] = in[i];
+    }
+}
+
+void launch_chw_to_hwc(const float* in, TensorView t, int s, cudaStream_t st) {
+    const int64_t n = (int64_t)t.C * t.H * t.W;
+    int grid = (int)std::min<int64_t>((n + 255) / 256, 4096);
+    chw_to_hwc_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(in, t, s);
+}
+
+// ---------------------------------------------------------------------------
+// On-device synthetic frame (synth_frame, synth.cpp:60-91, noise-free):
+// background 0.2 + 0.25*((31i+17j+47c) mod 101)/100, then sprites in order.
+__global__ void synth_kernel(float* out, int C, int H, int W, const SpriteRect* rects, int n) {
+    const int64_t total = (int64_t)C * H * W;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(k / ((int64_t)H * W));
+        const int64_t p = k - (int64_t)c * H * W;
+        const int j = (int)(p / W), i = (int)(p - (int64_t)j * W);
+        const unsigned v = (unsigned)(i * 31 + j * 17 + c * 47) % 101u;
+        float val = __fadd_rn(0.2f, __fmul_rn(0.25f, __fdiv_rn((float)v, 100.0f)));
+        for (int r = 0; r < n; ++r)
+            if (j >= rects[r].y0 && j < rects[r].y1 && i >= rects[r].x0 && i < rects[r].x1) val = rects[r].v;
+        out[k] = val;
+    }
+}
+
+void launch_synth_frame(float* out, int C, int H, int W, const SpriteRect* rects_dev, int n,
+                        cudaStream_t st) {
+    const int64_t total = (int64_t)C * H * W;
+    int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
+    synth_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(out, C, H, W, rects_dev, n);
+}
+
+}  // namespace cbx
+
+namespace cbx {
+
+__global__ void ingest_kernel(const float* const* frames, TensorView t) {
+    const int s = blockIdx.y;
+    const float* src = frames[s];
+    const int64_t HW = (int64_t)t.H * t.W, n = HW * t.C;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i / HW);
+        const int64_t p = i - (int64_t)c * HW;
+        const int y = (int)(p / t.W), x = (int)(p - (p / t.W) * t.W);
+        t.d[(int64_t)s * t.ss + ((int64_t)(y + t.hh) * t.Wp + x + t.hw) * t.Cp + c] = src[i];
+    }
+}
+
+void launch_ingest(const float* const* frames, TensorView t, int S, cudaStream_t st) {
+    const int64_t n = (int64_t)t.C * t.H * t.W;
+    int gx = (int)std::min<int64_t>((n + 255) / 256, 1024);
+    ingest_kernel<<<dim3(gx < 1 ? 1 : gx, S), 256, 0, st>>>(frames, t);
+}
+
+}  // namespace cbx

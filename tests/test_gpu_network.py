@@ -1,0 +1,177 @@
+"""GPU: network-level parity of the CUDA engine (through the C-ABI) with the
+oracle restatement, which is itself pinned to the reference (test_oracle.py).
+
+Exact mode (CBX_PREC_EXACT) must be BIT-EXACT in everything: labels, stats,
+every layer's activation, change masks and index lists. TF32 mode (tcgen05)
+keeps layer-1 masks/indices/outputs bit-exact and stays within the stated
+tolerance elsewhere (max-abs 1e-3 of final activations at tau=0, label
+disagreement <= 0.1%)."""
+import numpy as np
+import pytest
+
+from netutil import bits, c1_spec, generic_spec, paper_spec, stats_arr, tiny_spec, to_pkg_spec
+
+pytestmark = pytest.mark.gpu
+
+
+def run_pair(cbx, orc, spec, seed, cfg, frames, precision="exact", streams=1, check_layers=True):
+    w = orc.generate_weights(spec, seed)
+    onet = orc.load_network(spec, w)
+    net = cbx.Network(to_pkg_spec(cbx, spec), w, streams=streams, precision=precision)
+    ncb = sum(l["kind"] == "CBCONV" for l in spec["layers"])
+    for f in range(frames):
+        fr = orc.synth_frame(cfg, f)
+        want = onet.forward_frame(fr)
+        got = net.forward(np.stack([fr] * streams))
+        for s in range(streams):
+            yield f, s, want, got[s], onet, net, ncb
+
+
+@pytest.mark.parametrize("name,spec,seed,cfg,frames", [
+    ("c1", c1_spec(), 1, dict(channels=16, height=128, width=128, sprites=[(24, 7, 0.9)], seed=2), 8),
+    ("paper48", paper_spec(48, 64), 1, dict(channels=3, height=48, width=64, sprites=[(10, 2, 0.9)], noise=0.01, seed=3), 5),
+    ("tiny_tau0", tiny_spec(), 42, dict(channels=2, height=16, width=16, sprites=[(5, 1, 0.9)], noise=0.03, seed=7), 5),
+    ("generic", generic_spec(), 5, dict(channels=3, height=37, width=45, sprites=[(6, 2, 0.8)], noise=0.015, seed=9), 6),
+])
+def test_exact_bitwise(gpu, orc, name, spec, seed, cfg, frames):
+    for f, s, want, got, onet, net, ncb in run_pair(gpu, orc, spec, seed, cfg, frames):
+        assert np.array_equal(got.labels, want["labels"]), (name, f)
+        assert np.array_equal(stats_arr(got.stats), stats_arr(want["stats"])), (name, f)
+        assert got.macsTotal == want["macsTotal"]
+        for k, l in enumerate(spec["layers"]):
+            if l["kind"] == "CLASSIFY":
+                continue
+            assert np.array_equal(bits(net.layer_output(k)), bits(onet.layer_output(k))), (name, f, k)
+        for cb in range(ncb):
+            d1, u1 = net.trace(cb)
+            d2, u2 = onet.trace(cb)
+            assert (d1 is None) == (d2 is None)
+            if d1 is not None:
+                assert np.array_equal(d1, d2), (name, f, cb)
+            assert np.array_equal(u1, u2), (name, f, cb)
+
+
+def test_golden_c1_direct(gpu, orc, golden):
+    """The CUDA path against the reference's own recorded outputs (no oracle)."""
+    import json
+    d = golden("c1.npz")
+    spec = json.loads(str(d["spec"][0]))
+    cfg = json.loads(str(d["synth"][0]))
+    w = gpu.generate_weights(to_pkg_spec(gpu, spec), None, int(d["seed"][0]))
+    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="exact")
+    for f in range(8):
+        r = net.forward_frame(gpu.synth_frame(cfg, f))
+        assert np.array_equal(r.labels, d[f"f{f}_labels"])
+        assert np.array_equal(stats_arr(r.stats), d[f"f{f}_stats"])
+        det, upd = net.trace(0)
+        assert np.array_equal(upd, d[f"f{f}_cb0_upd"])
+        if det is not None:
+            assert np.array_equal(np.packbits(det.reshape(-1)), d[f"f{f}_cb0_det"])
+
+
+def test_tau0_cb_equals_baseline_gpu(gpu, orc):
+    """test_network.cpp:176-199 on the GPU engine, both precisions: CB == Baseline bitwise."""
+    spec = tiny_spec(0.0)
+    w = orc.generate_weights(spec, 42)
+    cfg = dict(channels=2, height=16, width=16, sprites=[(5, 1, 0.9)], noise=0.03, seed=7)
+    for prec in ("exact", "tf32"):
+        net = gpu.Network(to_pkg_spec(gpu, spec), w, precision=prec)
+        for f in range(5):
+            fr = orc.synth_frame(cfg, f)
+            a = net.forward_frame(fr, "cbinfer")
+            fa = net.final_activation(engine="cbinfer")
+            b = net.forward_frame(fr, "baseline")
+            fb = net.final_activation(engine="baseline")
+            assert np.array_equal(bits(fa), bits(fb)), (prec, f)
+            assert np.array_equal(a.labels, b.labels)
+
+
+def test_static_scene_and_reset(gpu, orc):
+    """test_network.cpp:163-174 and :236-257."""
+    spec = paper_spec(32, 48, (0.02, 0.05, 0.05))
+    w = orc.generate_weights(spec, 99)
+    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="exact")
+    fr = np.random.default_rng(71).random((3, 32, 48), dtype=np.float32)
+    first = net.forward_frame(fr)
+    assert first.macsTotal > 0
+    second = net.forward_frame(fr)
+    for cb in net.spec.cb_layers():
+        assert second.stats[cb]["gemmMacs"] == 0
+    assert np.array_equal(first.labels, second.labels)
+    net.reset_state()
+    again = net.forward_frame(fr)
+    assert again.macsTotal == first.macsTotal
+    assert np.array_equal(again.labels, first.labels)
+    assert np.array_equal(stats_arr(again.stats), stats_arr(first.stats))
+
+
+def test_baseline_leaves_cb_state(gpu, orc):
+    """network.cpp:278-285: interleaved Baseline frames do not disturb the CB state."""
+    spec = paper_spec(48, 64)
+    w = orc.generate_weights(spec, 1)
+    cfg = dict(channels=3, height=48, width=64, sprites=[(10, 2, 0.9)], noise=0.01, seed=3)
+    onet = orc.load_network(spec, w)
+    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="exact")
+    for f in range(4):
+        fr = orc.synth_frame(cfg, f)
+        net.forward_frame(orc.synth_frame(cfg, f + 7), "baseline")
+        got = net.forward_frame(fr, "cbinfer")
+        want = onet.forward_frame(fr)
+        assert np.array_equal(got.labels, want["labels"])
+        assert np.array_equal(stats_arr(got.stats), stats_arr(want["stats"]))
+
+
+def test_multistream_independent(gpu, orc):
+    """Streams batched in one context behave like independent Networks."""
+    spec = paper_spec(40, 56)
+    w = orc.generate_weights(spec, 3)
+    S = 3
+    cfgs = [dict(channels=3, height=40, width=56, sprites=[(8, 1 + s, 0.9)], noise=0.005 * s, seed=10 + s)
+            for s in range(S)]
+    onets = [orc.load_network(spec, w) for _ in range(S)]
+    net = gpu.Network(to_pkg_spec(gpu, spec), w, streams=S, precision="exact")
+    for f in range(4):
+        frames = [orc.synth_frame(c, f) for c in cfgs]
+        got = net.forward(np.stack(frames))
+        for s in range(S):
+            want = onets[s].forward_frame(frames[s])
+            assert np.array_equal(got[s].labels, want["labels"]), (f, s)
+            assert np.array_equal(stats_arr(got[s].stats), stats_arr(want["stats"])), (f, s)
+            for cb in range(3):
+                assert np.array_equal(net.trace(cb, s)[1], onets[s].trace(cb)[1])
+
+
+def test_tf32_tolerance(gpu, orc):
+    """TF32 (tcgen05) mode: layer-1 masks/indices/outputs bit-exact, final
+    activations within 1e-3 max-abs at tau=0, labels within 0.1%; at tau>0 the
+    per-layer changed-pixel mismatch counts are reported (and bounded)."""
+    spec = paper_spec(64, 96, (0.0, 0.0, 0.0))
+    w = orc.generate_weights(spec, 1)
+    cfg = dict(channels=3, height=64, width=96, sprites=[(12, 2, 0.9)], noise=0.01, seed=3)
+    onet = orc.load_network(spec, w)
+    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32")
+    for f in range(4):
+        fr = orc.synth_frame(cfg, f)
+        want = onet.forward_frame(fr)
+        got = net.forward_frame(fr)
+        assert np.array_equal(bits(net.layer_output(0)), bits(onet.layer_output(0)))
+        d1, u1 = net.trace(0)
+        d2, u2 = onet.trace(0)
+        assert np.array_equal(u1, u2)
+        err = np.abs(net.final_activation() - onet.final_activation()).max()
+        assert err <= 1e-3, err
+        assert (got.labels != want["labels"]).mean() <= 1e-3
+
+
+def test_errors(gpu, orc):
+    spec = paper_spec(32, 48)
+    w = orc.generate_weights(spec, 1)
+    net = gpu.Network(to_pkg_spec(gpu, spec), w)
+    with pytest.raises(gpu.ShapeError):
+        net.forward_frame(np.zeros((3, 32, 47), np.float32))
+    with pytest.raises(gpu.SpecError):
+        net.set_thresholds([0.1, 0.1])
+    with pytest.raises(gpu.SpecError):
+        net.set_thresholds([0.1, -0.1, 0.1])
+    net.set_thresholds([0.5, 0.25, 0.125])
+    assert net.thresholds() == [0.5, 0.25, 0.125]
