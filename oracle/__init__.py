@@ -170,7 +170,7 @@ class Oracle:
         ho, wo = out_hw(g, h, w)
         out = np.zeros((ho, wo), np.uint8)
         geom = _geom(g)
-        rc = self.lib.orc_worst_case_propagation(idx.ctypes.data_as(C.POINTER(C.c_int32)), len(idx),
+        rc = self.lib.orc_worst_case_propagation(idx.ctypes.data_as(C.POINTER(C.c_int32)), C.c_int64(len(idx)),
                                                  C.byref(geom), h, w,
                                                  out.ctypes.data_as(C.POINTER(C.c_uint8)))
         if rc:
@@ -180,7 +180,7 @@ class Oracle:
     def extract_indexes(self, m):
         m, pm = _u8(m)
         idx = np.zeros(m.size, np.int32)
-        n = self.lib.orc_extract_indexes(pm, m.size, idx.ctypes.data_as(C.POINTER(C.c_int32)))
+        n = self.lib.orc_extract_indexes(pm, C.c_int64(m.size), idx.ctypes.data_as(C.POINTER(C.c_int32)))
         return idx[:n].copy()
 
     def gen_x_reduced(self, inp, idx, g):
@@ -190,7 +190,7 @@ class Oracle:
         X = np.zeros((len(idx), rows), np.float32)  # column-major [n][rows]
         geom = _geom(g)
         rc = self.lib.orc_gen_x_reduced(pi, *inp.shape, idx.ctypes.data_as(C.POINTER(C.c_int32)),
-                                        len(idx), C.byref(geom), X.ctypes.data_as(C.POINTER(C.c_float)))
+                                        C.c_int64(len(idx)), C.byref(geom), X.ctypes.data_as(C.POINTER(C.c_float)))
         if rc:
             raise OracleError(rc)
         return X
@@ -202,7 +202,7 @@ class Oracle:
         rows, cols = K.shape
         n = X.shape[0]
         Y = np.zeros((rows, n), np.float32)
-        self.lib.orc_gemm(pk, pb, rows, cols, px, n, Y.ctypes.data_as(C.POINTER(C.c_float)))
+        self.lib.orc_gemm(pk, pb, rows, cols, px, C.c_int64(n), Y.ctypes.data_as(C.POINTER(C.c_float)))
         return Y
 
     def update_output(self, prev, Y, idx, fuse):
@@ -212,7 +212,7 @@ class Oracle:
         if Y.shape[1] != len(idx) or Y.shape[0] != out.shape[0]:
             raise OracleError(-1, "update_output")
         rc = self.lib.orc_update_output(out.ctypes.data_as(C.POINTER(C.c_float)), *out.shape, py,
-                                        idx.ctypes.data_as(C.POINTER(C.c_int32)), len(idx), int(fuse))
+                                        idx.ctypes.data_as(C.POINTER(C.c_int32)), C.c_int64(len(idx)), int(fuse))
         if rc:
             raise OracleError(rc)
         return out
@@ -233,7 +233,7 @@ class Oracle:
     def relu(self, t):
         t, pt = _f32(t)
         out = np.empty_like(t)
-        self.lib.orc_relu(pt, t.size, out.ctypes.data_as(C.POINTER(C.c_float)))
+        self.lib.orc_relu(pt, C.c_int64(t.size), out.ctypes.data_as(C.POINTER(C.c_float)))
         return out
 
     def maxpool(self, t, window, stride):

@@ -1,21 +1,474 @@
-// conv_tc.cu -- placeholder until the tcgen05 kernel lands.
+// conv_tc.cu -- gathered ("sparse") convolution on the 5th-generation tensor
+// cores (tcgen05, kind::tf32, fp32 accumulation in TMEM).
+//
+// Replaces gen_x_reduced + gemm + update_output
+// (/root/reference/proj/core/src/cbconv.cpp:115-155, baseline.cpp:47-63) for
+// every convolution whose input is a channels-last device tensor:
+//
+//   Y[n, o] = bias[o] + sum_K X[n, K] * W[o, K],  n over the change-index list
+//
+// * M = 128 output pixels per tile (one tile = 128 consecutive entries of the
+//   ascending index list, or of all pixels in full mode). A is the im2col of
+//   those pixels, GATHERED straight into shared memory: 4 producer warps, one
+//   thread per tile row, 16-byte cp.async per (tap, 4-channel) chunk of the
+//   zero-halo HWC input, written in the canonical K-major SWIZZLE_128B layout
+//   the UMMA descriptor expects (chunk j of row r at slot j ^ (r & 7)). K is
+//   ordered (kj, ki, c) and blocked by 32 tf32 values (128 B per row per
+//   K-block); chunks past the real K are zero-filled.
+// * B = the filter bank, pre-arranged on the host into exactly the smem image
+//   of every K-block (N_pad rows x 128 B, swizzled, tf32-rounded), loaded with
+//   one cp.async.bulk per stage that completes on the stage's mbarrier.
+// * One elected thread issues tcgen05.mma (M=128, N<=256 per instruction; two
+//   instructions when N_pad > 256, e.g. 304 = 256 + 48) into a TMEM
+//   accumulator; tcgen05.commit releases smem stages and hands finished
+//   accumulators to the epilogue. Persistent CTAs walk tiles; with N_pad <= 256
+//   the accumulator is double-buffered so the epilogue of tile t overlaps the
+//   MMAs of tile t+1.
+// * Epilogue (4 warps, thread = TMEM lane = tile row): tcgen05.ld 32 columns at
+//   a time, + bias, fused ReLU, compare with the value being overwritten
+//   (next CBCONV's change detection, cbconv.cpp:66-67), in-place scatter into
+//   the persistent output tensor (update_output without the full copy).
+#include <cstring>
+#include <vector>
+
 #include "conv_tc.hpp"
 #include "engine.hpp"
 
 namespace cbx {
 
+namespace {
+
+constexpr int kTileM = 128;
+constexpr int kKBlock = 32;        // tf32 elements per K-block (128 B per row)
+constexpr int kChunksPerKB = 8;    // 16-byte chunks per K-block row
+constexpr int kABytes = kTileM * 128;
+constexpr int kEpiThreads = 128, kProdThreads = 128;
+constexpr int kThreads = kEpiThreads + kProdThreads + 32;
+constexpr int kMaxSmem = 232448;   // 227 KB opt-in
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// 16-byte async copy; src_bytes == 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor: rows of 128 B, 8-row
+// core groups 1024 B apart (SBO), version 1 (Blackwell).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+// Instruction descriptor: D=f32, A=B=tf32, both K-major, M=128, N.
+__host__ __device__ constexpr uint32_t idesc_tf32(int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcArgs {
+    const float* in;
+    int64_t in_ss;
+    int in_Wp, in_Cp, in_hh, in_hw;
+    float* out;
+    int64_t out_ss;
+    int out_Wp, out_Cp, out_hh, out_hw;
+    int O, Ho, Wo;
+    int kh, kw, sh, sw, ph, pw;
+    const int32_t* idx;
+    const int* count;
+    int64_t full_count;
+    const float* Bw;     // [NKB][Npad][32] swizzled smem images
+    const float* bias;   // [O]
+    int NKB, Npad, N0, N1;
+    int stages, acc_stages, acc_cols, tmem_cols;
+    int relu;
+    uint8_t* chg;
+    int64_t chg_stride;
+    float tau;
+    unsigned long long* chg_cnt;
+    int cnt_stride;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int NS = a.stages;
+    const uint32_t b_bytes = (uint32_t)a.Npad * 128u;
+    uint8_t* sA = smem;                                  // NS x 16 KB
+    uint8_t* sB = sA + (size_t)NS * kABytes;             // NS x b_bytes
+    int* sTab = reinterpret_cast<int*>(sB + (size_t)NS * b_bytes);   // NKB*8 chunk offsets (floats)
+    float* sBias = reinterpret_cast<float*>(sTab + a.NKB * kChunksPerKB);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(sBias + ((a.O + 3) & ~3)) + 7) & ~uintptr_t(7));
+    uint64_t* full = bars;
+    uint64_t* empty = full + NS;
+    uint64_t* tfull = empty + NS;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int C4 = a.in_Cp >> 2;
+    const int nchunks = a.kh * a.kw * C4;
+
+    // ---- setup
+    for (int j = tid; j < a.NKB * kChunksPerKB; j += kThreads) {
+        int off = -1;
+        if (j < nchunks) {
+            const int tap = j / C4, c4 = j - tap * C4;
+            const int kj = tap / a.kw, ki = tap - kj * a.kw;
+            off = (kj * a.in_Wp + ki) * a.in_Cp + c4 * 4;
+        }
+        sTab[j] = off;
+    }
+    for (int o = tid; o < a.O; o += kThreads) sBias[o] = a.bias[o];
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], kProdThreads + 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], kEpiThreads);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 8) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sTmem)),
+                     "r"(a.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *sTmem;
+
+    const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
+    const int64_t ntiles = (total + kTileM - 1) / kTileM;
+    const int64_t HoWo = (int64_t)a.Ho * a.Wo;
+
+    if (warp >= 4 && warp < 8) {
+        // ================= producers: row r of every tile =================
+        const int r = tid - kEpiThreads;
+        const uint32_t swz = (uint32_t)(r & 7);
+        uint32_t it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t n = tile * kTileM + r;
+            const bool valid = n < total;
+            const float* base = a.in;
+            if (valid) {
+                const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
+                const int s = (int)(g / HoWo);
+                const int p = (int)(g - (int64_t)s * HoWo);
+                const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
+                base = a.in + (int64_t)s * a.in_ss +
+                       ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
+            }
+            for (int kb = 0; kb < a.NKB; ++kb, ++it) {
+                const uint32_t st = it % NS, ph = (it / NS) & 1u;
+                mbar_wait(&empty[st], ph ^ 1u);
+                if (r == 0) {
+                    mbar_arrive_expect_tx(&full[st], b_bytes);
+                    bulk_g2s(sB + (size_t)st * b_bytes, a.Bw + (size_t)kb * a.Npad * kKBlock, b_bytes, &full[st]);
+                }
+                const uint32_t row = smem_u32(sA + (size_t)st * kABytes + r * 128);
+                if (valid) {
+#pragma unroll
+                    for (int j = 0; j < kChunksPerKB; ++j) {
+                        const int off = sTab[kb * kChunksPerKB + j];
+                        cp_async16(row + ((j ^ swz) << 4), off >= 0 ? base + off : a.in, off >= 0 ? 16u : 0u);
+                    }
+                }
+                cp_async_arrive_noinc(&full[st]);
+            }
+        }
+    } else if (warp == 8) {
+        // ================= MMA issuer =================
+        if (lane == 0) {
+            const uint32_t id0 = idesc_tf32(a.N0), id1 = idesc_tf32(a.N1 > 0 ? a.N1 : 16);
+            uint32_t it = 0, acc_it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++acc_it) {
+                const uint32_t as = acc_it % a.acc_stages, aph = (acc_it / a.acc_stages) & 1u;
+                mbar_wait(&tempty[as], aph ^ 1u);
+                tc_fence_after();
+                const uint32_t d = tmem_base + as * a.acc_cols;
+                for (int kb = 0; kb < a.NKB; ++kb, ++it) {
+                    const uint32_t st = it % NS, ph = (it / NS) & 1u;
+                    mbar_wait(&full[st], ph);
+                    fence_proxy_async();
+                    tc_fence_after();
+                    const uint32_t aaddr = smem_u32(sA + (size_t)st * kABytes);
+                    const uint32_t baddr = smem_u32(sB + (size_t)st * b_bytes);
+#pragma unroll
+                    for (int k = 0; k < kKBlock / 8; ++k) {
+                        const uint64_t ad = smem_desc(aaddr + k * 32);
+                        const uint32_t accum = (kb | k) ? 1u : 0u;
+                        mma_tf32(d, ad, smem_desc(baddr + k * 32), id0, accum);
+                        if (a.N1 > 0) mma_tf32(d + a.N0, ad, smem_desc(baddr + a.N0 * 128 + k * 32), id1, accum);
+                    }
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&tfull[as]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ================= epilogue: thread = TMEM lane = tile row =================
+        const int r = tid;
+        uint32_t acc_it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++acc_it) {
+            const uint32_t as = acc_it % a.acc_stages, aph = (acc_it / a.acc_stages) & 1u;
+            mbar_wait(&tfull[as], aph);
+            tc_fence_after();
+            const int64_t n = tile * kTileM + r;
+            const bool valid = n < total;
+            int s = 0, p = 0;
+            float* dst = nullptr;
+            if (valid) {
+                const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
+                s = (int)(g / HoWo);
+                p = (int)(g - (int64_t)s * HoWo);
+                const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
+                dst = a.out + (int64_t)s * a.out_ss + ((int64_t)(y + a.out_hh) * a.out_Wp + (x + a.out_hw)) * a.out_Cp;
+            }
+            bool changed = false;
+            const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16) + as * a.acc_cols;
+            for (int c0 = 0; c0 < a.O; c0 += 32) {
+                float v[32];
+                tmem_ld32(trow + c0, v);
+                if (valid) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const int o = c0 + j;
+                        if (o >= a.O) break;
+                        float w4[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float t = (o + e < a.O) ? __fadd_rn(v[j + e], sBias[o + e]) : 0.0f;
+                            w4[e] = a.relu ? ref_relu(t) : t;
+                        }
+                        if (o + 3 < a.O) {
+                            float4* q = reinterpret_cast<float4*>(dst + o);
+                            if (a.chg) {
+                                const float4 old = *q;
+                                changed |= ref_changed(w4[0], old.x, a.tau) | ref_changed(w4[1], old.y, a.tau) |
+                                           ref_changed(w4[2], old.z, a.tau) | ref_changed(w4[3], old.w, a.tau);
+                            }
+                            *q = make_float4(w4[0], w4[1], w4[2], w4[3]);
+                        } else {
+                            for (int e = 0; e < 4 && o + e < a.O; ++e) {
+                                if (a.chg) changed |= ref_changed(w4[e], dst[o + e], a.tau);
+                                dst[o + e] = w4[e];
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[as]);
+            if (a.chg) {
+                if (valid && changed) a.chg[(int64_t)s * a.chg_stride + p] = 1;
+                if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols));
+    }
+}
+
+float round_tf32(float x) {
+    // round-to-nearest (ties away) to 10 explicit mantissa bits, as cvt.rna.tf32.f32
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+}
+
+}  // namespace
+
 struct TcLayer {
     cbx_geom g;
+    int Cp = 0, NKB = 0, Npad = 0, N0 = 0, N1 = 0;
+    int stages = 0, acc_stages = 1, acc_cols = 0, tmem_cols = 32;
+    size_t smem = 0;
+    float* Bw = nullptr;
 };
-void TcLayerDeleter::operator()(TcLayer* p) const { delete p; }
-bool tc_supported(const cbx_geom&) { return false; }
-std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g) {
-    return std::unique_ptr<TcLayer, TcLayerDeleter>(new TcLayer{g});
+
+void TcLayerDeleter::operator()(TcLayer* p) const {
+    if (p && p->Bw) cudaFree(p->Bw);
+    delete p;
 }
-void tc_load_weights(TcLayer&, const float*, cudaStream_t) {}
-void launch_conv_tc(const TcLayer&, TensorView, TensorView, const float*, const int32_t*, const int*,
-                    int64_t, bool, MaskView, float, unsigned long long*, int, int, cudaStream_t) {
-    throw Error(CBX_E_CUDA, "tcgen05 path not built");
+
+bool tc_supported(const cbx_geom& g) {
+    const int Npad = (int)round_up(g.outChannels, 16);
+    return g.outChannels >= 1 && Npad <= 512 && g.kernelH * g.kernelW * round_up(g.inChannels, 4) <= 65536;
+}
+
+std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g) {
+    std::unique_ptr<TcLayer, TcLayerDeleter> t(new TcLayer);
+    t->g = g;
+    t->Cp = (int)round_up(g.inChannels, 4);
+    const int nchunks = g.kernelH * g.kernelW * (t->Cp / 4);
+    t->NKB = (nchunks + kChunksPerKB - 1) / kChunksPerKB;
+    t->Npad = (int)round_up(g.outChannels, 16);
+    t->N0 = t->Npad > 256 ? 256 : t->Npad;
+    t->N1 = t->Npad - t->N0;
+    t->acc_cols = (int)round_up(t->Npad, 32);  // tcgen05.ld reads 32-column groups
+    t->acc_stages = (2 * t->acc_cols <= 512) ? 2 : 1;
+    int cols = 32;
+    while (cols < t->acc_stages * t->acc_cols) cols *= 2;
+    t->tmem_cols = cols;
+    const size_t b_bytes = (size_t)t->Npad * 128;
+    const size_t fixed = 1024 + (size_t)t->NKB * kChunksPerKB * 4 + round_up(g.outChannels, 4) * 4 + 16 + 8 * (2 * 16 + 4) + 16;
+    int ns = 8;
+    while (ns > 2 && fixed + (size_t)ns * (kABytes + b_bytes) > (size_t)kMaxSmem) --ns;
+    if (fixed + (size_t)ns * (kABytes + b_bytes) > (size_t)kMaxSmem)
+        throw Error(CBX_E_ARG, "tcgen05 conv: layer too wide for shared memory");
+    t->stages = ns;
+    t->smem = fixed + (size_t)ns * (kABytes + b_bytes);
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CBX_CUDA(cudaMalloc(&t->Bw, (size_t)t->NKB * b_bytes));
+    CBX_CUDA(cudaMemset(t->Bw, 0, (size_t)t->NKB * b_bytes));
+    return t;
+}
+
+// Host-side re-layout of the reference filter matrix K[o][(c*kh + kj)*kw + ki]
+// into per-K-block swizzled smem images: element (n, kb*32 + j*4 + e) at
+// float offset kb*Npad*32 + n*32 + ((j ^ (n & 7)) * 4) + e, where chunk
+// J = kb*8 + j covers tap J / C4 = (kj, ki) and channels 4*(J % C4) + e.
+void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
+    const cbx_geom& g = t.g;
+    const int C4 = t.Cp / 4, khw = g.kernelH * g.kernelW;
+    const int Kref = g.inChannels * khw;
+    std::vector<float> img((size_t)t.NKB * t.Npad * kKBlock, 0.0f);
+    for (int n = 0; n < g.outChannels; ++n)
+        for (int J = 0; J < t.NKB * kChunksPerKB; ++J) {
+            const int tap = J / C4, c4 = J - tap * C4;
+            if (tap >= khw) continue;
+            const int kb = J / kChunksPerKB, j = J - kb * kChunksPerKB;
+            for (int e = 0; e < 4; ++e) {
+                const int c = c4 * 4 + e;
+                if (c >= g.inChannels) continue;
+                const float w = K[(size_t)n * Kref + (size_t)c * khw + tap];
+                img[(size_t)kb * t.Npad * kKBlock + (size_t)n * kKBlock + ((j ^ (n & 7)) * 4) + e] = round_tf32(w);
+            }
+        }
+    CBX_CUDA(cudaMemcpyAsync(t.Bw, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+    CBX_CUDA(cudaStreamSynchronize(st));
+}
+
+void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float* bias, const int32_t* idx,
+                    const int* count, int64_t full_count, bool relu, MaskView chg, float tau,
+                    unsigned long long* cnt, int cstride, int S, cudaStream_t st) {
+    (void)S;
+    if (in.Cp != t.Cp) throw Error(CBX_E_SHAPE, "tcgen05 conv: input channel stride mismatch");
+    TcArgs a{};
+    a.in = in.d;
+    a.in_ss = in.ss;
+    a.in_Wp = in.Wp;
+    a.in_Cp = in.Cp;
+    a.in_hh = in.hh;
+    a.in_hw = in.hw;
+    a.out = out.d;
+    a.out_ss = out.ss;
+    a.out_Wp = out.Wp;
+    a.out_Cp = out.Cp;
+    a.out_hh = out.hh;
+    a.out_hw = out.hw;
+    a.O = out.C;
+    a.Ho = out.H;
+    a.Wo = out.W;
+    a.kh = t.g.kernelH;
+    a.kw = t.g.kernelW;
+    a.sh = t.g.strideH;
+    a.sw = t.g.strideW;
+    a.ph = t.g.padH;
+    a.pw = t.g.padW;
+    a.idx = idx;
+    a.count = count;
+    a.full_count = full_count;
+    a.Bw = t.Bw;
+    a.bias = bias;
+    a.NKB = t.NKB;
+    a.Npad = t.Npad;
+    a.N0 = t.N0;
+    a.N1 = t.N1;
+    a.stages = t.stages;
+    a.acc_stages = t.acc_stages;
+    a.acc_cols = t.acc_cols;
+    a.tmem_cols = t.tmem_cols;
+    a.relu = relu;
+    a.chg = chg.d;
+    a.chg_stride = chg.stride;
+    a.tau = tau;
+    a.chg_cnt = chg.d ? cnt : nullptr;
+    a.cnt_stride = cstride;
+    const int64_t max_tiles = (full_count + kTileM - 1) / kTileM;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, kNumSMs));
+    conv_tc_kernel<<<grid, kThreads, t.smem, st>>>(a);
 }
 
 }  // namespace cbx
