@@ -1,0 +1,56 @@
+"""GPU: the tcgen05 (tf32) gathered convolution against the exact oracle,
+with an error bound derived from the operands: tf32 keeps 10 mantissa bits,
+so |y_tc - y_exact| <= 2^-9 * sum_r |w_r x_r| (+ fp32 accumulation slack).
+Shapes cover N split (304 = 256 + 48), N padding (52 -> 64, 8 -> 16),
+channel padding (Cin % 4 != 0), stride, asymmetric kernels and K-blocks
+straddling taps."""
+import numpy as np
+import pytest
+
+from netutil import to_pkg_spec
+
+pytestmark = pytest.mark.gpu
+
+
+def two_layer(cin, h, w, layer):
+    # layer 0: exact 1x1 CONV from the planar frame to a channels-last tensor of
+    # `cin` channels; layer 1: the tcgen05 layer under test (tau=0, full frames).
+    return dict(inputChannels=3, inputHeight=h, inputWidth=w, numClasses=layer["outChannels"], layers=[
+        dict(kind="CONV", kernelH=1, kernelW=1, outChannels=cin, weightsFile="a"), layer])
+
+
+CASES = [
+    (52, 30, 40, dict(kind="CBCONV", kernelH=7, kernelW=7, padH=3, padW=3, outChannels=304, threshold=0.0, fuseRelu=True, weightsFile="b")),
+    (4, 60, 80, dict(kind="CBCONV", kernelH=7, kernelW=7, padH=3, padW=3, outChannels=52, threshold=0.0, fuseRelu=True, weightsFile="b")),
+    (304, 20, 24, dict(kind="CONV", kernelH=1, kernelW=1, outChannels=8, weightsFile="b")),
+    (6, 33, 47, dict(kind="CBCONV", kernelH=5, kernelW=3, strideH=2, strideW=1, padH=2, padW=1, outChannels=37, threshold=0.0, fuseRelu=False, weightsFile="b")),
+    (13, 17, 19, dict(kind="CBCONV", kernelH=3, kernelW=3, padH=1, padW=1, outChannels=300, threshold=0.0, fuseRelu=True, weightsFile="b")),
+]
+
+
+@pytest.mark.parametrize("cin,h,w,layer", CASES)
+def test_tc_layer_vs_exact(gpu, orc, cin, h, w, layer):
+    spec = two_layer(cin, h, w, layer)
+    wts = orc.generate_weights(spec, 11)
+    onet = orc.load_network(spec, wts)
+    net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="tf32")
+    cfg = dict(channels=3, height=h, width=w, sprites=[(5, 2, 0.9)], noise=0.02, seed=5)
+    for f in range(3):
+        fr = orc.synth_frame(cfg, f)
+        onet.forward_frame(fr)
+        net.forward_frame(fr)
+        x = onet.layer_output(0)
+        assert np.array_equal(net.layer_output(0).view(np.uint32), x.view(np.uint32))
+        want = onet.layer_output(1)
+        got = net.layer_output(1)
+        l = spec["layers"][1]
+        g = dict(kernelH=l["kernelH"], kernelW=l["kernelW"], strideH=l.get("strideH", 1),
+                 strideW=l.get("strideW", 1), padH=l.get("padH", 0), padW=l.get("padW", 0),
+                 inChannels=cin, outChannels=l["outChannels"])
+        K, b = wts[1]
+        ho, wo = want.shape[1:]
+        X = orc.gen_x_reduced(np.abs(x), np.arange(ho * wo, dtype=np.int32), g)
+        scale = orc.gemm(np.abs(K), np.abs(b), X).reshape(want.shape)
+        err = np.abs(got.astype(np.float64) - want)
+        bound = 2.0 ** -9 * scale + 1e-6
+        assert np.all(err <= bound), (float((err / bound).max()), float(err.max()))
