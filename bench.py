@@ -303,6 +303,7 @@ def run_gpu_arm(args):
 
     clocks = Clocks(local)
     clocks.start()
+    time.sleep(0.3)  # nvidia-smi needs a moment before its first sample
     # warm-up: frame 0 is the full evaluation, then W steady steps
     net.forward_device(ptrs(0))
     for i in range(1, args.warmup + 1):
@@ -312,7 +313,17 @@ def run_gpu_arm(args):
     K = args.steps
     ms = timed("cbinfer", i0, K)
     launches = net.last_launch_count()
+    # keep the GPU under the same load ~0.5 s so the sampler sees it (the timed
+    # region itself can be shorter than one nvidia-smi sample period)
+    t_end = time.perf_counter() + 0.5
+    j = i0 + K
+    while time.perf_counter() < t_end:
+        for _ in range(10):
+            net.forward_device(ptrs(j))
+            j += 1
+        net.sync()
     clk = clocks.stop()
+    clk["note"] = "sampled every 100 ms across warm-up, the timed region and a 0.5 s continuation of the same step"
     value = ws * S * K / (ms / 1000.0)
     log(f"[gpu] cbinfer: {ms / K:.3f} ms/step, {value:.1f} frames/s, {launches} kernels/frame")
 
