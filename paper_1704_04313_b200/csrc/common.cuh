@@ -29,7 +29,24 @@ struct MaskView {
     int64_t stride;
 };
 
+// Packed bit mask on a pixel grid (the engine's change / updated-pixel masks):
+// [S][stride] 32-bit words, row y occupies words [y*wpr, (y+1)*wpr), pixel x
+// is bit (x & 31) of word x >> 5; bits past W are always zero. stride is a
+// multiple of 256 words so compaction tiles never straddle two streams.
+struct BitMask {
+    uint32_t* d;
+    int H, W, wpr;
+    int64_t stride;
+};
+
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+__device__ __forceinline__ bool bit_test(const BitMask& m, int s, int y, int x) {
+    return (m.d[(int64_t)s * m.stride + (int64_t)y * m.wpr + (x >> 5)] >> (x & 31)) & 1u;
+}
+__device__ __forceinline__ void bit_set(const BitMask& m, int s, int y, int x) {
+    atomicOr(m.d + (int64_t)s * m.stride + (int64_t)y * m.wpr + (x >> 5), 1u << (x & 31));
+}
 
 // Reference ReLU: std::max(0.0f, v) == (0.0f < v) ? v : 0.0f (baseline.cpp:115).
 __device__ __forceinline__ float ref_relu(float v) { return (0.0f < v) ? v : 0.0f; }

@@ -139,8 +139,7 @@ struct TcArgs {
     int NKB, Npad, N0, N1;
     int stages, acc_stages, acc_cols, tmem_cols;
     int relu;
-    uint8_t* chg;
-    int64_t chg_stride;
+    BitMask chg;
     float tau;
     unsigned long long* chg_cnt;
     int cnt_stride;
@@ -279,13 +278,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
             tc_fence_after();
             const int64_t n = tile * kTileM + r;
             const bool valid = n < total;
-            int s = 0, p = 0;
+            int s = 0, p = 0, y = 0, x = 0;
             float* dst = nullptr;
             if (valid) {
                 const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
                 s = (int)(g / HoWo);
                 p = (int)(g - (int64_t)s * HoWo);
-                const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
+                y = p / a.Wo;
+                x = p - y * a.Wo;
                 dst = a.out + (int64_t)s * a.out_ss + ((int64_t)(y + a.out_hh) * a.out_Wp + (x + a.out_hw)) * a.out_Cp;
             }
             bool changed = false;
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
                         }
                         if (o + 3 < a.O) {
                             float4* q = reinterpret_cast<float4*>(dst + o);
-                            if (a.chg) {
+                            if (a.chg.d) {
                                 const float4 old = *q;
                                 changed |= ref_changed(w4[0], old.x, a.tau) | ref_changed(w4[1], old.y, a.tau) |
                                            ref_changed(w4[2], old.z, a.tau) | ref_changed(w4[3], old.w, a.tau);
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
                             *q = make_float4(w4[0], w4[1], w4[2], w4[3]);
                         } else {
                             for (int e = 0; e < 4 && o + e < a.O; ++e) {
-                                if (a.chg) changed |= ref_changed(w4[e], dst[o + e], a.tau);
+                                if (a.chg.d) changed |= ref_changed(w4[e], dst[o + e], a.tau);
                                 dst[o + e] = w4[e];
                             }
                         }
@@ -323,8 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
             }
             tc_fence_before();
             mbar_arrive(&tempty[as]);
-            if (a.chg) {
-                if (valid && changed) a.chg[(int64_t)s * a.chg_stride + p] = 1;
+            if (a.chg.d) {
+                if (valid && changed) bit_set(a.chg, s, y, x);
                 if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
             }
         }
@@ -421,7 +421,7 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
 }
 
 void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float* bias, const int32_t* idx,
-                    const int* count, int64_t full_count, bool relu, MaskView chg, float tau,
+                    const int* count, int64_t full_count, bool relu, BitMask chg, float tau,
                     unsigned long long* cnt, int cstride, int S, cudaStream_t st) {
     (void)S;
     if (in.Cp != t.Cp) throw Error(CBX_E_SHAPE, "tcgen05 conv: input channel stride mismatch");
@@ -461,8 +461,7 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.acc_cols = t.acc_cols;
     a.tmem_cols = t.tmem_cols;
     a.relu = relu;
-    a.chg = chg.d;
-    a.chg_stride = chg.stride;
+    a.chg = chg;
     a.tau = tau;
     a.chg_cnt = chg.d ? cnt : nullptr;
     a.cnt_stride = cstride;

@@ -21,7 +21,7 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g);
 void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st);
 void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float* bias,
                     const int32_t* idx, const int* count, int64_t full_count, bool relu,
-                    MaskView chg, float tau, unsigned long long* cnt, int cstride, int S,
+                    BitMask chg, float tau, unsigned long long* cnt, int cstride, int S,
                     cudaStream_t st);
 
 }  // namespace cbx

@@ -133,11 +133,11 @@ struct Engine::Plan {
     bool baseline = false;
     std::vector<TensorView> T;      // nl+1; T[0] = frame (planar) unless ingested
     bool ingest = false;            // first layer is not a conv: frame copied to HWC T[0]
-    std::vector<MaskView> chg;      // nl+1
+    std::vector<BitMask> chg;       // nl+1
     std::vector<bool> chg_by_conv;  // chg written with 1s only -> cleared per frame
-    std::vector<MaskView> upd;      // nl+1 (aliases)
+    std::vector<BitMask> upd;       // nl+1 (aliases)
     std::vector<int> upd_owner;     // producing layer of upd[t] (-1 detect, -2 none)
-    std::vector<MaskView> U;        // nl (owned)
+    std::vector<BitMask> U;         // nl (owned)
     std::vector<int32_t*> idx;
     std::vector<int*> cnt;
     std::vector<int> idx_src;       // conv layer whose list is reused (-1: own)
@@ -160,9 +160,10 @@ struct Engine::Plan {
         allocs.push_back(p);
         return p;
     }
-    MaskView mask(int S, int H, int W) {
-        MaskView m{nullptr, H, W, round_up((int64_t)H * W, 16)};
-        m.d = alloc<uint8_t>((size_t)(m.stride * S));
+    BitMask mask(int S, int H, int W) {
+        const int wpr = (W + 31) / 32;
+        BitMask m{nullptr, H, W, wpr, round_up((int64_t)H * wpr, 256)};
+        m.d = alloc<uint32_t>((size_t)(m.stride * S));
         return m;
     }
 };
@@ -240,11 +241,11 @@ void Engine::build_plan(Plan& p, bool baseline) {
     const int nl = (int)layers_.size(), S = S_;
     p.baseline = baseline;
     p.T.assign(nl + 1, TensorView{});
-    p.chg.assign(nl + 1, MaskView{nullptr, 0, 0, 0});
+    p.chg.assign(nl + 1, BitMask{nullptr, 0, 0, 0, 0});
     p.chg_by_conv.assign(nl + 1, false);
-    p.upd.assign(nl + 1, MaskView{nullptr, 0, 0, 0});
+    p.upd.assign(nl + 1, BitMask{nullptr, 0, 0, 0, 0});
     p.upd_owner.assign(nl + 1, -2);
-    p.U.assign(nl, MaskView{nullptr, 0, 0, 0});
+    p.U.assign(nl, BitMask{nullptr, 0, 0, 0, 0});
     p.idx.assign(nl, nullptr);
     p.cnt.assign(nl, nullptr);
     p.idx_src.assign(nl, -1);
@@ -366,7 +367,12 @@ void Engine::build_plan(Plan& p, bool baseline) {
         }
         p.idx[k] = p.alloc<int32_t>((size_t)S * Ho * Wo);
         p.cnt[k] = p.alloc<int>(1);
-        ws = std::max(ws, compact_workspace_bytes(S, (int64_t)Ho * Wo));
+        const int wpr = (Wo + 31) / 32;
+        ws = std::max(ws, dilate_compact_workspace(BitMask{nullptr, Ho, Wo, wpr, round_up((int64_t)Ho * wpr, 256)}, S));
+        // strided geometries dilate separately, then compact the dilated mask
+        if (!identity_geom(l.geom) && (l.geom.strideH != 1 || l.geom.strideW != 1 || l.geom.kernelW - 1 - l.geom.padW > 31 ||
+                                       l.geom.padW > 31) && !p.U[k].d)
+            p.U[k] = p.mask(S, Ho, Wo);
     }
     if (ws) p.ws = p.alloc<uint8_t>(ws);
 }
@@ -379,16 +385,20 @@ void Engine::record(Plan& p, bool full) {
         CBX_CUDA(cudaMemsetAsync(p.stats, 0, sizeof(unsigned long long) * 2 * S * nl, st));
         for (int t = 0; t <= nl; ++t)
             if (p.chg_by_conv[t] && p.chg[t].d)
-                CBX_CUDA(cudaMemsetAsync(p.chg[t].d, 0, (size_t)(p.chg[t].stride * S), st));
+                CBX_CUDA(cudaMemsetAsync(p.chg[t].d, 0, sizeof(uint32_t) * (size_t)(p.chg[t].stride * S), st));
     }
     // K1: detection on the raw frames
     if (!full) {
         const auto& in = p.T[0];
-        if (p.chg[0].d)
-            launch_detect_planar(d_cur_, d_prev_, S, in.C, in.H, in.W, layers_[0].threshold, 0, p.chg[0],
-                                 stats_of(0, 0), 2, st); mark("detect", 0);
-        if (p.upd[0].d && p.upd_owner[0] == -1)
-            launch_detect_planar(d_cur_, d_prev_, S, in.C, in.H, in.W, 0.0f, 1, p.upd[0], nullptr, 2, st); mark("detect_bitwise", 0);
+        if (p.chg[0].d) {
+            launch_detect_bits(d_cur_, d_prev_, S, in.C, in.H, in.W, layers_[0].threshold, 0, p.chg[0],
+                               stats_of(0, 0), 2, st);
+            mark("detect", 0);
+        }
+        if (p.upd[0].d && p.upd_owner[0] == -1) {
+            launch_detect_bits(d_cur_, d_prev_, S, in.C, in.H, in.W, 0.0f, 1, p.upd[0], nullptr, 2, st);
+            mark("detect_bitwise", 0);
+        }
     }
     if (p.ingest) {
         launch_ingest(d_cur_, p.T[0], S, st);
@@ -397,7 +407,7 @@ void Engine::record(Plan& p, bool full) {
     for (int k = 0; k < nl; ++k) {
         const auto& l = layers_[k];
         const bool has_next = k + 1 < nl;
-        MaskView chg_next = (!full && has_next) ? p.chg[k + 1] : MaskView{nullptr, 0, 0, 0};
+        BitMask chg_next = (!full && has_next) ? p.chg[k + 1] : BitMask{nullptr, 0, 0, 0, 0};
         const float tau_next = has_next ? layers_[k + 1].threshold : 0.0f;
         unsigned long long* cnt_next = has_next ? stats_of(k + 1, 0) : nullptr;
         switch (l.kind) {
@@ -407,15 +417,25 @@ void Engine::record(Plan& p, bool full) {
                 const int32_t* idx = nullptr;
                 const int* count = nullptr;
                 if (!full) {
-                    if (l.kind == CBX_CBCONV) {
-                        launch_dilate(p.chg[k], p.U[k], S, g.kernelH, g.kernelW, g.strideH, g.strideW, g.padH, g.padW, st); mark("dilate", k);
-                        launch_compact(p.U[k], S, p.idx[k], p.cnt[k], p.ws, stats_of(k, 1), 2, st); mark("compact", k);
-                    } else if (p.idx_src[k] < 0) {
+                    if (p.idx_src[k] < 0) {
+                        // U_k = dilate(input change mask) (CBCONV) or dilate(input updated mask) (CONV)
+                        const BitMask& src = l.kind == CBX_CBCONV ? p.chg[k] : p.upd[k];
+                        unsigned long long* cnt = l.kind == CBX_CBCONV ? stats_of(k, 1) : nullptr;
+                        const bool fused = g.strideH == 1 && g.strideW == 1 && g.padW <= 31 && g.kernelW - 1 - g.padW <= 31;
                         if (identity_geom(g)) {
-                            launch_compact(p.upd[k], S, p.idx[k], p.cnt[k], p.ws, nullptr, 2, st); mark("compact", k);
+                            const bool own = p.U[k].d != nullptr;  // CBCONV 1x1: U_k is its own mask
+                            launch_dilate_compact(src, own ? p.U[k] : src, own, S, 1, 1, 0, 0, p.idx[k], p.cnt[k], p.ws,
+                                                  cnt, 2, st);
+                            mark("compact", k);
+                        } else if (fused) {
+                            launch_dilate_compact(src, p.U[k], true, S, g.kernelH, g.kernelW, g.padH, g.padW, p.idx[k],
+                                                  p.cnt[k], p.ws, cnt, 2, st);
+                            mark("dilate_compact", k);
                         } else {
-                            launch_dilate(p.upd[k], p.U[k], S, g.kernelH, g.kernelW, g.strideH, g.strideW, g.padH, g.padW, st); mark("dilate", k);
-                            launch_compact(p.U[k], S, p.idx[k], p.cnt[k], p.ws, nullptr, 2, st); mark("compact", k);
+                            launch_dilate_bits(src, p.U[k], S, g.kernelH, g.kernelW, g.strideH, g.strideW, g.padH, g.padW, st);
+                            mark("dilate", k);
+                            launch_dilate_compact(p.U[k], p.U[k], false, S, 1, 1, 0, 0, p.idx[k], p.cnt[k], p.ws, cnt, 2, st);
+                            mark("compact", k);
                         }
                     }
                     const int src = p.idx_src[k] >= 0 ? p.idx_src[k] : k;
@@ -455,59 +475,34 @@ void Engine::record(Plan& p, bool full) {
                 }
                 break;
             }
-            case CBX_RELU: {
-                PointArgs a{};
-                a.in = p.T[k];
-                a.out = p.T[k + 1];
-                a.upd = full ? nullptr : p.upd[k].d;
-                a.upd_stride = p.upd[k].stride;
-                a.chg = chg_next;
-                a.tau = tau_next;
-                a.chg_cnt = cnt_next;
-                a.cnt_stride = 2;
-                a.S = S;
-                launch_relu(a, st); mark("relu", k);
-                break;
-            }
+            case CBX_RELU:
             case CBX_MAXPOOL: {
-                PoolArgs a{};
+                const BitMask none{nullptr, 0, 0, 0, 0};
+                PointBitsArgs a{};
                 a.in = p.T[k];
                 a.out = p.T[k + 1];
-                a.window = l.window;
-                a.stride = l.stride;
-                a.upd_in = full ? nullptr : p.upd[k].d;
-                a.upd_in_stride = p.upd[k].stride;
-                a.upd_out = full ? nullptr : p.U[k].d;
-                a.upd_out_stride = p.U[k].stride;
+                a.relu = l.kind == CBX_RELU;
+                a.window = a.relu ? 1 : l.window;
+                a.stride = a.relu ? 1 : l.stride;
+                a.upd_in = full ? none : p.upd[k];
+                a.U_out = (full || a.relu) ? none : p.U[k];
                 a.chg = chg_next;
                 a.tau = tau_next;
                 a.chg_cnt = cnt_next;
                 a.cnt_stride = 2;
                 a.S = S;
-                launch_pool(a, st); mark("pool", k);
+                launch_point_bits(a, st);
+                mark(a.relu ? "relu" : "pool", k);
                 break;
             }
-            case CBX_CLASSIFY: {
-                PointArgs a{};
-                a.in = p.T[k];
-                a.upd = full ? nullptr : p.upd[k].d;
-                a.upd_stride = p.upd[k].stride;
-                a.labels = p.labels;
-                a.S = S;
-                launch_classify(a, st);
+            case CBX_CLASSIFY:
+                launch_classify_bits(p.T[k], full ? BitMask{nullptr, 0, 0, 0, 0} : p.upd[k], p.labels, S, st);
                 mark("classify", k);
                 break;
-            }
         }
     }
     if (layers_.back().kind != CBX_CLASSIFY) {
-        PointArgs a{};
-        a.in = p.T[nl];
-        a.upd = full ? nullptr : p.upd[nl].d;
-        a.upd_stride = p.upd[nl].stride;
-        a.labels = p.labels;
-        a.S = S;
-        launch_classify(a, st);
+        launch_classify_bits(p.T[nl], full ? BitMask{nullptr, 0, 0, 0, 0} : p.upd[nl], p.labels, S, st);
         mark("classify", nl);
     }
     CBX_CUDA(cudaGetLastError());
@@ -710,10 +705,16 @@ void Engine::get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64
     const bool full = last_full_[CBX_ENGINE_CBINFER];
     if (first) *first = full;
     if (detected) {
-        if (full)
+        if (full) {
             std::memset(detected, 0, (size_t)H * W);
-        else
-            CBX_CUDA(cudaMemcpy(detected, p.chg[k].d + (int64_t)s * p.chg[k].stride, (size_t)H * W, cudaMemcpyDeviceToHost));
+        } else {
+            uint8_t* tmp = nullptr;
+            CBX_CUDA(cudaMallocAsync(&tmp, (size_t)H * W, stream_));
+            launch_unpack_bits(p.chg[k], s, tmp, stream_);
+            CBX_CUDA(cudaMemcpyAsync(detected, tmp, (size_t)H * W, cudaMemcpyDeviceToHost, stream_));
+            CBX_CUDA(cudaFreeAsync(tmp, stream_));
+            sync();
+        }
     }
     if (full) {
         if (updated)

@@ -1,0 +1,419 @@
+// k_bits.cu -- the engine's change-mask pipeline on packed bit masks.
+//
+// Every mask the engine keeps (change masks "chg", updated-pixel masks "U")
+// is one bit per pixel, rows padded to 32-bit words (see BitMask in
+// common.cuh), so the O(frame) mask traffic is 1/8 of the reference's
+// uint8 ChangeMap (cbconv.hpp:17-29) and dilation is a handful of funnel
+// shifts per 32 pixels.
+//
+//   detect_bits        <- detect_changes  cbconv.cpp:57-71      (K1)
+//   dilate_compact     <- dilate_changes + extract_indexes
+//                         cbconv.cpp:73-82, 99-113              (K3+K2, one pass)
+//   dilate_bits        <- dilate_changes for strided geometries (K3)
+//   point_bits         <- maxpool / relu over updated pixels     (K5)
+//                         baseline.cpp:113-145, fused with the next
+//                         layer's change detection
+//   classify_bits      <- argmax_classify  baseline.cpp:147-163
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace cbx {
+
+// ---------------------------------------------------------------------------
+// K1: detection on the planar frames, 4 pixels per thread (128-bit loads of
+// every channel plane of both frames), packed with warp shuffles into words.
+template <int MODE>
+__global__ void __launch_bounds__(256) detect_bits_kernel(const float* const* cur, const float* const* prev, int C,
+                                                          int H, int W, float tau, BitMask m,
+                                                          unsigned long long* cnt, int cstride) {
+    const int s = blockIdx.y;
+    const float* a = cur[s];
+    const float* b = prev[s];
+    const int64_t HW = (int64_t)H * W;
+    const bool vec = (W % 4 == 0) && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 16 == 0);
+    const int qpr = m.wpr * 8;  // pixel quads per (padded) row
+    const int64_t nq = (int64_t)H * qpr;
+    const int lane = threadIdx.x & 31;
+    uint32_t* dst = m.d + (int64_t)s * m.stride;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nq; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = base + threadIdx.x;
+        const bool act = q < nq;
+        uint32_t flags = 0;
+        if (act) {
+            const int y = (int)(q / qpr);
+            const int x0 = (int)(q - (int64_t)y * qpr) * 4;
+            if (x0 < W) {
+                const int64_t p0 = (int64_t)y * W + x0;
+                if (vec) {
+                    for (int c = 0; c < C; ++c) {
+                        const float4 u = __ldcs(reinterpret_cast<const float4*>(a + c * HW + p0));
+                        const float4 v = __ldcs(reinterpret_cast<const float4*>(b + c * HW + p0));
+                        if (MODE == 0) {
+                            flags |= (ref_changed(u.x, v.x, tau) ? 1u : 0u) | (ref_changed(u.y, v.y, tau) ? 2u : 0u) |
+                                     (ref_changed(u.z, v.z, tau) ? 4u : 0u) | (ref_changed(u.w, v.w, tau) ? 8u : 0u);
+                        } else {
+                            flags |= (__float_as_uint(u.x) != __float_as_uint(v.x) ? 1u : 0u) |
+                                     (__float_as_uint(u.y) != __float_as_uint(v.y) ? 2u : 0u) |
+                                     (__float_as_uint(u.z) != __float_as_uint(v.z) ? 4u : 0u) |
+                                     (__float_as_uint(u.w) != __float_as_uint(v.w) ? 8u : 0u);
+                        }
+                    }
+                } else {
+                    for (int e = 0; e < 4 && x0 + e < W; ++e)
+                        for (int c = 0; c < C; ++c) {
+                            const float u = a[c * HW + p0 + e], v = b[c * HW + p0 + e];
+                            const bool f = MODE == 0 ? ref_changed(u, v, tau) : (__float_as_uint(u) != __float_as_uint(v));
+                            flags |= f ? (1u << e) : 0u;
+                        }
+                }
+            }
+        }
+        uint32_t word = flags << (4 * (lane & 7));
+        word |= __shfl_xor_sync(0xffffffffu, word, 1);
+        word |= __shfl_xor_sync(0xffffffffu, word, 2);
+        word |= __shfl_xor_sync(0xffffffffu, word, 4);
+        if (act && (lane & 7) == 0) dst[q >> 3] = word;
+        if (cnt) {
+            const int n = __reduce_add_sync(0xffffffffu, __popc(flags));
+            if (lane == 0 && n) atomicAdd(cnt + (int64_t)s * cstride, (unsigned long long)n);
+        }
+    }
+}
+
+void launch_detect_bits(const float* const* cur, const float* const* prev, int S, int C, int H, int W, float tau,
+                        int mode, BitMask m, unsigned long long* cnt, int cstride, cudaStream_t st) {
+    const int64_t nq = (int64_t)H * m.wpr * 8;
+    int gx = (int)((nq + 255) / 256);
+    const int cap = (kNumSMs * 8 + S - 1) / S;
+    if (gx > cap) gx = cap < 1 ? 1 : cap;
+    dim3 grid(gx, S);
+    if (mode == 0)
+        detect_bits_kernel<0><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
+    else
+        detect_bits_kernel<1><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
+}
+
+// ---------------------------------------------------------------------------
+// K3+K2 fused, stride-1 geometries: each thread owns one output word (32
+// output pixels of a row): vertical OR over kh input rows of the horizontally
+// dilated row slices (funnel shifts over the neighbouring words), optional
+// write of the dilated word (the layer's updated-pixel mask), then
+// single-pass stream compaction with decoupled look-back. Tiles of 256 words
+// never straddle a stream (stride is a multiple of 256 words).
+constexpr int kDcThreads = 256;
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPre = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint32_t hslice(uint32_t prev, uint32_t cur, uint32_t next, int t) {
+    // bits of the input row at output positions x + t, x in this word
+    if (t == 0) return cur;
+    if (t > 0) return __funnelshift_r(cur, next, t);
+    return __funnelshift_l(prev, cur, -t);
+}
+
+// Returns the block-exclusive prefix of `my` and the block total (all threads).
+__device__ __forceinline__ int block_scan(int my, int* s_warp, int& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = my;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int x = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
+        }
+        if (lane < (int)(blockDim.x >> 5)) s_warp[lane] = x;
+    }
+    __syncthreads();
+    total = s_warp[(blockDim.x >> 5) - 1];
+    return (warp ? s_warp[warp - 1] : 0) + incl - my;
+}
+
+// Decoupled look-back by warp 0; returns the exclusive global prefix of `tile`.
+__device__ __forceinline__ long long lookback(unsigned long long* status, unsigned tile, int agg) {
+    const int lane = threadIdx.x & 31;
+    long long base = 0;
+    if (tile == 0) {
+        if (lane == 0) atomicExch(status, kFlagPre | (unsigned long long)agg);
+        return 0;
+    }
+    if (lane == 0) atomicExch(status + tile, kFlagAgg | (unsigned long long)agg);
+    long long pos = (long long)tile - 1;
+    while (true) {
+        const long long j = pos - lane;
+        unsigned long long st = kFlagPre;
+        if (j >= 0) {
+            do {
+                st = atomicAdd(status + j, 0ull);
+            } while ((st >> 62) == 0);
+        }
+        const unsigned pre = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        const int stop = pre ? __ffs(pre) - 1 : 32;
+        long long val = (lane <= stop) ? (long long)(st & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        base += val;
+        if (pre) break;
+        pos -= 32;
+    }
+    if (lane == 0) atomicExch(status + tile, kFlagPre | (unsigned long long)(base + agg));
+    return base;
+}
+
+__global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, BitMask out, bool write_out,
+                                                                    int kh, int kw, int ph, int pw, bool identity,
+                                                                    int32_t* __restrict__ idx, int* total,
+                                                                    unsigned long long* status, unsigned* tile_counter,
+                                                                    unsigned long long* cnt, int cstride) {
+    __shared__ unsigned s_tile;
+    __shared__ int s_warp[kDcThreads / 32];
+    __shared__ long long s_base;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const int tps = (int)(out.stride / kDcThreads);
+    const int s = tile / tps;
+    const int64_t wi = (int64_t)(tile - (unsigned)s * tps) * kDcThreads + threadIdx.x;
+    const int y = (int)(wi / out.wpr), w = (int)(wi - (int64_t)(wi / out.wpr) * out.wpr);
+    uint32_t word = 0;
+    if (y < out.H) {
+        const uint32_t* src = in.d + (int64_t)s * in.stride;
+        if (identity) {
+            word = src[(int64_t)y * in.wpr + w];
+        } else {
+            for (int kj = 0; kj < kh; ++kj) {
+                const int yy = y - ph + kj;
+                if (yy < 0 || yy >= in.H) continue;
+                const uint32_t* row = src + (int64_t)yy * in.wpr;
+                const uint32_t prev = w > 0 && w - 1 < in.wpr ? row[w - 1] : 0u;
+                const uint32_t cur = w < in.wpr ? row[w] : 0u;
+                const uint32_t next = w + 1 < in.wpr ? row[w + 1] : 0u;
+                for (int d = 0; d < kw; ++d) word |= hslice(prev, cur, next, d - pw);
+            }
+        }
+        const int rem = out.W - 32 * w;
+        if (rem < 32) word &= rem > 0 ? ((1u << rem) - 1u) : 0u;
+    }
+    if (write_out) out.d[(int64_t)s * out.stride + wi] = word;
+    int agg;
+    const int my = __popc(word);
+    const int excl = block_scan(my, s_warp, agg);
+    if (threadIdx.x < 32) {
+        const long long b = lookback(status, tile, agg);
+        if (threadIdx.x == 0) {
+            s_base = b;
+            if (agg) {
+                atomicAdd(total, agg);
+                if (cnt) atomicAdd(cnt + (int64_t)s * cstride, (unsigned long long)agg);
+            }
+        }
+    }
+    __syncthreads();
+    int64_t o = s_base + excl;
+    const int64_t gbase = (int64_t)s * out.H * out.W + (int64_t)y * out.W + 32 * w;
+    while (word) {
+        const int k = __ffs(word) - 1;
+        word &= word - 1;
+        idx[o++] = (int32_t)(gbase + k);
+    }
+}
+
+size_t dilate_compact_workspace(const BitMask& out, int S) {
+    const int64_t tiles = (int64_t)S * (out.stride / kDcThreads);
+    return (size_t)round_up(tiles * 8 + 16, 256);
+}
+
+void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw,
+                           int32_t* idx, int* total, void* workspace, unsigned long long* cnt, int cstride,
+                           cudaStream_t st) {
+    const int64_t tiles = (int64_t)S * (out.stride / kDcThreads);
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(workspace);
+    unsigned* counter = reinterpret_cast<unsigned*>(status + tiles);
+    const bool identity = kh == 1 && kw == 1 && ph == 0 && pw == 0;
+    cudaMemsetAsync(workspace, 0, tiles * 8 + 16, st);
+    cudaMemsetAsync(total, 0, sizeof(int), st);
+    dilate_compact_kernel<<<(unsigned)tiles, kDcThreads, 0, st>>>(in, out, write_out, kh, kw, ph, pw, identity, idx,
+                                                                   total, status, counter, cnt, cstride);
+}
+
+// ---------------------------------------------------------------------------
+// Generic dilation (any stride): one thread per output word; every output
+// pixel ORs its zero-padded receptive field via bit tests.
+__global__ void dilate_bits_kernel(BitMask in, BitMask out, int kh, int kw, int sh, int sw, int ph, int pw) {
+    const int s = blockIdx.y;
+    const int64_t nw = (int64_t)out.H * out.wpr;
+    for (int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += (int64_t)gridDim.x * blockDim.x) {
+        const int y = (int)(wi / out.wpr), w = (int)(wi % out.wpr);
+        uint32_t word = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int x = 32 * w + b;
+            if (x >= out.W) break;
+            bool any = false;
+            for (int kj = 0; kj < kh && !any; ++kj) {
+                const int yy = y * sh - ph + kj;
+                if (yy < 0 || yy >= in.H) continue;
+                for (int ki = 0; ki < kw; ++ki) {
+                    const int xx = x * sw - pw + ki;
+                    if (xx >= 0 && xx < in.W && bit_test(in, s, yy, xx)) {
+                        any = true;
+                        break;
+                    }
+                }
+            }
+            word |= any ? (1u << b) : 0u;
+        }
+        out.d[(int64_t)s * out.stride + wi] = word;
+    }
+}
+
+void launch_dilate_bits(BitMask in, BitMask out, int S, int kh, int kw, int sh, int sw, int ph, int pw,
+                        cudaStream_t st) {
+    const int64_t nw = (int64_t)out.H * out.wpr;
+    int gx = (int)std::min<int64_t>((nw + 127) / 128, 4096);
+    dilate_bits_kernel<<<dim3(gx < 1 ? 1 : gx, S), 128, 0, st>>>(in, out, kh, kw, sh, sw, ph, pw);
+}
+
+// ---------------------------------------------------------------------------
+// K5: max-pool (window/stride) or ReLU (window 1) recomputed for the output
+// pixels whose input window holds an updated pixel, compare-before-write
+// feeding the next CBCONV's change mask. A block handles one output word (32
+// pixels of a row) at a time; its threads sweep (pixel, 4-channel) items so
+// that neighbouring threads read neighbouring 16-byte chunks.
+constexpr int kPtThreads = 128;
+
+__global__ void __launch_bounds__(kPtThreads) point_bits_kernel(PointBitsArgs a) {
+    __shared__ uint32_t s_touched, s_changed;
+    const int Ho = a.out.H, Wo = a.out.W;
+    const int wpr = (Wo + 31) / 32;
+    const int64_t nseg = (int64_t)a.S * Ho * wpr;
+    const int c4n = a.in.Cp / 4;
+    const int lane = threadIdx.x & 31;
+    for (int64_t seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
+        const int s = (int)(seg / ((int64_t)Ho * wpr));
+        const int64_t r = seg - (int64_t)s * Ho * wpr;
+        const int y = (int)(r / wpr), w = (int)(r - (int64_t)(r / wpr) * wpr);
+        if (threadIdx.x < 32) {
+            const int x = 32 * w + lane;
+            bool t = x < Wo;
+            if (t && a.upd_in.d) {
+                bool any = false;
+                for (int kj = 0; kj < a.window && !any; ++kj)
+                    for (int ki = 0; ki < a.window; ++ki)
+                        if (bit_test(a.upd_in, s, y * a.stride + kj, x * a.stride + ki)) {
+                            any = true;
+                            break;
+                        }
+                t = any;
+            }
+            const uint32_t tw = __ballot_sync(0xffffffffu, t);
+            if (lane == 0) {
+                s_touched = tw;
+                s_changed = 0;
+            }
+        }
+        __syncthreads();
+        const uint32_t tw = s_touched;
+        if (tw) {
+            const int items = 32 * c4n;
+            for (int it = threadIdx.x; it < items; it += kPtThreads) {
+                const int j = it / c4n, c4 = it - j * c4n;
+                if (!((tw >> j) & 1u)) continue;
+                const int x = 32 * w + j;
+                const float4* src = reinterpret_cast<const float4*>(
+                    a.in.d + (int64_t)s * a.in.ss +
+                    ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
+                float4* dst = reinterpret_cast<float4*>(
+                    a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp) + c4;
+                float4 m;
+                if (a.relu) {
+                    const float4 v = *src;
+                    m = make_float4(ref_relu(v.x), ref_relu(v.y), ref_relu(v.z), ref_relu(v.w));
+                } else {
+                    m = *src;
+                    const int rowq = a.in.Wp * c4n;
+                    for (int kj = 0; kj < a.window; ++kj)
+                        for (int ki = 0; ki < a.window; ++ki) {
+                            const float4 v = src[kj * rowq + ki * c4n];
+                            m = make_float4(ref_max(m.x, v.x), ref_max(m.y, v.y), ref_max(m.z, v.z), ref_max(m.w, v.w));
+                        }
+                }
+                if (a.chg.d) {
+                    const float4 o = *dst;
+                    if (ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
+                        ref_changed(m.w, o.w, a.tau))
+                        atomicOr(&s_changed, 1u << j);
+                }
+                *dst = m;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int64_t wo = (int64_t)s * a.U_out.stride + (int64_t)y * wpr + w;
+            if (a.U_out.d) a.U_out.d[wo] = tw;
+            if (a.chg.d) {
+                a.chg.d[(int64_t)s * a.chg.stride + (int64_t)y * wpr + w] = s_changed;
+                if (a.chg_cnt && s_changed) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, (unsigned long long)__popc(s_changed));
+            }
+        }
+        __syncthreads();
+    }
+}
+
+void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
+    const int wpr = (a.out.W + 31) / 32;
+    const int64_t nseg = (int64_t)a.S * a.out.H * wpr;
+    int grid = (int)std::min<int64_t>(nseg, (int64_t)kNumSMs * 16);
+    point_bits_kernel<<<grid < 1 ? 1 : grid, kPtThreads, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) classify_bits_kernel(TensorView in, BitMask upd, uint16_t* labels, int S) {
+    const int H = in.H, W = in.W;
+    const int64_t HW = (int64_t)H * W, total = HW * S;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(i / HW);
+        const int p = (int)(i - (int64_t)s * HW);
+        const int y = p / W, x = p - (p / W) * W;
+        if (upd.d && !bit_test(upd, s, y, x)) continue;
+        const float* src = in.d + (int64_t)s * in.ss + ((int64_t)(y + in.hh) * in.Wp + x + in.hw) * in.Cp;
+        int best = 0;
+        float bv = src[0];
+        for (int c = 1; c < in.C; ++c) {
+            const float v = src[c];
+            if (v > bv) {
+                bv = v;
+                best = c;
+            }
+        }
+        labels[i] = (uint16_t)best;
+    }
+}
+
+void launch_classify_bits(TensorView in, BitMask upd, uint16_t* labels, int S, cudaStream_t st) {
+    const int64_t total = (int64_t)in.H * in.W * S;
+    int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
+    classify_bits_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(in, upd, labels, S);
+}
+
+// Unpacks one stream of a bit mask into bytes (trace readback).
+__global__ void unpack_bits_kernel(BitMask m, int s, uint8_t* out) {
+    const int64_t n = (int64_t)m.H * m.W;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int y = (int)(i / m.W), x = (int)(i % m.W);
+        out[i] = bit_test(m, s, y, x) ? 1 : 0;
+    }
+}
+
+void launch_unpack_bits(BitMask m, int s, uint8_t* out, cudaStream_t st) {
+    const int64_t n = (int64_t)m.H * m.W;
+    int grid = (int)std::min<int64_t>((n + 255) / 256, 4096);
+    unpack_bits_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(m, s, out);
+}
+
+}  // namespace cbx

@@ -19,11 +19,13 @@
 
 namespace cbx {
 
-constexpr int kConvThreads = 128, kConvOC = 16, kConvKC = 128;
+constexpr int kConvThreads = 128, kConvKC = 256;
 
-template <bool PLANAR>
+// kConvOC output channels per pass: 4 for the paper's first layer (3->4),
+// 8 or 16 otherwise, so no accumulator is wasted on padding.
+template <bool PLANAR, int kConvOC>
 __global__ void __launch_bounds__(kConvThreads) conv_exact_kernel(ConvArgs a) {
-    __shared__ float sW[kConvOC][kConvKC];
+    __shared__ __align__(16) float sW[kConvKC][kConvOC];  // r-major: the OC weights of one tap are one 16B-vector load
     const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
     const int64_t ntiles = (total + kConvThreads - 1) / kConvThreads;
     const int Ho = a.out.H, Wo = a.out.W, O = a.out.C;
@@ -54,7 +56,7 @@ __global__ void __launch_bounds__(kConvThreads) conv_exact_kernel(ConvArgs a) {
                 __syncthreads();
                 for (int t = threadIdx.x; t < kConvOC * kConvKC; t += kConvThreads) {
                     const int j = t / kConvKC, r = t - j * kConvKC;
-                    sW[j][r] = (o0 + j < O && r0 + r < Kdim) ? a.K[(int64_t)(o0 + j) * Kdim + r0 + r] : 0.0f;
+                    sW[r][j] = (o0 + j < O && r0 + r < Kdim) ? a.K[(int64_t)(o0 + j) * Kdim + r0 + r] : 0.0f;
                 }
                 __syncthreads();
                 if (!valid) continue;
@@ -73,8 +75,15 @@ __global__ void __launch_bounds__(kConvThreads) conv_exact_kernel(ConvArgs a) {
                     } else {
                         v = __ldg(src + ((int64_t)kj * a.in.Wp + ki) * a.in.Cp + c);
                     }
+                    const float4* w4 = reinterpret_cast<const float4*>(sW[r - r0]);
 #pragma unroll
-                    for (int j = 0; j < kConvOC; ++j) acc[j] = __fadd_rn(acc[j], __fmul_rn(sW[j][r - r0], v));
+                    for (int q = 0; q < kConvOC / 4; ++q) {
+                        const float4 wq = w4[q];
+                        acc[4 * q + 0] = __fadd_rn(acc[4 * q + 0], __fmul_rn(wq.x, v));
+                        acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(wq.y, v));
+                        acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(wq.z, v));
+                        acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(wq.w, v));
+                    }
                     if (++ki == a.kw) {
                         ki = 0;
                         if (++kj == a.kh) {
@@ -95,20 +104,30 @@ __global__ void __launch_bounds__(kConvThreads) conv_exact_kernel(ConvArgs a) {
             }
         }
         if (a.chg.d) {
-            if (valid && changed) a.chg.d[(int64_t)s * a.chg.stride + p] = 1;
+            if (valid && changed) bit_set(a.chg, s, y, x);
             if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
         }
     }
 }
 
+template <int OC>
+static void launch_conv_exact_oc(const ConvArgs& a, int grid, cudaStream_t st) {
+    if (a.in_ptrs)
+        conv_exact_kernel<true, OC><<<grid, kConvThreads, 0, st>>>(a);
+    else
+        conv_exact_kernel<false, OC><<<grid, kConvThreads, 0, st>>>(a);
+}
+
 void launch_conv_exact(const ConvArgs& a, cudaStream_t st) {
     const int64_t max_tiles = (a.full_count + kConvThreads - 1) / kConvThreads;
-    int grid = (int)std::min<int64_t>(max_tiles, (int64_t)kNumSMs * 8);
+    int grid = (int)std::min<int64_t>(max_tiles, (int64_t)kNumSMs * 12);
     if (grid < 1) grid = 1;
-    if (a.in_ptrs)
-        conv_exact_kernel<true><<<grid, kConvThreads, 0, st>>>(a);
+    if (a.out.C <= 4)
+        launch_conv_exact_oc<4>(a, grid, st);
+    else if (a.out.C <= 8)
+        launch_conv_exact_oc<8>(a, grid, st);
     else
-        conv_exact_kernel<false><<<grid, kConvThreads, 0, st>>>(a);
+        launch_conv_exact_oc<16>(a, grid, st);
 }
 
 // ---------------------------------------------------------------------------

@@ -4,11 +4,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cbx {
 
-// ---- k_change.cu ----
+// ---- k_change.cu: byte-mask kernels behind the op-level C-ABI (cbx_op_*) ----
 void launch_detect_planar(const float* const* cur, const float* const* prev, int S, int C, int H,
                           int W, float tau, int mode, MaskView m, unsigned long long* cnt,
                           int cstride, cudaStream_t st);
@@ -18,9 +20,34 @@ size_t compact_workspace_bytes(int S, int64_t N);
 void launch_compact(MaskView m, int S, int32_t* idx, int* total, void* workspace,
                     unsigned long long* cnt, int cstride, cudaStream_t st);
 
+// ---- k_bits.cu: the engine's packed-bit mask pipeline ----
+void launch_detect_bits(const float* const* cur, const float* const* prev, int S, int C, int H, int W, float tau,
+                        int mode, BitMask m, unsigned long long* cnt, int cstride, cudaStream_t st);
+size_t dilate_compact_workspace(const BitMask& out, int S);
+void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw,
+                           int32_t* idx, int* total, void* workspace, unsigned long long* cnt, int cstride,
+                           cudaStream_t st);
+void launch_dilate_bits(BitMask in, BitMask out, int S, int kh, int kw, int sh, int sw, int ph, int pw,
+                        cudaStream_t st);
+
+struct PointBitsArgs {  // MAXPOOL (window/stride) or RELU (relu=1, window=stride=1)
+    TensorView in, out;
+    int window, stride, relu;
+    BitMask upd_in;   // updated pixels of the input grid; d == nullptr => all
+    BitMask U_out;    // touched output pixels (optional)
+    BitMask chg;      // consumer CBCONV change mask (optional)
+    float tau;
+    unsigned long long* chg_cnt;
+    int cnt_stride;
+    int S;
+};
+void launch_point_bits(const PointBitsArgs& a, cudaStream_t st);
+void launch_classify_bits(TensorView in, BitMask upd, uint16_t* labels, int S, cudaStream_t st);
+void launch_unpack_bits(BitMask m, int s, uint8_t* out, cudaStream_t st);
+
 // ---- k_layers.cu ----
 // Gathered convolution over an output-pixel list (or all pixels when idx is
-// null), result written in place into the output tensor.
+// null), exact fp32 reference order, result written in place.
 struct ConvArgs {
     // input: HWC tensor, or the planar frame table when in_ptrs != nullptr
     TensorView in;
@@ -34,7 +61,7 @@ struct ConvArgs {
     int64_t full_count;  // S*Ho*Wo
     int relu;
     // change test of the consumer CBCONV (compare new vs stored value)
-    MaskView chg;        // chg.d == nullptr => no test
+    BitMask chg;         // chg.d == nullptr => no test
     float tau;
     unsigned long long* chg_cnt;
     int cnt_stride;
@@ -42,14 +69,15 @@ struct ConvArgs {
 };
 void launch_conv_exact(const ConvArgs& a, cudaStream_t st);
 
+// byte-mask pool / classify used by the op-level API
 struct PoolArgs {
     TensorView in, out;
     int window, stride;
-    const uint8_t* upd_in;  // updated mask of the input grid; null => all pixels
+    const uint8_t* upd_in;
     int64_t upd_in_stride;
-    uint8_t* upd_out;       // touched mask of the output grid (optional)
+    uint8_t* upd_out;
     int64_t upd_out_stride;
-    MaskView chg;           // consumer CBCONV change mask (optional)
+    MaskView chg;
     float tau;
     unsigned long long* chg_cnt;
     int cnt_stride;
@@ -57,15 +85,15 @@ struct PoolArgs {
 };
 void launch_pool(const PoolArgs& a, cudaStream_t st);
 
-struct PointArgs {  // RELU / CLASSIFY over updated pixels
+struct PointArgs {
     TensorView in, out;
-    const uint8_t* upd;  // null => all
+    const uint8_t* upd;
     int64_t upd_stride;
     MaskView chg;
     float tau;
     unsigned long long* chg_cnt;
     int cnt_stride;
-    uint16_t* labels;    // CLASSIFY output [S][H][W]
+    uint16_t* labels;
     int S;
 };
 void launch_relu(const PointArgs& a, cudaStream_t st);
@@ -77,15 +105,12 @@ void launch_chw_to_hwc(const float* in, TensorView t, int s, cudaStream_t st);
 // planar frames (device pointer table) -> channels-last tensor, all streams
 void launch_ingest(const float* const* frames, TensorView t, int S, cudaStream_t st);
 
-// ---- k_synth.cu ----
+// ---- synthetic frames ----
 struct SpriteRect {
     int y0, x0, y1, x1;
     float v;
 };
 void launch_synth_frame(float* out, int C, int H, int W, const SpriteRect* rects_dev, int n,
                         cudaStream_t st);
-
-// ---- k_conv_tc.cu (tcgen05) ----
-struct TcConvArgs;  // defined in conv_tc.hpp
 
 }  // namespace cbx
