@@ -32,7 +32,7 @@ struct MaskView {
 // Packed bit mask on a pixel grid (the engine's change / updated-pixel masks):
 // [S][stride] 32-bit words, row y occupies words [y*wpr, (y+1)*wpr), pixel x
 // is bit (x & 31) of word x >> 5; bits past W are always zero. stride is a
-// multiple of 256 words so compaction tiles never straddle two streams.
+// multiple of 2048 words so compaction tiles never straddle two streams.
 struct BitMask {
     uint32_t* d;
     int H, W, wpr;

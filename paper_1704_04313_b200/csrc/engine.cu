@@ -162,7 +162,7 @@ struct Engine::Plan {
     }
     BitMask mask(int S, int H, int W) {
         const int wpr = (W + 31) / 32;
-        BitMask m{nullptr, H, W, wpr, round_up((int64_t)H * wpr, 256)};
+        BitMask m{nullptr, H, W, wpr, round_up((int64_t)H * wpr, 2048)};
         m.d = alloc<uint32_t>((size_t)(m.stride * S));
         return m;
     }
@@ -368,7 +368,7 @@ void Engine::build_plan(Plan& p, bool baseline) {
         p.idx[k] = p.alloc<int32_t>((size_t)S * Ho * Wo);
         p.cnt[k] = p.alloc<int>(1);
         const int wpr = (Wo + 31) / 32;
-        ws = std::max(ws, dilate_compact_workspace(BitMask{nullptr, Ho, Wo, wpr, round_up((int64_t)Ho * wpr, 256)}, S));
+        ws = std::max(ws, dilate_compact_workspace(BitMask{nullptr, Ho, Wo, wpr, round_up((int64_t)Ho * wpr, 2048)}, S));
         // strided geometries dilate separately, then compact the dilated mask
         if (!identity_geom(l.geom) && (l.geom.strideH != 1 || l.geom.strideW != 1 || l.geom.kernelW - 1 - l.geom.padW > 31 ||
                                        l.geom.padW > 31) && !p.U[k].d)

@@ -23,7 +23,7 @@ namespace cbx {
 // K1: detection on the planar frames, 4 pixels per thread (128-bit loads of
 // every channel plane of both frames), packed with warp shuffles into words.
 template <int MODE>
-__global__ void __launch_bounds__(256) detect_bits_kernel(const float* const* cur, const float* const* prev, int C,
+__global__ void __launch_bounds__(256, 4) detect_bits_kernel(const float* const* cur, const float* const* prev, int C,
                                                           int H, int W, float tau, BitMask m,
                                                           unsigned long long* cnt, int cstride) {
     const int s = blockIdx.y;
@@ -150,7 +150,7 @@ __device__ __forceinline__ long long lookback(unsigned long long* status, unsign
         unsigned long long st = kFlagPre;
         if (j >= 0) {
             do {
-                st = atomicAdd(status + j, 0ull);
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(st) : "l"(status + j) : "memory");
             } while ((st >> 62) == 0);
         }
         const unsigned pre = __ballot_sync(0xffffffffu, (st >> 62) == 2);
@@ -166,6 +166,32 @@ __device__ __forceinline__ long long lookback(unsigned long long* status, unsign
     return base;
 }
 
+constexpr int kDcWords = 8;  // words per thread; a tile is kDcThreads * kDcWords words
+
+__device__ __forceinline__ uint32_t dilated_word(const BitMask& in, const BitMask& out, int s, int64_t wi, int kh,
+                                                 int kw, int ph, int pw, bool identity) {
+    const int y = (int)(wi / out.wpr), w = (int)(wi - (int64_t)(wi / out.wpr) * out.wpr);
+    if (y >= out.H) return 0u;
+    const uint32_t* src = in.d + (int64_t)s * in.stride;
+    uint32_t word = 0;
+    if (identity) {
+        word = src[(int64_t)y * in.wpr + w];
+    } else {
+        for (int kj = 0; kj < kh; ++kj) {
+            const int yy = y - ph + kj;
+            if (yy < 0 || yy >= in.H) continue;
+            const uint32_t* row = src + (int64_t)yy * in.wpr;
+            const uint32_t prev = w > 0 && w - 1 < in.wpr ? __ldg(row + w - 1) : 0u;
+            const uint32_t cur = w < in.wpr ? __ldg(row + w) : 0u;
+            const uint32_t next = w + 1 < in.wpr ? __ldg(row + w + 1) : 0u;
+            for (int d = 0; d < kw; ++d) word |= hslice(prev, cur, next, d - pw);
+        }
+    }
+    const int rem = out.W - 32 * w;
+    if (rem < 32) word &= rem > 0 ? ((1u << rem) - 1u) : 0u;
+    return word;
+}
+
 __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, BitMask out, bool write_out,
                                                                     int kh, int kw, int ph, int pw, bool identity,
                                                                     int32_t* __restrict__ idx, int* total,
@@ -177,32 +203,22 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
-    const int tps = (int)(out.stride / kDcThreads);
+    const int tps = (int)(out.stride / (kDcThreads * kDcWords));
     const int s = tile / tps;
-    const int64_t wi = (int64_t)(tile - (unsigned)s * tps) * kDcThreads + threadIdx.x;
-    const int y = (int)(wi / out.wpr), w = (int)(wi - (int64_t)(wi / out.wpr) * out.wpr);
-    uint32_t word = 0;
-    if (y < out.H) {
-        const uint32_t* src = in.d + (int64_t)s * in.stride;
-        if (identity) {
-            word = src[(int64_t)y * in.wpr + w];
-        } else {
-            for (int kj = 0; kj < kh; ++kj) {
-                const int yy = y - ph + kj;
-                if (yy < 0 || yy >= in.H) continue;
-                const uint32_t* row = src + (int64_t)yy * in.wpr;
-                const uint32_t prev = w > 0 && w - 1 < in.wpr ? row[w - 1] : 0u;
-                const uint32_t cur = w < in.wpr ? row[w] : 0u;
-                const uint32_t next = w + 1 < in.wpr ? row[w + 1] : 0u;
-                for (int d = 0; d < kw; ++d) word |= hslice(prev, cur, next, d - pw);
-            }
-        }
-        const int rem = out.W - 32 * w;
-        if (rem < 32) word &= rem > 0 ? ((1u << rem) - 1u) : 0u;
+    const int64_t w0 = (int64_t)(tile - (unsigned)s * tps) * (kDcThreads * kDcWords) + (int64_t)threadIdx.x * kDcWords;
+    uint32_t words[kDcWords];
+    int my = 0;
+#pragma unroll
+    for (int i = 0; i < kDcWords; ++i) {
+        words[i] = dilated_word(in, out, s, w0 + i, kh, kw, ph, pw, identity);
+        my += __popc(words[i]);
     }
-    if (write_out) out.d[(int64_t)s * out.stride + wi] = word;
+    if (write_out) {
+        uint4* o4 = reinterpret_cast<uint4*>(out.d + (int64_t)s * out.stride + w0);
+        o4[0] = make_uint4(words[0], words[1], words[2], words[3]);
+        o4[1] = make_uint4(words[4], words[5], words[6], words[7]);
+    }
     int agg;
-    const int my = __popc(word);
     const int excl = block_scan(my, s_warp, agg);
     if (threadIdx.x < 32) {
         const long long b = lookback(status, tile, agg);
@@ -216,23 +232,31 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
     }
     __syncthreads();
     int64_t o = s_base + excl;
-    const int64_t gbase = (int64_t)s * out.H * out.W + (int64_t)y * out.W + 32 * w;
-    while (word) {
-        const int k = __ffs(word) - 1;
-        word &= word - 1;
-        idx[o++] = (int32_t)(gbase + k);
+    const int64_t sbase = (int64_t)s * out.H * out.W;
+#pragma unroll
+    for (int i = 0; i < kDcWords; ++i) {
+        uint32_t word = words[i];
+        if (!word) continue;
+        const int64_t wi = w0 + i;
+        const int y = (int)(wi / out.wpr), w = (int)(wi - (int64_t)(wi / out.wpr) * out.wpr);
+        const int64_t gbase = sbase + (int64_t)y * out.W + 32 * w;
+        while (word) {
+            const int k = __ffs(word) - 1;
+            word &= word - 1;
+            idx[o++] = (int32_t)(gbase + k);
+        }
     }
 }
 
 size_t dilate_compact_workspace(const BitMask& out, int S) {
-    const int64_t tiles = (int64_t)S * (out.stride / kDcThreads);
+    const int64_t tiles = (int64_t)S * (out.stride / (kDcThreads * kDcWords));
     return (size_t)round_up(tiles * 8 + 16, 256);
 }
 
 void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw,
                            int32_t* idx, int* total, void* workspace, unsigned long long* cnt, int cstride,
                            cudaStream_t st) {
-    const int64_t tiles = (int64_t)S * (out.stride / kDcThreads);
+    const int64_t tiles = (int64_t)S * (out.stride / (kDcThreads * kDcWords));
     unsigned long long* status = reinterpret_cast<unsigned long long*>(workspace);
     unsigned* counter = reinterpret_cast<unsigned*>(status + tiles);
     const bool identity = kh == 1 && kw == 1 && ph == 0 && pw == 0;
@@ -285,51 +309,52 @@ void launch_dilate_bits(BitMask in, BitMask out, int S, int kh, int kw, int sh, 
 // feeding the next CBCONV's change mask. A block handles one output word (32
 // pixels of a row) at a time; its threads sweep (pixel, 4-channel) items so
 // that neighbouring threads read neighbouring 16-byte chunks.
-constexpr int kPtThreads = 128;
+constexpr int kPtThreads = 256;
 
+// One warp per output word (32 pixels of a row). Lanes first test their
+// pixel's input window against the updated mask (ballot -> touched word);
+// untouched words cost one mask probe and one store. Touched pixels are then
+// swept as (pixel, 4-channel) items so that neighbouring lanes read
+// neighbouring 16-byte chunks of the channels-last input.
 __global__ void __launch_bounds__(kPtThreads) point_bits_kernel(PointBitsArgs a) {
-    __shared__ uint32_t s_touched, s_changed;
+    __shared__ uint32_t s_changed[kPtThreads / 32];
     const int Ho = a.out.H, Wo = a.out.W;
     const int wpr = (Wo + 31) / 32;
     const int64_t nseg = (int64_t)a.S * Ho * wpr;
     const int c4n = a.in.Cp / 4;
-    const int lane = threadIdx.x & 31;
-    for (int64_t seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t warps = (int64_t)gridDim.x * (kPtThreads / 32);
+    for (int64_t seg = (int64_t)blockIdx.x * (kPtThreads / 32) + wib; seg < nseg; seg += warps) {
         const int s = (int)(seg / ((int64_t)Ho * wpr));
         const int64_t r = seg - (int64_t)s * Ho * wpr;
         const int y = (int)(r / wpr), w = (int)(r - (int64_t)(r / wpr) * wpr);
-        if (threadIdx.x < 32) {
-            const int x = 32 * w + lane;
-            bool t = x < Wo;
-            if (t && a.upd_in.d) {
-                bool any = false;
-                for (int kj = 0; kj < a.window && !any; ++kj)
-                    for (int ki = 0; ki < a.window; ++ki)
-                        if (bit_test(a.upd_in, s, y * a.stride + kj, x * a.stride + ki)) {
-                            any = true;
-                            break;
-                        }
-                t = any;
-            }
-            const uint32_t tw = __ballot_sync(0xffffffffu, t);
-            if (lane == 0) {
-                s_touched = tw;
-                s_changed = 0;
-            }
+        const int x = 32 * w + lane;
+        bool t = x < Wo;
+        if (t && a.upd_in.d) {
+            bool any = false;
+            for (int kj = 0; kj < a.window && !any; ++kj)
+                for (int ki = 0; ki < a.window; ++ki)
+                    if (bit_test(a.upd_in, s, y * a.stride + kj, x * a.stride + ki)) {
+                        any = true;
+                        break;
+                    }
+            t = any;
         }
-        __syncthreads();
-        const uint32_t tw = s_touched;
+        const uint32_t tw = __ballot_sync(0xffffffffu, t);
+        uint32_t cw = 0;
         if (tw) {
+            if (lane == 0) s_changed[wib] = 0;
+            __syncwarp();
             const int items = 32 * c4n;
-            for (int it = threadIdx.x; it < items; it += kPtThreads) {
+            for (int it = lane; it < items; it += 32) {
                 const int j = it / c4n, c4 = it - j * c4n;
                 if (!((tw >> j) & 1u)) continue;
-                const int x = 32 * w + j;
+                const int xj = 32 * w + j;
                 const float4* src = reinterpret_cast<const float4*>(
                     a.in.d + (int64_t)s * a.in.ss +
-                    ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
+                    ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + xj * a.stride + a.in.hw) * a.in.Cp) + c4;
                 float4* dst = reinterpret_cast<float4*>(
-                    a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp) + c4;
+                    a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + xj + a.out.hw) * a.out.Cp) + c4;
                 float4 m;
                 if (a.relu) {
                     const float4 v = *src;
@@ -347,28 +372,29 @@ __global__ void __launch_bounds__(kPtThreads) point_bits_kernel(PointBitsArgs a)
                     const float4 o = *dst;
                     if (ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
                         ref_changed(m.w, o.w, a.tau))
-                        atomicOr(&s_changed, 1u << j);
+                        atomicOr(&s_changed[wib], 1u << j);
                 }
                 *dst = m;
             }
+            __syncwarp();
+            cw = s_changed[wib];
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int64_t wo = (int64_t)s * a.U_out.stride + (int64_t)y * wpr + w;
-            if (a.U_out.d) a.U_out.d[wo] = tw;
+        if (lane == 0) {
+            if (a.U_out.d) a.U_out.d[(int64_t)s * a.U_out.stride + (int64_t)y * wpr + w] = tw;
             if (a.chg.d) {
-                a.chg.d[(int64_t)s * a.chg.stride + (int64_t)y * wpr + w] = s_changed;
-                if (a.chg_cnt && s_changed) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, (unsigned long long)__popc(s_changed));
+                a.chg.d[(int64_t)s * a.chg.stride + (int64_t)y * wpr + w] = cw;
+                if (a.chg_cnt && cw) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, (unsigned long long)__popc(cw));
             }
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
     const int wpr = (a.out.W + 31) / 32;
     const int64_t nseg = (int64_t)a.S * a.out.H * wpr;
-    int grid = (int)std::min<int64_t>(nseg, (int64_t)kNumSMs * 16);
+    const int64_t blocks = (nseg + kPtThreads / 32 - 1) / (kPtThreads / 32);
+    int grid = (int)std::min<int64_t>(blocks, (int64_t)kNumSMs * 8);
     point_bits_kernel<<<grid < 1 ? 1 : grid, kPtThreads, 0, st>>>(a);
 }
 

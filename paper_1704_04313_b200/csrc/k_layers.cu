@@ -110,9 +110,102 @@ __global__ void __launch_bounds__(kConvThreads) conv_exact_kernel(ConvArgs a) {
     }
 }
 
+// Planar-frame variant (the first layer): all filters of an output-channel
+// group resident in shared memory as r-major float4 vectors, one output pixel
+// per thread, the kw taps of a kernel row loaded together (predicated, up to
+// 8 in flight) before they are accumulated in reference order.
+template <int OC>
+__global__ void __launch_bounds__(kConvThreads) conv_planar_kernel(ConvArgs a) {
+    extern __shared__ float4 sWv[];  // [Kdim][OC/4]
+    const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
+    const int64_t ntiles = (total + kConvThreads - 1) / kConvThreads;
+    const int Wo = a.out.W, O = a.out.C, H = a.in.H, W = a.in.W;
+    const int64_t HoWo = (int64_t)a.out.H * Wo, HW = (int64_t)H * W;
+    const int Kdim = a.in.C * a.kh * a.kw;
+    const bool single = O <= OC;
+    auto load_w = [&](int o0) {
+        float* sw = reinterpret_cast<float*>(sWv);
+        for (int t = threadIdx.x; t < Kdim * OC; t += kConvThreads) {
+            const int r = t / OC, j = t - r * OC;
+            sw[t] = (o0 + j < O) ? a.K[(int64_t)(o0 + j) * Kdim + r] : 0.0f;
+        }
+    };
+    if (single) {
+        load_w(0);
+        __syncthreads();
+    }
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t n = tile * kConvThreads + threadIdx.x;
+        const bool valid = n < total;
+        const int64_t g = valid ? (a.idx ? (int64_t)a.idx[n] : n) : 0;
+        const int s = (int)(g / HoWo);
+        const int p = (int)(g - (int64_t)s * HoWo);
+        const int y = p / Wo, x = p - (p / Wo) * Wo;
+        const int y0 = y * a.sh - a.ph, x0 = x * a.sw - a.pw;
+        const float* src = a.in_ptrs[s];
+        float* dst = a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + (x + a.out.hw)) * a.out.Cp;
+        bool changed = false;
+        for (int o0 = 0; o0 < O; o0 += OC) {
+            if (!single) {
+                __syncthreads();
+                load_w(o0);
+                __syncthreads();
+            }
+            if (valid) {
+                float acc[OC];
+#pragma unroll
+                for (int j = 0; j < OC; ++j) acc[j] = (o0 + j < O) ? a.bias[o0 + j] : 0.0f;
+                const float4* wr = sWv;
+                for (int c = 0; c < a.in.C; ++c) {
+                    for (int kj = 0; kj < a.kh; ++kj) {
+                        const int yy = y0 + kj;
+                        const bool rowok = (unsigned)yy < (unsigned)H;
+                        const float* rowp = src + c * HW + (int64_t)(rowok ? yy : 0) * W;
+                        for (int ki0 = 0; ki0 < a.kw; ki0 += 8) {
+                            float v[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const int xx = x0 + ki0 + u;
+                                v[u] = (rowok && ki0 + u < a.kw && (unsigned)xx < (unsigned)W) ? __ldg(rowp + xx) : 0.0f;
+                            }
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                if (ki0 + u >= a.kw) break;
+#pragma unroll
+                                for (int q = 0; q < OC / 4; ++q) {
+                                    const float4 wq = wr[q];
+                                    acc[4 * q + 0] = __fadd_rn(acc[4 * q + 0], __fmul_rn(wq.x, v[u]));
+                                    acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(wq.y, v[u]));
+                                    acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(wq.z, v[u]));
+                                    acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(wq.w, v[u]));
+                                }
+                                wr += OC / 4;
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < OC; ++j) {
+                    if (o0 + j >= O) break;
+                    const float v = a.relu ? ref_relu(acc[j]) : acc[j];
+                    if (a.chg.d) changed |= ref_changed(v, dst[o0 + j], a.tau);
+                    dst[o0 + j] = v;
+                }
+            }
+        }
+        if (a.chg.d) {
+            if (valid && changed) bit_set(a.chg, s, y, x);
+            if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
+        }
+    }
+}
+
 template <int OC>
 static void launch_conv_exact_oc(const ConvArgs& a, int grid, cudaStream_t st) {
-    if (a.in_ptrs)
+    const size_t smem = (size_t)a.in.C * a.kh * a.kw * OC * sizeof(float);
+    if (a.in_ptrs && smem <= 48 * 1024)
+        conv_planar_kernel<OC><<<grid, kConvThreads, smem, st>>>(a);
+    else if (a.in_ptrs)
         conv_exact_kernel<true, OC><<<grid, kConvThreads, 0, st>>>(a);
     else
         conv_exact_kernel<false, OC><<<grid, kConvThreads, 0, st>>>(a);
