@@ -549,6 +549,9 @@ void Engine::launch(Plan& p, bool full) {
 
 void Engine::stage_frame_pointers(int engine, const float* const* cur, const float* const* prev) {
     (void)engine;
+    for (int s = 0; s < S_; ++s)
+        if (!cur[s] || reinterpret_cast<uintptr_t>(cur[s]) % 16)
+            throw Error(CBX_E_ARG, "frame pointers must be non-null and 16-byte aligned");
     std::vector<const float*> tbl(2 * (size_t)S_);
     for (int s = 0; s < S_; ++s) {
         tbl[s] = cur[s];

@@ -22,15 +22,15 @@ namespace cbx {
 // ---------------------------------------------------------------------------
 // K1: detection on the planar frames, 4 pixels per thread (128-bit loads of
 // every channel plane of both frames), packed with warp shuffles into words.
-template <int MODE>
-__global__ void __launch_bounds__(256, 4) detect_bits_kernel(const float* const* cur, const float* const* prev, int C,
+template <int MODE, bool VEC>
+__global__ void __launch_bounds__(256) detect_bits_kernel(const float* const* cur, const float* const* prev, int C,
                                                           int H, int W, float tau, BitMask m,
                                                           unsigned long long* cnt, int cstride) {
     const int s = blockIdx.y;
     const float* a = cur[s];
     const float* b = prev[s];
     const int64_t HW = (int64_t)H * W;
-    const bool vec = (W % 4 == 0) && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 16 == 0);
+    constexpr bool vec = VEC;
     const int qpr = m.wpr * 8;  // pixel quads per (padded) row
     const int64_t nq = (int64_t)H * qpr;
     const int lane = threadIdx.x & 31;
@@ -44,7 +44,8 @@ __global__ void __launch_bounds__(256, 4) detect_bits_kernel(const float* const*
             const int x0 = (int)(q - (int64_t)y * qpr) * 4;
             if (x0 < W) {
                 const int64_t p0 = (int64_t)y * W + x0;
-                if (vec) {
+                if constexpr (vec) {
+#pragma unroll 1
                     for (int c = 0; c < C; ++c) {
                         const float4 u = __ldcs(reinterpret_cast<const float4*>(a + c * HW + p0));
                         const float4 v = __ldcs(reinterpret_cast<const float4*>(b + c * HW + p0));
@@ -87,10 +88,16 @@ void launch_detect_bits(const float* const* cur, const float* const* prev, int S
     const int cap = (kNumSMs * 8 + S - 1) / S;
     if (gx > cap) gx = cap < 1 ? 1 : cap;
     dim3 grid(gx, S);
-    if (mode == 0)
-        detect_bits_kernel<0><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
+    // frame pointers are 16-byte aligned (engine slots; checked for user frames in forward_device)
+    const bool vec = W % 4 == 0;
+    if (mode == 0 && vec)
+        detect_bits_kernel<0, true><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
+    else if (mode == 0)
+        detect_bits_kernel<0, false><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
+    else if (vec)
+        detect_bits_kernel<1, true><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
     else
-        detect_bits_kernel<1><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
+        detect_bits_kernel<1, false><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
 }
 
 // ---------------------------------------------------------------------------
@@ -168,50 +175,71 @@ __device__ __forceinline__ long long lookback(unsigned long long* status, unsign
 
 constexpr int kDcWords = 8;  // words per thread; a tile is kDcThreads * kDcWords words
 
-__device__ __forceinline__ uint32_t dilated_word(const BitMask& in, const BitMask& out, int s, int64_t wi, int kh,
-                                                 int kw, int ph, int pw, bool identity) {
-    const int y = (int)(wi / out.wpr), w = (int)(wi - (int64_t)(wi / out.wpr) * out.wpr);
-    if (y >= out.H) return 0u;
-    const uint32_t* src = in.d + (int64_t)s * in.stride;
-    uint32_t word = 0;
-    if (identity) {
-        word = src[(int64_t)y * in.wpr + w];
-    } else {
-        for (int kj = 0; kj < kh; ++kj) {
-            const int yy = y - ph + kj;
-            if (yy < 0 || yy >= in.H) continue;
-            const uint32_t* row = src + (int64_t)yy * in.wpr;
-            const uint32_t prev = w > 0 && w - 1 < in.wpr ? __ldg(row + w - 1) : 0u;
-            const uint32_t cur = w < in.wpr ? __ldg(row + w) : 0u;
-            const uint32_t next = w + 1 < in.wpr ? __ldg(row + w + 1) : 0u;
-            for (int d = 0; d < kw; ++d) word |= hslice(prev, cur, next, d - pw);
-        }
-    }
-    const int rem = out.W - 32 * w;
-    if (rem < 32) word &= rem > 0 ? ((1u << rem) - 1u) : 0u;
-    return word;
-}
-
+// Output words [w0, w0 + tile) of one stream need input rows
+// [y(w0) - ph, y(w0 + tile - 1) - ph + kh) -- one contiguous range of input
+// words, staged into shared memory with coalesced 16-byte loads so that the
+// 3*kh word reads per output word are shared-memory hits.
 __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, BitMask out, bool write_out,
                                                                     int kh, int kw, int ph, int pw, bool identity,
                                                                     int32_t* __restrict__ idx, int* total,
                                                                     unsigned long long* status, unsigned* tile_counter,
                                                                     unsigned long long* cnt, int cstride) {
+    extern __shared__ uint4 s_rows4[];
+    uint32_t* s_rows = reinterpret_cast<uint32_t*>(s_rows4);
     __shared__ unsigned s_tile;
     __shared__ int s_warp[kDcThreads / 32];
     __shared__ long long s_base;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
-    const int tps = (int)(out.stride / (kDcThreads * kDcWords));
+    constexpr int kTile = kDcThreads * kDcWords;
+    const int tps = (int)(out.stride / kTile);
     const int s = tile / tps;
-    const int64_t w0 = (int64_t)(tile - (unsigned)s * tps) * (kDcThreads * kDcWords) + (int64_t)threadIdx.x * kDcWords;
+    const int64_t t0 = (int64_t)(tile - (unsigned)s * tps) * kTile;
+    const int64_t w0 = t0 + (int64_t)threadIdx.x * kDcWords;
+    // stage input rows
+    const int ya = (int)(t0 / out.wpr);
+    const int yb = (int)((t0 + kTile - 1) / out.wpr);
+    const int ra = identity ? ya : max(0, ya - ph);
+    const int rb = identity ? min(in.H - 1, yb) : min(in.H - 1, yb - ph + kh - 1);
+    const uint32_t* src = in.d + (int64_t)s * in.stride;
+    const int64_t sw0 = (int64_t)ra * in.wpr;
+    const int nwords = rb >= ra ? (rb - ra + 1) * in.wpr : 0;
+    {
+        // 16-byte aligned window over [sw0, sw0 + nwords)
+        const int64_t a4 = sw0 & ~int64_t(3);
+        const int n4 = (int)((sw0 + nwords - a4 + 3) >> 2);
+        const uint4* g4 = reinterpret_cast<const uint4*>(src + a4);
+        for (int i = threadIdx.x; i < n4; i += kDcThreads) s_rows4[i] = __ldg(g4 + i);
+    }
+    __syncthreads();
+    const int shift = (int)(sw0 & 3);  // s_rows[shift + (word - sw0)]
     uint32_t words[kDcWords];
     int my = 0;
 #pragma unroll
     for (int i = 0; i < kDcWords; ++i) {
-        words[i] = dilated_word(in, out, s, w0 + i, kh, kw, ph, pw, identity);
-        my += __popc(words[i]);
+        const int64_t wi = w0 + i;
+        const int y = (int)(wi / out.wpr), w = (int)(wi - (int64_t)(wi / out.wpr) * out.wpr);
+        uint32_t word = 0;
+        if (y < out.H) {
+            if (identity) {
+                word = s_rows[shift + (int)((int64_t)(y - ra) * in.wpr) + w];
+            } else {
+                for (int kj = 0; kj < kh; ++kj) {
+                    const int yy = y - ph + kj;
+                    if (yy < 0 || yy >= in.H) continue;
+                    const uint32_t* row = s_rows + shift + (yy - ra) * in.wpr;
+                    const uint32_t prev = w > 0 && w - 1 < in.wpr ? row[w - 1] : 0u;
+                    const uint32_t cur = w < in.wpr ? row[w] : 0u;
+                    const uint32_t next = w + 1 < in.wpr ? row[w + 1] : 0u;
+                    for (int d = 0; d < kw; ++d) word |= hslice(prev, cur, next, d - pw);
+                }
+            }
+            const int rem = out.W - 32 * w;
+            if (rem < 32) word &= rem > 0 ? ((1u << rem) - 1u) : 0u;
+        }
+        words[i] = word;
+        my += __popc(word);
     }
     if (write_out) {
         uint4* o4 = reinterpret_cast<uint4*>(out.d + (int64_t)s * out.stride + w0);
@@ -248,6 +276,11 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
     }
 }
 
+static size_t dc_smem_bytes(const BitMask& in, const BitMask& out, int kh) {
+    const int rows = (kDcThreads * kDcWords) / out.wpr + 2 + kh;
+    return ((size_t)rows * in.wpr + 8) * sizeof(uint32_t);
+}
+
 size_t dilate_compact_workspace(const BitMask& out, int S) {
     const int64_t tiles = (int64_t)S * (out.stride / (kDcThreads * kDcWords));
     return (size_t)round_up(tiles * 8 + 16, 256);
@@ -262,8 +295,11 @@ void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int k
     const bool identity = kh == 1 && kw == 1 && ph == 0 && pw == 0;
     cudaMemsetAsync(workspace, 0, tiles * 8 + 16, st);
     cudaMemsetAsync(total, 0, sizeof(int), st);
-    dilate_compact_kernel<<<(unsigned)tiles, kDcThreads, 0, st>>>(in, out, write_out, kh, kw, ph, pw, identity, idx,
-                                                                   total, status, counter, cnt, cstride);
+    const size_t smem = dc_smem_bytes(in, out, identity ? 1 : kh);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(dilate_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dilate_compact_kernel<<<(unsigned)tiles, kDcThreads, smem, st>>>(in, out, write_out, kh, kw, ph, pw, identity, idx,
+                                                                      total, status, counter, cnt, cstride);
 }
 
 // ---------------------------------------------------------------------------
