@@ -45,18 +45,27 @@ __global__ void __launch_bounds__(256) detect_bits_kernel(const float* const* cu
             if (x0 < W) {
                 const int64_t p0 = (int64_t)y * W + x0;
                 if constexpr (vec) {
-#pragma unroll 1
-                    for (int c = 0; c < C; ++c) {
-                        const float4 u = __ldcs(reinterpret_cast<const float4*>(a + c * HW + p0));
-                        const float4 v = __ldcs(reinterpret_cast<const float4*>(b + c * HW + p0));
-                        if (MODE == 0) {
-                            flags |= (ref_changed(u.x, v.x, tau) ? 1u : 0u) | (ref_changed(u.y, v.y, tau) ? 2u : 0u) |
-                                     (ref_changed(u.z, v.z, tau) ? 4u : 0u) | (ref_changed(u.w, v.w, tau) ? 8u : 0u);
-                        } else {
-                            flags |= (__float_as_uint(u.x) != __float_as_uint(v.x) ? 1u : 0u) |
-                                     (__float_as_uint(u.y) != __float_as_uint(v.y) ? 2u : 0u) |
-                                     (__float_as_uint(u.z) != __float_as_uint(v.z) ? 4u : 0u) |
-                                     (__float_as_uint(u.w) != __float_as_uint(v.w) ? 8u : 0u);
+                    // all channel planes of both frames in flight before the compares
+                    for (int c0 = 0; c0 < C; c0 += 4) {
+                        float4 u[4], v[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if (c0 + c < C) {
+                                u[c] = __ldcs(reinterpret_cast<const float4*>(a + (c0 + c) * HW + p0));
+                                v[c] = __ldcs(reinterpret_cast<const float4*>(b + (c0 + c) * HW + p0));
+                            }
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            if (c0 + c >= C) break;
+                            if (MODE == 0) {
+                                flags |= (ref_changed(u[c].x, v[c].x, tau) ? 1u : 0u) | (ref_changed(u[c].y, v[c].y, tau) ? 2u : 0u) |
+                                         (ref_changed(u[c].z, v[c].z, tau) ? 4u : 0u) | (ref_changed(u[c].w, v[c].w, tau) ? 8u : 0u);
+                            } else {
+                                flags |= (__float_as_uint(u[c].x) != __float_as_uint(v[c].x) ? 1u : 0u) |
+                                         (__float_as_uint(u[c].y) != __float_as_uint(v[c].y) ? 2u : 0u) |
+                                         (__float_as_uint(u[c].z) != __float_as_uint(v[c].z) ? 4u : 0u) |
+                                         (__float_as_uint(u[c].w) != __float_as_uint(v[c].w) ? 8u : 0u);
+                            }
                         }
                     }
                 } else {
@@ -186,12 +195,12 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
                                                                     unsigned long long* cnt, int cstride) {
     extern __shared__ uint4 s_rows4[];
     uint32_t* s_rows = reinterpret_cast<uint32_t*>(s_rows4);
-    __shared__ unsigned s_tile;
     __shared__ int s_warp[kDcThreads / 32];
     __shared__ long long s_base;
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-    __syncthreads();
-    const unsigned tile = s_tile;
+    // Tile = block index: blocks are dispatched in index order, so every
+    // predecessor a tile waits on in the look-back is already resident.
+    (void)tile_counter;
+    const unsigned tile = blockIdx.x;
     constexpr int kTile = kDcThreads * kDcWords;
     const int tps = (int)(out.stride / kTile);
     const int s = tile / tps;
