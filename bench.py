@@ -327,12 +327,15 @@ def run_gpu_arm(args):
     value = ws * S * K / (ms / 1000.0)
     log(f"[gpu] cbinfer: {ms / K:.3f} ms/step, {value:.1f} frames/s, {launches} kernels/frame")
 
-    # changed fractions on following frames of the same clip (untimed, per-step readback)
+    # changed fractions of exactly the timed frames: replay the clip from reset
+    # (untimed, per-step readback)
     st_all = []
-    for i in range(i0 + K, i0 + K + 4):
+    net.reset_state()
+    for i in range(0, i0 + K):
         net.forward_device(ptrs(i))
-        stats, _ = net.read_stats()
-        st_all.append(stats)
+        if i >= i0:
+            stats, _ = net.read_stats()
+            st_all.append(stats)
     cb = spec.cb_layers()
     frac_in = float(np.mean([s[cb[0]]["changedInputPixels"] for st in st_all for s in st])) / (args.height * args.width)
     frac_out = [float(np.mean([s[k]["changedOutputPixels"] for st in st_all for s in st])) /
@@ -340,7 +343,7 @@ def run_gpu_arm(args):
 
     # per-kernel device times (graph-free pass with CUDA events on the launch stream)
     prof_runs = []
-    for i in range(i0 + K + 4, i0 + K + 7):
+    for i in range(i0 + K, i0 + K + 3):
         prof_runs.append((net.profile(ptrs(i)), net.read_stats()[0]))
     per = {}
     for prof, st in prof_runs:

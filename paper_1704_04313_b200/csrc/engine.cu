@@ -421,7 +421,8 @@ void Engine::record(Plan& p, bool full) {
                         // U_k = dilate(input change mask) (CBCONV) or dilate(input updated mask) (CONV)
                         const BitMask& src = l.kind == CBX_CBCONV ? p.chg[k] : p.upd[k];
                         unsigned long long* cnt = l.kind == CBX_CBCONV ? stats_of(k, 1) : nullptr;
-                        const bool fused = g.strideH == 1 && g.strideW == 1 && g.padW <= 31 && g.kernelW - 1 - g.padW <= 31;
+                        const bool fused = g.strideH == 1 && g.strideW == 1 && g.padW <= 31 &&
+                                           g.kernelW - 1 - g.padW <= 31 && 2 * g.padW <= g.kernelW - 1;
                         if (identity_geom(g)) {
                             const bool own = p.U[k].d != nullptr;  // CBCONV 1x1: U_k is its own mask
                             launch_dilate_compact(src, own ? p.U[k] : src, own, S, 1, 1, 0, 0, p.idx[k], p.cnt[k], p.ws,

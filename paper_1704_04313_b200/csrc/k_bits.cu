@@ -182,16 +182,61 @@ __device__ __forceinline__ long long lookback(unsigned long long* status, unsign
     return base;
 }
 
-constexpr int kDcWords = 8;  // words per thread; a tile is kDcThreads * kDcWords words
 
-// Output words [w0, w0 + tile) of one stream need input rows
-// [y(w0) - ph, y(w0 + tile - 1) - ph + kh) -- one contiguous range of input
-// words, staged into shared memory with coalesced 16-byte loads so that the
-// 3*kh word reads per output word are shared-memory hits.
+// OR over a horizontal window: output bit x of the word = OR of input bits
+// x + t, t in [-pw, kw - 1 - pw], with the neighbouring words supplying the
+// bits that cross the word boundary (64-bit doubling: ~log2(kw) shift/or).
+__device__ __forceinline__ uint32_t hdilate(uint32_t prev, uint32_t cur, uint32_t next, int kw, int pw) {
+    const int tmax = kw - 1 - pw;  // rightward reach (may be negative)
+    uint32_t out = 0;
+    if (tmax >= 0) {
+        uint64_t r = ((uint64_t)next << 32) | cur;  // bit j = input position j
+        int covered = 1;
+        const int wdt = tmax + 1;
+        uint64_t acc = r;
+        while (covered * 2 <= wdt) {
+            acc |= acc >> covered;
+            covered *= 2;
+        }
+        if (covered < wdt) acc |= acc >> (wdt - covered);
+        out |= (uint32_t)acc;  // positions x .. x + tmax
+        if (pw > 0) {
+            // positions x - pw .. x - 1: bits of (prev, cur) shifted
+            uint64_t l = ((uint64_t)cur << 32) | prev;  // bit j = input position j - 32
+            uint64_t accl = l;
+            int cv = 1;
+            while (cv * 2 <= pw) {
+                accl |= accl >> cv;
+                cv *= 2;
+            }
+            if (cv < pw) accl |= accl >> (pw - cv);
+            out |= (uint32_t)(accl >> (32 - pw));  // bit x <- OR of positions x-pw .. x-1
+        }
+    } else {
+        // window entirely left of x: positions x - pw .. x - pw + kw - 1
+        uint64_t l = ((uint64_t)cur << 32) | prev;
+        uint64_t accl = l;
+        int cv = 1;
+        while (cv * 2 <= kw) {
+            accl |= accl >> cv;
+            cv *= 2;
+        }
+        if (cv < kw) accl |= accl >> (kw - cv);
+        out = (uint32_t)(accl >> (32 - pw));
+    }
+    return out;
+}
+
+// Output words [t0, t0 + tile) of one stream need input rows
+// [y(t0) - ph, y(t0 + tile - 1) - ph + kh) -- one contiguous range of input
+// words. It is staged into shared memory with coalesced 16-byte loads,
+// horizontally dilated once per input word, and every output word is then
+// the OR of kh shared-memory words.
+template <int WPT>
 __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, BitMask out, bool write_out,
                                                                     int kh, int kw, int ph, int pw, bool identity,
                                                                     int32_t* __restrict__ idx, int* total,
-                                                                    unsigned long long* status, unsigned* tile_counter,
+                                                                    unsigned long long* status,
                                                                     unsigned long long* cnt, int cstride) {
     extern __shared__ uint4 s_rows4[];
     uint32_t* s_rows = reinterpret_cast<uint32_t*>(s_rows4);
@@ -199,14 +244,12 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
     __shared__ long long s_base;
     // Tile = block index: blocks are dispatched in index order, so every
     // predecessor a tile waits on in the look-back is already resident.
-    (void)tile_counter;
     const unsigned tile = blockIdx.x;
-    constexpr int kTile = kDcThreads * kDcWords;
+    constexpr int kTile = kDcThreads * WPT;
     const int tps = (int)(out.stride / kTile);
     const int s = tile / tps;
     const int64_t t0 = (int64_t)(tile - (unsigned)s * tps) * kTile;
-    const int64_t w0 = t0 + (int64_t)threadIdx.x * kDcWords;
-    // stage input rows
+    const int64_t w0 = t0 + (int64_t)threadIdx.x * WPT;
     const int ya = (int)(t0 / out.wpr);
     const int yb = (int)((t0 + kTile - 1) / out.wpr);
     const int ra = identity ? ya : max(0, ya - ph);
@@ -214,46 +257,53 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
     const uint32_t* src = in.d + (int64_t)s * in.stride;
     const int64_t sw0 = (int64_t)ra * in.wpr;
     const int nwords = rb >= ra ? (rb - ra + 1) * in.wpr : 0;
+    const int64_t a4 = sw0 & ~int64_t(3);
+    const int shift = (int)(sw0 - a4);
+    const int n4 = (int)((sw0 + nwords - a4 + 3) >> 2);
     {
-        // 16-byte aligned window over [sw0, sw0 + nwords)
-        const int64_t a4 = sw0 & ~int64_t(3);
-        const int n4 = (int)((sw0 + nwords - a4 + 3) >> 2);
         const uint4* g4 = reinterpret_cast<const uint4*>(src + a4);
         for (int i = threadIdx.x; i < n4; i += kDcThreads) s_rows4[i] = __ldg(g4 + i);
     }
     __syncthreads();
-    const int shift = (int)(sw0 & 3);  // s_rows[shift + (word - sw0)]
-    uint32_t words[kDcWords];
+    const uint32_t* rows = s_rows + shift;
+    uint32_t* hrows = s_rows + 4 * n4 + 4;  // horizontally dilated copy
+    if (!identity) {
+        for (int i = threadIdx.x; i < nwords; i += kDcThreads) {
+            const int w = i % in.wpr;
+            const uint32_t prev = w > 0 ? rows[i - 1] : 0u;
+            const uint32_t next = w + 1 < in.wpr ? rows[i + 1] : 0u;
+            hrows[i] = hdilate(prev, rows[i], next, kw, pw);
+        }
+        __syncthreads();
+    }
+    uint32_t words[WPT];
     int my = 0;
 #pragma unroll
-    for (int i = 0; i < kDcWords; ++i) {
+    for (int i = 0; i < WPT; ++i) {
         const int64_t wi = w0 + i;
         const int y = (int)(wi / out.wpr), w = (int)(wi - (int64_t)(wi / out.wpr) * out.wpr);
         uint32_t word = 0;
-        if (y < out.H) {
+        if (y < out.H && w < in.wpr) {
             if (identity) {
-                word = s_rows[shift + (int)((int64_t)(y - ra) * in.wpr) + w];
+                word = rows[(y - ra) * in.wpr + w];
             } else {
-                for (int kj = 0; kj < kh; ++kj) {
-                    const int yy = y - ph + kj;
-                    if (yy < 0 || yy >= in.H) continue;
-                    const uint32_t* row = s_rows + shift + (yy - ra) * in.wpr;
-                    const uint32_t prev = w > 0 && w - 1 < in.wpr ? row[w - 1] : 0u;
-                    const uint32_t cur = w < in.wpr ? row[w] : 0u;
-                    const uint32_t next = w + 1 < in.wpr ? row[w + 1] : 0u;
-                    for (int d = 0; d < kw; ++d) word |= hslice(prev, cur, next, d - pw);
-                }
+                const int k0 = max(0, ph - y), k1 = min(kh, in.H + ph - y);
+                for (int kj = k0; kj < k1; ++kj) word |= hrows[(y - ph + kj - ra) * in.wpr + w];
             }
+        }
+        if (y < out.H) {
             const int rem = out.W - 32 * w;
             if (rem < 32) word &= rem > 0 ? ((1u << rem) - 1u) : 0u;
+        } else {
+            word = 0;
         }
         words[i] = word;
         my += __popc(word);
     }
     if (write_out) {
-        uint4* o4 = reinterpret_cast<uint4*>(out.d + (int64_t)s * out.stride + w0);
-        o4[0] = make_uint4(words[0], words[1], words[2], words[3]);
-        o4[1] = make_uint4(words[4], words[5], words[6], words[7]);
+        uint32_t* o = out.d + (int64_t)s * out.stride + w0;
+#pragma unroll
+        for (int i = 0; i < WPT; ++i) o[i] = words[i];
     }
     int agg;
     const int excl = block_scan(my, s_warp, agg);
@@ -271,7 +321,7 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
     int64_t o = s_base + excl;
     const int64_t sbase = (int64_t)s * out.H * out.W;
 #pragma unroll
-    for (int i = 0; i < kDcWords; ++i) {
+    for (int i = 0; i < WPT; ++i) {
         uint32_t word = words[i];
         if (!word) continue;
         const int64_t wi = w0 + i;
@@ -285,30 +335,46 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
     }
 }
 
-static size_t dc_smem_bytes(const BitMask& in, const BitMask& out, int kh) {
-    const int rows = (kDcThreads * kDcWords) / out.wpr + 2 + kh;
-    return ((size_t)rows * in.wpr + 8) * sizeof(uint32_t);
+static size_t dc_smem_bytes(const BitMask& in, const BitMask& out, int kh, int wpt) {
+    const int rows = (kDcThreads * wpt) / out.wpr + 2 + kh;
+    return (2 * ((size_t)rows * in.wpr + 8) + 16) * sizeof(uint32_t);
 }
 
 size_t dilate_compact_workspace(const BitMask& out, int S) {
-    const int64_t tiles = (int64_t)S * (out.stride / (kDcThreads * kDcWords));
+    const int64_t tiles = (int64_t)S * (out.stride / kDcThreads);  // WPT = 1 upper bound
     return (size_t)round_up(tiles * 8 + 16, 256);
+}
+
+template <int WPT>
+static void launch_dc(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw, bool identity,
+                      int32_t* idx, int* total, unsigned long long* status, unsigned long long* cnt, int cstride,
+                      cudaStream_t st) {
+    const int64_t tiles = (int64_t)S * (out.stride / (kDcThreads * WPT));
+    const size_t smem = dc_smem_bytes(in, out, identity ? 1 : kh, WPT);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(dilate_compact_kernel<WPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dilate_compact_kernel<WPT><<<(unsigned)tiles, kDcThreads, smem, st>>>(in, out, write_out, kh, kw, ph, pw, identity,
+                                                                          idx, total, status, cnt, cstride);
 }
 
 void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw,
                            int32_t* idx, int* total, void* workspace, unsigned long long* cnt, int cstride,
                            cudaStream_t st) {
-    const int64_t tiles = (int64_t)S * (out.stride / (kDcThreads * kDcWords));
     unsigned long long* status = reinterpret_cast<unsigned long long*>(workspace);
-    unsigned* counter = reinterpret_cast<unsigned*>(status + tiles);
     const bool identity = kh == 1 && kw == 1 && ph == 0 && pw == 0;
+    const int64_t words = (int64_t)S * out.stride;
+    // enough tiles to cover the SMs twice, at most 8 words per thread
+    int wpt = 8;
+    while (wpt > 1 && words / (kDcThreads * wpt) < 2 * kNumSMs) wpt /= 2;
+    const int64_t tiles = words / (kDcThreads * wpt);
     cudaMemsetAsync(workspace, 0, tiles * 8 + 16, st);
     cudaMemsetAsync(total, 0, sizeof(int), st);
-    const size_t smem = dc_smem_bytes(in, out, identity ? 1 : kh);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(dilate_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dilate_compact_kernel<<<(unsigned)tiles, kDcThreads, smem, st>>>(in, out, write_out, kh, kw, ph, pw, identity, idx,
-                                                                      total, status, counter, cnt, cstride);
+    switch (wpt) {
+        case 8: launch_dc<8>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st); break;
+        case 4: launch_dc<4>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st); break;
+        case 2: launch_dc<2>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st); break;
+        default: launch_dc<1>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st); break;
+    }
 }
 
 // ---------------------------------------------------------------------------
