@@ -204,37 +204,45 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
     const int64_t HoWo = (int64_t)a.Ho * a.Wo;
 
     if (warp >= 4 && warp < 8) {
-        // ================= producers: row r of every tile =================
-        const int r = tid - kEpiThreads;
-        const uint32_t swz = (uint32_t)(r & 7);
+        // ================= producers =================
+        // Thread pt copies chunk j = pt % 8 of rows rsub + 16*i (i < 8), so the
+        // 8 lanes of a row fetch its 128 contiguous-ish bytes together and a
+        // warp instruction touches 4 rows instead of 32 scattered pixels.
+        const int pt = tid - kEpiThreads;
+        const int j = pt & 7, rsub = pt >> 3;
+        const uint32_t swz_off = (uint32_t)((j ^ (rsub & 7)) << 4);
+        constexpr int kRowsPerThread = kTileM / 16;
         uint32_t it = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int64_t n = tile * kTileM + r;
-            const bool valid = n < total;
-            const float* base = a.in;
-            if (valid) {
-                const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
-                const int s = (int)(g / HoWo);
-                const int p = (int)(g - (int64_t)s * HoWo);
-                const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
-                base = a.in + (int64_t)s * a.in_ss +
-                       ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
+            const float* base[kRowsPerThread];
+            uint32_t vmask = 0;
+#pragma unroll
+            for (int i = 0; i < kRowsPerThread; ++i) {
+                const int64_t n = tile * kTileM + rsub + 16 * i;
+                base[i] = a.in;
+                if (n < total) {
+                    vmask |= 1u << i;
+                    const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
+                    const int s = (int)(g / HoWo);
+                    const int p = (int)(g - (int64_t)s * HoWo);
+                    const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
+                    base[i] = a.in + (int64_t)s * a.in_ss +
+                              ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
+                }
             }
             for (int kb = 0; kb < a.NKB; ++kb, ++it) {
                 const uint32_t st = it % NS, ph = (it / NS) & 1u;
                 mbar_wait(&empty[st], ph ^ 1u);
-                if (r == 0) {
+                if (pt == 0) {
                     mbar_arrive_expect_tx(&full[st], b_bytes);
                     bulk_g2s(sB + (size_t)st * b_bytes, a.Bw + (size_t)kb * a.Npad * kKBlock, b_bytes, &full[st]);
                 }
-                const uint32_t row = smem_u32(sA + (size_t)st * kABytes + r * 128);
-                if (valid) {
+                const int off = sTab[kb * kChunksPerKB + j];
+                const uint32_t stage = smem_u32(sA + (size_t)st * kABytes) + swz_off;
 #pragma unroll
-                    for (int j = 0; j < kChunksPerKB; ++j) {
-                        const int off = sTab[kb * kChunksPerKB + j];
-                        cp_async16(row + ((j ^ swz) << 4), off >= 0 ? base + off : a.in, off >= 0 ? 16u : 0u);
-                    }
-                }
+                for (int i = 0; i < kRowsPerThread; ++i)
+                    if ((vmask >> i) & 1u)
+                        cp_async16(stage + (rsub + 16 * i) * 128, off >= 0 ? base[i] + off : a.in, off >= 0 ? 16u : 0u);
                 cp_async_arrive_noinc(&full[st]);
             }
         }

@@ -156,28 +156,57 @@ __global__ void __launch_bounds__(kConvThreads) conv_planar_kernel(ConvArgs a) {
 #pragma unroll
                 for (int j = 0; j < OC; ++j) acc[j] = (o0 + j < O) ? a.bias[o0 + j] : 0.0f;
                 const float4* wr = sWv;
-                for (int c = 0; c < a.in.C; ++c) {
-                    for (int kj = 0; kj < a.kh; ++kj) {
-                        const int yy = y0 + kj;
-                        const bool rowok = (unsigned)yy < (unsigned)H;
-                        const float* rowp = src + c * HW + (int64_t)(rowok ? yy : 0) * W;
-                        for (int ki0 = 0; ki0 < a.kw; ki0 += 8) {
-                            float v[8];
+                // rows (c, kj) in reference order; the taps of row r+1 are
+                // loaded while row r is accumulated (software pipeline)
+                const int nrows = a.in.C * a.kh;
+                auto load_row = [&](int rr, float (&v)[8]) {
+                    const int c = rr / a.kh, kj = rr - c * a.kh;
+                    const int yy = y0 + kj;
+                    const bool rowok = rr < nrows && (unsigned)yy < (unsigned)H;
+                    const float* rowp = src + c * HW + (int64_t)(rowok ? yy : 0) * W;
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) {
-                                const int xx = x0 + ki0 + u;
-                                v[u] = (rowok && ki0 + u < a.kw && (unsigned)xx < (unsigned)W) ? __ldg(rowp + xx) : 0.0f;
+                    for (int u = 0; u < 8; ++u) {
+                        const int xx = x0 + u;
+                        v[u] = (rowok && u < a.kw && (unsigned)xx < (unsigned)W) ? __ldg(rowp + xx) : 0.0f;
+                    }
+                };
+                float vc[8], vn[8];
+                if (a.kw <= 8) {
+                    load_row(0, vc);
+                    for (int rr = 0; rr < nrows; ++rr) {
+                        load_row(rr + 1, vn);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (u >= a.kw) break;
+#pragma unroll
+                            for (int q = 0; q < OC / 4; ++q) {
+                                const float4 wq = wr[q];
+                                acc[4 * q + 0] = __fadd_rn(acc[4 * q + 0], __fmul_rn(wq.x, vc[u]));
+                                acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(wq.y, vc[u]));
+                                acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(wq.z, vc[u]));
+                                acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(wq.w, vc[u]));
                             }
+                            wr += OC / 4;
+                        }
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) {
-                                if (ki0 + u >= a.kw) break;
+                        for (int u = 0; u < 8; ++u) vc[u] = vn[u];
+                    }
+                } else {
+                    for (int c = 0; c < a.in.C; ++c) {
+                        for (int kj = 0; kj < a.kh; ++kj) {
+                            const int yy = y0 + kj;
+                            const bool rowok = (unsigned)yy < (unsigned)H;
+                            const float* rowp = src + c * HW + (int64_t)(rowok ? yy : 0) * W;
+                            for (int ki = 0; ki < a.kw; ++ki) {
+                                const int xx = x0 + ki;
+                                const float v = (rowok && (unsigned)xx < (unsigned)W) ? __ldg(rowp + xx) : 0.0f;
 #pragma unroll
                                 for (int q = 0; q < OC / 4; ++q) {
                                     const float4 wq = wr[q];
-                                    acc[4 * q + 0] = __fadd_rn(acc[4 * q + 0], __fmul_rn(wq.x, v[u]));
-                                    acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(wq.y, v[u]));
-                                    acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(wq.z, v[u]));
-                                    acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(wq.w, v[u]));
+                                    acc[4 * q + 0] = __fadd_rn(acc[4 * q + 0], __fmul_rn(wq.x, v));
+                                    acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(wq.y, v));
+                                    acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(wq.z, v));
+                                    acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(wq.w, v));
                                 }
                                 wr += OC / 4;
                             }
