@@ -116,6 +116,14 @@ CBX_API int cbx_load_layer(cbx_ctx* ctx, int layer, const float* K, const float*
 CBX_API int cbx_set_thresholds(cbx_ctx* ctx, const float* taus, int n);
 CBX_API int cbx_get_thresholds(const cbx_ctx* ctx, float* taus, int n);
 
+/* Runtime options. CBX_OPT_FUSE_TAIL (default 1): run the per-pixel layers
+ * that end the network (1x1 CONV / RELU / CLASSIFY after the last tcgen05
+ * conv) inside that conv's epilogue; their intermediate tensors are then not
+ * materialized (cbx_get_activation reports CBX_E_SPEC for them). 0 keeps every
+ * layer's output, e.g. for per-layer parity checks. Results are identical. */
+typedef enum { CBX_OPT_FUSE_TAIL = 0 } cbx_option;
+CBX_API int cbx_set_option(cbx_ctx* ctx, int option, int value);
+
 /* Drops all change-based state of every stream: the next frame is a full
  * evaluation (reset_state, network.cpp:317-320). */
 CBX_API int cbx_reset(cbx_ctx* ctx);

@@ -270,7 +270,7 @@ class Network:
     of reference weight files (read_weights_f32le)."""
 
     def __init__(self, spec: NetworkSpec, weights, device: int = 0, streams: int = 1,
-                 precision: str = "tf32"):
+                 precision: str = "tf32", fuse_tail: bool = True):
         self.spec = spec
         self.shapes = chain_dims(spec)
         self.streams = streams
@@ -301,6 +301,8 @@ class Network:
                     raise IoError(f"layer {k + 1} ({l.kind}): weight shape mismatch")
                 self._chk(lib.cbx_load_layer(self._h, k, K.ctypes.data_as(C.POINTER(C.c_float)),
                                              b.ctypes.data_as(C.POINTER(C.c_float))))
+        if not fuse_tail:
+            self.set_fuse_tail(False)
         last = spec.layers[-1]
         self.label_hw = self.shapes[-1][0][1:] if last.kind == "CLASSIFY" else self.shapes[-1][1][1:]
         self._frame_elems = spec.inputChannels * spec.inputHeight * spec.inputWidth
@@ -332,6 +334,11 @@ class Network:
 
     def reset_state(self) -> None:
         self._chk(lib.cbx_reset(self._h))
+
+    def set_fuse_tail(self, on: bool) -> None:
+        """CBX_OPT_FUSE_TAIL: run the network's per-pixel tail in the last
+        tcgen05 conv's epilogue (default) or materialize every layer."""
+        self._chk(lib.cbx_set_option(self._h, 0, int(bool(on))))
 
     # -- forward
     def forward(self, frames: np.ndarray, engine: str = "cbinfer") -> List[ForwardResult]:

@@ -96,7 +96,7 @@ lib.cbx_stream.argtypes = [VP]
 lib.cbx_last_launch_count.argtypes = [VP]
 lib.cbx_op_extract_workspace.restype = C.c_size_t
 lib.cbx_op_extract_workspace.argtypes = [C.c_int64]
-for _name in ("cbx_load_layer", "cbx_set_thresholds", "cbx_get_thresholds", "cbx_reset", "cbx_forward",
+for _name in ("cbx_load_layer", "cbx_set_thresholds", "cbx_get_thresholds", "cbx_set_option", "cbx_reset", "cbx_forward",
               "cbx_forward_device", "cbx_sync", "cbx_read_labels", "cbx_read_stats", "cbx_labels_device",
               "cbx_get_activation", "cbx_get_trace", "cbx_destroy"):
     getattr(lib, _name).argtypes = None
@@ -105,7 +105,7 @@ lib.cbx_destroy.argtypes = [VP]
 # exported symbols declared in include/cbx.h (checked by tests without a GPU)
 EXPORTS = [
     "cbx_last_error", "cbx_version", "cbx_chain_dims", "cbx_create", "cbx_destroy", "cbx_load_layer",
-    "cbx_set_thresholds", "cbx_get_thresholds", "cbx_reset", "cbx_forward", "cbx_forward_device",
+    "cbx_set_thresholds", "cbx_get_thresholds", "cbx_set_option", "cbx_reset", "cbx_forward", "cbx_forward_device",
     "cbx_sync", "cbx_read_labels", "cbx_read_stats", "cbx_labels_device", "cbx_stream",
     "cbx_last_launch_count", "cbx_profile_forward", "cbx_get_activation", "cbx_get_trace", "cbx_op_detect", "cbx_op_dilate",
     "cbx_op_extract_workspace", "cbx_op_extract", "cbx_op_maxpool", "cbx_op_argmax",

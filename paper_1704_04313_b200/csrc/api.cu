@@ -139,6 +139,10 @@ CBX_API int cbx_get_thresholds(const cbx_ctx* ctx, float* taus, int n) {
     return guarded(const_cast<cbx_ctx*>(ctx), [&] { E(const_cast<cbx_ctx*>(ctx)).get_thresholds(taus, n); });
 }
 
+CBX_API int cbx_set_option(cbx_ctx* ctx, int option, int value) {
+    return guarded(ctx, [&] { E(ctx).set_option(option, value); });
+}
+
 CBX_API int cbx_reset(cbx_ctx* ctx) {
     return guarded(ctx, [&] { E(ctx).reset(); });
 }

@@ -122,6 +122,47 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Remaining per-pixel ops of a fused tail (after the first 1x1 CONV, whose
+// outputs arrive in `cur`): RELU (ref_relu), 1x1 CONV (bias-first, ascending
+// channel order, one rounding per multiply and add -- the reference gemm
+// order), then the final activation is stored and argmax-classified with the
+// reference tie rule (strict >, lowest channel wins).
+__device__ __forceinline__ void run_tail(const TcTail& t, float (&cur)[kTailMaxC], int s, int y, int x, int p) {
+    int C = t.cout[0];
+    for (int k = 1; k < t.n; ++k) {
+        if (t.kind[k] == 1) {
+#pragma unroll
+            for (int q = 0; q < kTailMaxC; ++q) cur[q] = ref_relu(cur[q]);
+        } else {
+            const int O = t.cout[k];
+            float nxt[kTailMaxC];
+#pragma unroll
+            for (int q = 0; q < kTailMaxC; ++q) {
+                float acc = (q < O) ? __ldg(t.b[k] + q) : 0.0f;
+                if (q < O)
+                    for (int c = 0; c < C; ++c) acc = __fadd_rn(acc, __fmul_rn(__ldg(t.W[k] + q * C + c), cur[c]));
+                nxt[q] = acc;
+            }
+#pragma unroll
+            for (int q = 0; q < kTailMaxC; ++q) cur[q] = nxt[q];
+            C = O;
+        }
+    }
+    float* fo = t.final_out + (int64_t)s * t.fo_ss + ((int64_t)(y + t.fo_hh) * t.fo_Wp + (x + t.fo_hw)) * t.fo_Cp;
+    int best = 0;
+    float bv = cur[0];
+#pragma unroll
+    for (int q = 0; q < kTailMaxC; ++q) {
+        if (q >= C) break;
+        fo[q] = cur[q];
+        if (q > 0 && cur[q] > bv) {
+            bv = cur[q];
+            best = q;
+        }
+    }
+    t.labels[(int64_t)s * t.l_ss + p] = (uint16_t)best;
+}
+
 struct TcArgs {
     const float* in;
     int64_t in_ss;
@@ -143,8 +184,15 @@ struct TcArgs {
     float tau;
     unsigned long long* chg_cnt;
     int cnt_stride;
+    int write_out;  // store this layer's output tensor (off when a fused tail consumes it)
+    TcTail tail;
 };
 
+// ROWLANE: producer thread = tile row (each lane gathers its own pixel; best
+// when a pixel's taps are 16 B, i.e. 4 channels, so a warp's 32 rows of one
+// tap are 32 neighbouring pixels). Otherwise 8 lanes cooperate on a row's 128
+// contiguous K-block bytes and a warp instruction covers 4 rows.
+template <bool ROWLANE>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -205,6 +253,41 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
 
     if (warp >= 4 && warp < 8) {
         // ================= producers =================
+        if constexpr (ROWLANE) {
+            const int r = tid - kEpiThreads;
+            const uint32_t swz = (uint32_t)(r & 7);
+            uint32_t it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int64_t n = tile * kTileM + r;
+                const bool valid = n < total;
+                const float* base = a.in;
+                if (valid) {
+                    const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
+                    const int s = (int)(g / HoWo);
+                    const int p = (int)(g - (int64_t)s * HoWo);
+                    const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
+                    base = a.in + (int64_t)s * a.in_ss +
+                           ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
+                }
+                for (int kb = 0; kb < a.NKB; ++kb, ++it) {
+                    const uint32_t st = it % NS, ph = (it / NS) & 1u;
+                    mbar_wait(&empty[st], ph ^ 1u);
+                    if (r == 0) {
+                        mbar_arrive_expect_tx(&full[st], b_bytes);
+                        bulk_g2s(sB + (size_t)st * b_bytes, a.Bw + (size_t)kb * a.Npad * kKBlock, b_bytes, &full[st]);
+                    }
+                    const uint32_t row = smem_u32(sA + (size_t)st * kABytes + r * 128);
+                    if (valid) {
+#pragma unroll
+                        for (int j = 0; j < kChunksPerKB; ++j) {
+                            const int off = sTab[kb * kChunksPerKB + j];
+                            cp_async16(row + ((j ^ swz) << 4), off >= 0 ? base + off : a.in, off >= 0 ? 16u : 0u);
+                        }
+                    }
+                    cp_async_arrive_noinc(&full[st]);
+                }
+            }
+        } else {
         // Thread pt copies chunk j = pt % 8 of rows rsub + 16*i (i < 8), so the
         // 8 lanes of a row fetch its 128 contiguous-ish bytes together and a
         // warp instruction touches 4 rows instead of 32 scattered pixels.
@@ -245,6 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
                         cp_async16(stage + (rsub + 16 * i) * 128, off >= 0 ? base[i] + off : a.in, off >= 0 ? 16u : 0u);
                 cp_async_arrive_noinc(&full[st]);
             }
+        }
         }
     } else if (warp == 8) {
         // ================= MMA issuer =================
@@ -298,6 +382,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
             }
             bool changed = false;
             const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16) + as * a.acc_cols;
+            // fused per-pixel tail: first op is a 1x1 CONV over this layer's
+            // outputs, accumulated chunk by chunk in ascending channel order
+            const int n_tail = a.tail.n;
+            const int c1 = n_tail ? a.tail.cout[0] : 0;
+            float t1[kTailMaxC];
+#pragma unroll
+            for (int q = 0; q < kTailMaxC; ++q) t1[q] = (q < c1) ? __ldg(a.tail.b[0] + q) : 0.0f;
             for (int c0 = 0; c0 < a.O; c0 += 32) {
                 float v[32];
                 tmem_ld32(trow + c0, v);
@@ -312,6 +403,32 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
                             const float t = (o + e < a.O) ? __fadd_rn(v[j + e], sBias[o + e]) : 0.0f;
                             w4[e] = a.relu ? ref_relu(t) : t;
                         }
+                        if (n_tail) {
+                            const float* W0 = a.tail.W[0];
+                            if ((a.O & 3) == 0) {
+                                // 4 ascending channels per 16-byte weight load (warp-uniform address)
+#pragma unroll
+                                for (int q = 0; q < kTailMaxC; ++q) {
+                                    if (q >= c1) break;
+                                    const float4 wq = __ldg(reinterpret_cast<const float4*>(W0 + (int64_t)q * a.O + o));
+                                    float acc = t1[q];
+                                    acc = __fadd_rn(acc, __fmul_rn(wq.x, w4[0]));
+                                    acc = __fadd_rn(acc, __fmul_rn(wq.y, w4[1]));
+                                    acc = __fadd_rn(acc, __fmul_rn(wq.z, w4[2]));
+                                    acc = __fadd_rn(acc, __fmul_rn(wq.w, w4[3]));
+                                    t1[q] = acc;
+                                }
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    if (o + e >= a.O) break;
+#pragma unroll
+                                    for (int q = 0; q < kTailMaxC; ++q)
+                                        if (q < c1) t1[q] = __fadd_rn(t1[q], __fmul_rn(__ldg(W0 + (int64_t)q * a.O + o + e), w4[e]));
+                                }
+                            }
+                        }
+                        if (!a.write_out) continue;
                         if (o + 3 < a.O) {
                             float4* q = reinterpret_cast<float4*>(dst + o);
                             if (a.chg.d) {
@@ -331,6 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
             }
             tc_fence_before();
             mbar_arrive(&tempty[as]);
+            if (n_tail && valid) run_tail(a.tail, t1, s, y, x, p);
             if (a.chg.d) {
                 if (valid && changed) bit_set(a.chg, s, y, x);
                 if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
@@ -397,7 +515,8 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g) {
         throw Error(CBX_E_ARG, "tcgen05 conv: layer too wide for shared memory");
     t->stages = ns;
     t->smem = fixed + (size_t)ns * (kABytes + b_bytes);
-    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CBX_CUDA(cudaMalloc(&t->Bw, (size_t)t->NKB * b_bytes));
     CBX_CUDA(cudaMemset(t->Bw, 0, (size_t)t->NKB * b_bytes));
     return t;
@@ -430,7 +549,7 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
 
 void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float* bias, const int32_t* idx,
                     const int* count, int64_t full_count, bool relu, BitMask chg, float tau,
-                    unsigned long long* cnt, int cstride, int S, cudaStream_t st) {
+                    unsigned long long* cnt, int cstride, int S, cudaStream_t st, const TcTail* tail) {
     (void)S;
     if (in.Cp != t.Cp) throw Error(CBX_E_SHAPE, "tcgen05 conv: input channel stride mismatch");
     TcArgs a{};
@@ -473,9 +592,14 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.tau = tau;
     a.chg_cnt = chg.d ? cnt : nullptr;
     a.cnt_stride = cstride;
+    a.write_out = !(tail && tail->n && !tail->keep_out);
+    if (tail) a.tail = *tail;
     const int64_t max_tiles = (full_count + kTileM - 1) / kTileM;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, kNumSMs));
-    conv_tc_kernel<<<grid, kThreads, t.smem, st>>>(a);
+    if (in.Cp <= 4)
+        conv_tc_kernel<true><<<grid, kThreads, t.smem, st>>>(a);
+    else
+        conv_tc_kernel<false><<<grid, kThreads, t.smem, st>>>(a);
 }
 
 }  // namespace cbx

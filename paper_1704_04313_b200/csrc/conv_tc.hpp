@@ -15,6 +15,26 @@ struct TcLayerDeleter {
     void operator()(TcLayer* p) const;
 };
 
+// A chain of per-pixel layers fused into the epilogue of the preceding
+// tcgen05 conv: ops[0] is a 1x1 CONV over the conv's outputs, then RELU (1)
+// / 1x1 CONV (0) ops on at most kTailMaxC channels; the result (the input of
+// CLASSIFY) is stored to final_out and argmax-classified into labels.
+constexpr int kTailMaxC = 16;
+constexpr int kTailMaxOps = 8;
+struct TcTail {
+    int n;
+    int kind[kTailMaxOps];  // 0 = CONV 1x1, 1 = RELU
+    int cout[kTailMaxOps];
+    const float* W[kTailMaxOps];  // [cout][cin] reference layout
+    const float* b[kTailMaxOps];
+    float* final_out;
+    int64_t fo_ss;
+    int fo_Wp, fo_Cp, fo_hh, fo_hw;
+    uint16_t* labels;
+    int64_t l_ss;
+    int keep_out;  // also store the conv's own output tensor
+};
+
 bool tc_supported(const cbx_geom& g);
 std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g);
 // K in the reference layout [O][Cin*kh*kw], columns (c,kj,ki); host memory.
@@ -22,6 +42,6 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st);
 void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float* bias,
                     const int32_t* idx, const int* count, int64_t full_count, bool relu,
                     BitMask chg, float tau, unsigned long long* cnt, int cstride, int S,
-                    cudaStream_t st);
+                    cudaStream_t st, const TcTail* tail = nullptr);
 
 }  // namespace cbx

@@ -148,6 +148,7 @@ struct Engine::Plan {
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int launches[2] = {0, 0};
     bool dirty = true;
+    int fused_from = -1;            // conv layer whose epilogue runs the per-pixel tail (-1: none)
 
     ~Plan() {
         for (auto& g : gexec)
@@ -192,7 +193,10 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
             dBias_[k] = dmalloc<float>(g.outChannels);
             // tcgen05 for channels-last inputs in TF32 mode (every conv but a
             // first layer reading the planar frame).
-            if (precision_ == CBX_PREC_TF32 && k > 0 && tc_supported(g)) tc_[k] = make_tc_layer(g);
+            // (N >= 32 output channels: narrower 1x1 heads stay exact on CUDA cores,
+            //  usually fused into the epilogue of the preceding tcgen05 layer)
+            if (precision_ == CBX_PREC_TF32 && k > 0 && g.outChannels >= 32 && tc_supported(g))
+                tc_[k] = make_tc_layer(g);
         }
     }
     const bool hasClassify = layers_.back().kind == CBX_CLASSIFY;
@@ -404,6 +408,7 @@ void Engine::record(Plan& p, bool full) {
         launch_ingest(d_cur_, p.T[0], S, st);
         mark("ingest", 0);
     }
+    p.fused_from = -1;
     for (int k = 0; k < nl; ++k) {
         const auto& l = layers_[k];
         const bool has_next = k + 1 < nl;
@@ -446,7 +451,39 @@ void Engine::record(Plan& p, bool full) {
                 const bool planar_in = (k == 0 && !p.ingest);
                 const bool relu = l.kind == CBX_CBCONV && l.fuseRelu;
                 const int64_t full_count = (int64_t)S * dims_[6 * k + 4] * dims_[6 * k + 5];
-                if (tc_[k] && !planar_in) {
+                const int tail_last = (tc_[k] && !planar_in) ? tail_end(k) : -1;
+                if (tail_last > 0) {
+                    // per-pixel layers k+1..tail_last fused into this conv's epilogue
+                    TcTail t{};
+                    int prevC = l.geom.outChannels;
+                    for (int j = k + 1; j <= tail_last && layers_[j].kind != CBX_CLASSIFY; ++j) {
+                        if (layers_[j].kind == CBX_CONV) {
+                            t.kind[t.n] = 0;
+                            t.cout[t.n] = layers_[j].geom.outChannels;
+                            t.W[t.n] = dK_[j];
+                            t.b[t.n] = dBias_[j];
+                            prevC = t.cout[t.n];
+                        } else {
+                            t.kind[t.n] = 1;
+                            t.cout[t.n] = prevC;
+                        }
+                        ++t.n;
+                    }
+                    const TensorView& fo = p.T[final_tensor()];
+                    t.final_out = fo.d;
+                    t.fo_ss = fo.ss;
+                    t.fo_Wp = fo.Wp;
+                    t.fo_Cp = fo.Cp;
+                    t.fo_hh = fo.hh;
+                    t.fo_hw = fo.hw;
+                    t.labels = p.labels;
+                    t.l_ss = (int64_t)lh_ * lw_;
+                    launch_conv_tc(*tc_[k], p.T[k], p.T[k + 1], dBias_[k], idx, count, full_count, relu,
+                                   chg_next, tau_next, cnt_next, 2, S, st, &t);
+                    mark("conv_tc_tail", k);
+                    p.fused_from = k;
+                    break;
+                } else if (tc_[k] && !planar_in) {
                     launch_conv_tc(*tc_[k], p.T[k], p.T[k + 1], dBias_[k], idx, count, full_count, relu,
                                    chg_next, tau_next, cnt_next, 2, S, st);
                     mark("conv_tc", k);
@@ -501,8 +538,9 @@ void Engine::record(Plan& p, bool full) {
                 mark("classify", k);
                 break;
         }
+        if (p.fused_from == k) break;  // the rest of the network ran in that epilogue
     }
-    if (layers_.back().kind != CBX_CLASSIFY) {
+    if (p.fused_from < 0 && layers_.back().kind != CBX_CLASSIFY) {
         launch_classify_bits(p.T[nl], full ? BitMask{nullptr, 0, 0, 0, 0} : p.upd[nl], p.labels, S, st);
         mark("classify", nl);
     }
@@ -689,6 +727,9 @@ void Engine::get_activation(int engine, int layer, int s, float* out) {
     if (layer < 0 || layer >= (int)layers_.size() || s < 0 || s >= S_) throw Error(CBX_E_BOUNDS, "layer/stream out of range");
     if (layers_[layer].kind == CBX_CLASSIFY) throw Error(CBX_E_SPEC, "CLASSIFY produces labels, not an activation");
     Plan& p = plan(engine);
+    if (p.fused_from >= 0 && layer + 1 > p.fused_from && layer + 1 < final_tensor())
+        throw Error(CBX_E_SPEC, "layer " + std::to_string(layer + 1) +
+                                    " output is not materialized (fused tail); set CBX_OPT_FUSE_TAIL = 0");
     const TensorView& t = p.T[layer + 1];
     const size_t n = (size_t)t.C * t.H * t.W;
     float* tmp = nullptr;
@@ -791,6 +832,48 @@ void Engine::profile(int engine, const float* const* frames_dev, std::vector<cbx
         has_history_ = true;
         last_cb_frames_.assign(frames_dev, frames_dev + S_);
     }
+}
+
+}  // namespace cbx
+
+namespace cbx {
+
+// Index of the tensor classified into labels (input of CLASSIFY, or the last
+// layer's output when the network has no CLASSIFY).
+int Engine::final_tensor() const {
+    const int nl = (int)layers_.size();
+    return layers_.back().kind == CBX_CLASSIFY ? nl - 1 : nl;
+}
+
+// Last layer of a per-pixel tail that can run in the epilogue of tcgen05 conv
+// k: 1x1 CONVs (<= kTailMaxC outputs) and RELUs up to the end of the network
+// (optionally closed by CLASSIFY), first op a CONV. -1 when not fusable.
+int Engine::tail_end(int k) const {
+    const int nl = (int)layers_.size();
+    if (!fuse_tail_ || k + 1 >= nl) return -1;
+    const auto& first = layers_[k + 1];
+    if (first.kind != CBX_CONV || !identity_geom(first.geom) || first.geom.outChannels > kTailMaxC) return -1;
+    int ops = 0;
+    for (int j = k + 1; j < nl; ++j) {
+        const auto& l = layers_[j];
+        if (l.kind == CBX_CLASSIFY) return j == nl - 1 ? j : -1;
+        if (l.kind == CBX_RELU) {
+            ++ops;
+        } else if (l.kind == CBX_CONV && identity_geom(l.geom) && l.geom.outChannels <= kTailMaxC) {
+            ++ops;
+        } else {
+            return -1;
+        }
+        if (ops > kTailMaxOps) return -1;
+    }
+    return nl - 1;
+}
+
+void Engine::set_option(int option, int value) {
+    if (option != CBX_OPT_FUSE_TAIL) throw Error(CBX_E_ARG, "unknown option");
+    fuse_tail_ = value != 0;
+    cb_->dirty = true;
+    if (base_) base_->dirty = true;
 }
 
 }  // namespace cbx

@@ -59,6 +59,7 @@ public:
     void get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64_t* n, int* first);
 
     void profile(int engine, const float* const* frames_dev, std::vector<cbx_kernel_time>& out);
+    void set_option(int option, int value);
 
     cudaStream_t stream() const { return stream_; }
     int last_launch_count() const { return last_launches_; }
@@ -75,6 +76,9 @@ private:
     void stage_frame_pointers(int engine, const float* const* cur, const float* const* prev);
     void finish_stats(Plan& p, bool full, int engine);
     void mark(const char* name, int layer);
+    int tail_end(int k) const;
+    int final_tensor() const;
+    bool fuse_tail_ = true;
 
     struct ProfMark {
         std::string name;

@@ -457,57 +457,35 @@ __global__ void __launch_bounds__(kPtThreads) point_bits_kernel(PointBitsArgs a)
             if (lane == 0) s_changed[wib] = 0;
             __syncwarp();
             const int items = 32 * c4n;
-            const int rowq = a.in.Wp * c4n;
-            // two (pixel, channel-quad) items per lane per pass: all window
-            // loads of both are in flight before the max/compare/store
-            for (int it0 = lane; it0 < items; it0 += 64) {
-                const float4* src[2];
-                float4* dst[2];
-                bool has[2];
-                int jj[2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int it = it0 + 32 * u;
-                    const int j = it / c4n, c4 = it - j * c4n;
-                    jj[u] = j;
-                    has[u] = it < items && ((tw >> j) & 1u);
-                    const int xj = 32 * w + (has[u] ? j : 0);
-                    src[u] = reinterpret_cast<const float4*>(
-                                 a.in.d + (int64_t)s * a.in.ss +
-                                 ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + xj * a.stride + a.in.hw) * a.in.Cp) + c4;
-                    dst[u] = reinterpret_cast<float4*>(
-                                 a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + xj + a.out.hw) * a.out.Cp) + c4;
-                }
-                float4 m[2], o[2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    m[u] = has[u] ? *src[u] : make_float4(0.f, 0.f, 0.f, 0.f);
-                    o[u] = (has[u] && a.chg.d) ? *dst[u] : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
+            for (int it = lane; it < items; it += 32) {
+                const int j = it / c4n, c4 = it - j * c4n;
+                if (!((tw >> j) & 1u)) continue;
+                const int xj = 32 * w + j;
+                const float4* src = reinterpret_cast<const float4*>(
+                    a.in.d + (int64_t)s * a.in.ss +
+                    ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + xj * a.stride + a.in.hw) * a.in.Cp) + c4;
+                float4* dst = reinterpret_cast<float4*>(
+                    a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + xj + a.out.hw) * a.out.Cp) + c4;
+                float4 m;
                 if (a.relu) {
-#pragma unroll
-                    for (int u = 0; u < 2; ++u)
-                        m[u] = make_float4(ref_relu(m[u].x), ref_relu(m[u].y), ref_relu(m[u].z), ref_relu(m[u].w));
+                    const float4 v = *src;
+                    m = make_float4(ref_relu(v.x), ref_relu(v.y), ref_relu(v.z), ref_relu(v.w));
                 } else {
+                    m = *src;
+                    const int rowq = a.in.Wp * c4n;
                     for (int kj = 0; kj < a.window; ++kj)
                         for (int ki = 0; ki < a.window; ++ki) {
-                            float4 v[2];
-#pragma unroll
-                            for (int u = 0; u < 2; ++u) v[u] = has[u] ? src[u][kj * rowq + ki * c4n] : m[u];
-#pragma unroll
-                            for (int u = 0; u < 2; ++u)
-                                m[u] = make_float4(ref_max(m[u].x, v[u].x), ref_max(m[u].y, v[u].y), ref_max(m[u].z, v[u].z),
-                                                   ref_max(m[u].w, v[u].w));
+                            const float4 v = src[kj * rowq + ki * c4n];
+                            m = make_float4(ref_max(m.x, v.x), ref_max(m.y, v.y), ref_max(m.z, v.z), ref_max(m.w, v.w));
                         }
                 }
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    if (!has[u]) continue;
-                    if (a.chg.d && (ref_changed(m[u].x, o[u].x, a.tau) | ref_changed(m[u].y, o[u].y, a.tau) |
-                                    ref_changed(m[u].z, o[u].z, a.tau) | ref_changed(m[u].w, o[u].w, a.tau)))
-                        atomicOr(&s_changed[wib], 1u << jj[u]);
-                    *dst[u] = m[u];
+                if (a.chg.d) {
+                    const float4 o = *dst;
+                    if (ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
+                        ref_changed(m.w, o.w, a.tau))
+                        atomicOr(&s_changed[wib], 1u << j);
                 }
+                *dst = m;
             }
             __syncwarp();
             cw = s_changed[wib];

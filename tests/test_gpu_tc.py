@@ -54,3 +54,26 @@ def test_tc_layer_vs_exact(gpu, orc, cin, h, w, layer):
         err = np.abs(got.astype(np.float64) - want)
         bound = 2.0 ** -9 * scale + 1e-6
         assert np.all(err <= bound), (float((err / bound).max()), float(err.max()))
+
+
+def test_fused_tail_equals_unfused(gpu, orc):
+    """The per-pixel head (1x1 CONV, RELU, 1x1 CONV, CLASSIFY) run inside the
+    last tcgen05 conv's epilogue gives bitwise the same labels, final
+    activation and stats as running every layer separately."""
+    from netutil import paper_spec, stats_arr
+    spec = paper_spec(72, 112)
+    w = orc.generate_weights(spec, 1)
+    fused = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32", fuse_tail=True)
+    plain = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32", fuse_tail=False)
+    cfg = dict(channels=3, height=72, width=112, sprites=[(14, 3, 0.9)], noise=0.01, seed=4)
+    for f in range(4):
+        fr = orc.synth_frame(cfg, f)
+        a, b = fused.forward_frame(fr), plain.forward_frame(fr)
+        assert np.array_equal(a.labels, b.labels)
+        assert np.array_equal(stats_arr(a.stats), stats_arr(b.stats))
+        assert np.array_equal(fused.final_activation().view(np.uint32), plain.final_activation().view(np.uint32))
+    with pytest.raises(gpu.SpecError):
+        fused.layer_output(5)  # the head's first 1x1 conv output is not materialized
+    for engine in ("baseline",):
+        a, b = fused.forward_frame(fr, engine), plain.forward_frame(fr, engine)
+        assert np.array_equal(a.labels, b.labels)
