@@ -185,6 +185,7 @@ struct TcArgs {
     unsigned long long* chg_cnt;
     int cnt_stride;
     int write_out;  // store this layer's output tensor (off when a fused tail consumes it)
+    int tail_w_floats;  // shared memory reserved for the first tail conv's filters
     TcTail tail;
 };
 
@@ -202,8 +203,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
     uint8_t* sB = sA + (size_t)NS * kABytes;             // NS x b_bytes
     int* sTab = reinterpret_cast<int*>(sB + (size_t)NS * b_bytes);   // NKB*8 chunk offsets (floats)
     float* sBias = reinterpret_cast<float*>(sTab + a.NKB * kChunksPerKB);
+    float* sTailW = sBias + ((a.O + 3) & ~3);  // first tail conv's filters [c1][O] (16B aligned)
     uint64_t* bars = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(sBias + ((a.O + 3) & ~3)) + 7) & ~uintptr_t(7));
+        (reinterpret_cast<uintptr_t>(sTailW + a.tail_w_floats) + 7) & ~uintptr_t(7));
     uint64_t* full = bars;
     uint64_t* empty = full + NS;
     uint64_t* tfull = empty + NS;
@@ -226,6 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
         sTab[j] = off;
     }
     for (int o = tid; o < a.O; o += kThreads) sBias[o] = a.bias[o];
+    if (a.tail.n) {
+        const int nw = a.tail.cout[0] * a.O;
+        for (int i = tid; i < nw; i += kThreads) sTailW[i] = a.tail.W[0][i];
+    }
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], kProdThreads + 1);
@@ -404,13 +410,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
                             w4[e] = a.relu ? ref_relu(t) : t;
                         }
                         if (n_tail) {
-                            const float* W0 = a.tail.W[0];
+                            const float* W0 = sTailW;
                             if ((a.O & 3) == 0) {
                                 // 4 ascending channels per 16-byte weight load (warp-uniform address)
 #pragma unroll
                                 for (int q = 0; q < kTailMaxC; ++q) {
                                     if (q >= c1) break;
-                                    const float4 wq = __ldg(reinterpret_cast<const float4*>(W0 + (int64_t)q * a.O + o));
+                                    const float4 wq = *reinterpret_cast<const float4*>(W0 + q * a.O + o);
                                     float acc = t1[q];
                                     acc = __fadd_rn(acc, __fmul_rn(wq.x, w4[0]));
                                     acc = __fadd_rn(acc, __fmul_rn(wq.y, w4[1]));
@@ -424,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
                                     if (o + e >= a.O) break;
 #pragma unroll
                                     for (int q = 0; q < kTailMaxC; ++q)
-                                        if (q < c1) t1[q] = __fadd_rn(t1[q], __fmul_rn(__ldg(W0 + (int64_t)q * a.O + o + e), w4[e]));
+                                        if (q < c1) t1[q] = __fadd_rn(t1[q], __fmul_rn(W0[q * a.O + o + e], w4[e]));
                                 }
                             }
                         }
@@ -479,6 +485,7 @@ struct TcLayer {
     cbx_geom g;
     int Cp = 0, NKB = 0, Npad = 0, N0 = 0, N1 = 0;
     int stages = 0, acc_stages = 1, acc_cols = 0, tmem_cols = 32;
+    int tail_w_floats = 0;
     size_t smem = 0;
     float* Bw = nullptr;
 };
@@ -493,7 +500,7 @@ bool tc_supported(const cbx_geom& g) {
     return g.outChannels >= 1 && Npad <= 512 && g.kernelH * g.kernelW * round_up(g.inChannels, 4) <= 65536;
 }
 
-std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g) {
+std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats) {
     std::unique_ptr<TcLayer, TcLayerDeleter> t(new TcLayer);
     t->g = g;
     t->Cp = (int)round_up(g.inChannels, 4);
@@ -508,7 +515,9 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g) {
     while (cols < t->acc_stages * t->acc_cols) cols *= 2;
     t->tmem_cols = cols;
     const size_t b_bytes = (size_t)t->Npad * 128;
-    const size_t fixed = 1024 + (size_t)t->NKB * kChunksPerKB * 4 + round_up(g.outChannels, 4) * 4 + 16 + 8 * (2 * 16 + 4) + 16;
+    t->tail_w_floats = (int)round_up(tail_floats, 4);
+    const size_t fixed = 1024 + (size_t)t->NKB * kChunksPerKB * 4 + round_up(g.outChannels, 4) * 4 +
+                         (size_t)t->tail_w_floats * 4 + 16 + 8 * (2 * 16 + 4) + 16;
     int ns = 8;
     while (ns > 2 && fixed + (size_t)ns * (kABytes + b_bytes) > (size_t)kMaxSmem) --ns;
     if (fixed + (size_t)ns * (kABytes + b_bytes) > (size_t)kMaxSmem)
@@ -587,6 +596,9 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.acc_stages = t.acc_stages;
     a.acc_cols = t.acc_cols;
     a.tmem_cols = t.tmem_cols;
+    a.tail_w_floats = t.tail_w_floats;
+    if (tail && tail->n && tail->cout[0] * out.C > t.tail_w_floats)
+        throw Error(CBX_E_ARG, "tcgen05 conv: fused tail filters exceed the reserved shared memory");
     a.relu = relu;
     a.chg = chg;
     a.tau = tau;

@@ -195,8 +195,11 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
             // first layer reading the planar frame).
             // (N >= 32 output channels: narrower 1x1 heads stay exact on CUDA cores,
             //  usually fused into the epilogue of the preceding tcgen05 layer)
-            if (precision_ == CBX_PREC_TF32 && k > 0 && g.outChannels >= 32 && tc_supported(g))
-                tc_[k] = make_tc_layer(g);
+            if (precision_ == CBX_PREC_TF32 && k > 0 && g.outChannels >= 32 && tc_supported(g)) {
+                const int te = tail_end(k);
+                const int tail_floats = te > 0 ? layers_[k + 1].geom.outChannels * g.outChannels : 0;
+                tc_[k] = make_tc_layer(g, tail_floats);
+            }
         }
     }
     const bool hasClassify = layers_.back().kind == CBX_CLASSIFY;
