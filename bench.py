@@ -245,7 +245,12 @@ def algorithmic_work(kernel, layer, st, S, dims, spec):
         while spec["layers"][src]["kind"] != "CBCONV" and src > 0:
             src -= 1
         n = sum(s[src]["changedOutputPixels"] for s in st)
-        return 2 * g * n, "tensor" if kernel == "conv_tc" else "fp32"
+        if kernel == "conv_tc_tail":  # + the fused 1x1 head convs on the same pixels
+            for j in range(layer + 1, len(spec["layers"])):
+                lj = spec["layers"][j]
+                if lj["kind"] == "CONV":
+                    g += dims[j][0][0] * lj["outChannels"]
+        return 2 * g * n, "tensor" if kernel.startswith("conv_tc") else "fp32"
     if kernel == "pool":
         (c, h, w), (_, ho, wo) = dims[layer]
         cp = (c + 3) // 4 * 4
@@ -366,7 +371,16 @@ def run_gpu_arm(args):
         peak = tf32 if bound == "tensor" else 75.0
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    # DRAM bytes per launch of this kernel from the committed ncu --set full capture
     roof["traffic"] = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        ent = tr.get("kernels", {}).get(f"{kname}[{klayer}]")
+        if ent:
+            roof["traffic"] = ent["dram_bytes"]
+            roof["traffic_source"] = tr.get("source")
+    except (OSError, ValueError):
+        pass
     roof["kernel"] = f"{kname}[layer {klayer}]"
     roof["kernel_share_of_step"] = kms / step_ms if step_ms else None
     roof["peak_source"] = (f"{peak_src} MEASURED_PEAKS.json" + ("" if bound == "hbm" else

@@ -1,0 +1,101 @@
+// cbx_run -- C++ host driver over the drop-in API (include/cbinfer_b200.hpp),
+// the B200 counterpart of the reference CLI's `cbench run`
+// (/root/reference/proj/tools/cbench.cpp:95-173): runs a frame sequence
+// through one Network and prints one CSV row per frame.
+//
+//   cbx_run --net spec.json --weights DIR [--seq DIR | --synth C,H,W,N,SIZE,VEL,SEED]
+//           [--engine cbinfer|baseline] [--precision tf32|exact] [--thresholds a,b,c]
+//
+// --seq reads frame_%04d.f32le + manifest.json (synth.cpp:130-186 layout).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "cbinfer_b200.hpp"
+
+namespace cb = cbinfer_b200;
+
+static std::vector<float> parse_floats(const std::string& s) {
+    std::vector<float> v;
+    std::stringstream ss(s);
+    std::string tok;
+    while (std::getline(ss, tok, ',')) v.push_back(std::stof(tok));
+    return v;
+}
+
+int main(int argc, char** argv) {
+    std::string net_path, wdir, seq, synth, engine = "cbinfer", precision = "tf32", taus;
+    for (int i = 1; i + 1 < argc; i += 2) {
+        const std::string k = argv[i], v = argv[i + 1];
+        if (k == "--net") net_path = v;
+        else if (k == "--weights") wdir = v;
+        else if (k == "--seq") seq = v;
+        else if (k == "--synth") synth = v;
+        else if (k == "--engine") engine = v;
+        else if (k == "--precision") precision = v;
+        else if (k == "--thresholds") taus = v;
+        else {
+            std::cerr << "unknown option " << k << "\n";
+            return 1;
+        }
+    }
+    if (net_path.empty() || wdir.empty() || (seq.empty() && synth.empty())) {
+        std::cerr << "usage: cbx_run --net spec.json --weights DIR (--seq DIR | --synth C,H,W,N,SIZE,VEL,SEED)\n";
+        return 1;
+    }
+    try {
+        cb::NetworkSpec spec = cb::load_network_spec(net_path);
+        cb::Network net(spec, wdir, 0, precision == "exact" ? cb::Precision::Exact : cb::Precision::TF32);
+        if (!taus.empty()) net.set_thresholds(parse_floats(taus));
+        const cb::Engine eng = engine == "baseline" ? cb::Engine::Baseline : cb::Engine::CBInfer;
+        std::vector<cb::FrameTensor> frames;
+        if (!seq.empty()) {
+            auto man = nlohmann::json::parse(std::ifstream(seq + "/manifest.json"));
+            const int C = man.at("channels"), H = man.at("height"), W = man.at("width"), N = man.at("frames");
+            for (int f = 0; f < N; ++f) {
+                char name[64];
+                std::snprintf(name, sizeof(name), "/frame_%04d.f32le", f);
+                cb::FrameTensor t(C, H, W);
+                std::ifstream in(seq + name, std::ios::binary);
+                if (!in) throw cb::io_error(std::string("missing frame ") + seq + name);
+                in.read(reinterpret_cast<char*>(t.data.data()), std::streamsize(t.data.size() * 4));
+                frames.push_back(std::move(t));
+            }
+        } else {
+            const auto v = parse_floats(synth);
+            if (v.size() != 7) throw cb::spec_error("--synth needs C,H,W,N,SIZE,VEL,SEED");
+            cbx_sprite sp{int(v[4]), int(v[5]), 0.9f};
+            cbx_synth_cfg cfg{int(v[0]), int(v[1]), int(v[2]), int(v[3]), 1, &sp, 0.0f, uint32_t(v[6])};
+            for (int f = 0; f < cfg.frames; ++f) {
+                cb::FrameTensor t(cfg.channels, cfg.height, cfg.width);
+                cb::check(cbx_synth_frame(&cfg, f, t.data.data()));
+                frames.push_back(std::move(t));
+            }
+        }
+        std::cout << "frame,wallNanos,macsTotal";
+        for (size_t k = 0; k < spec.layers.size(); ++k)
+            if (spec.layers[k].kind == cb::LayerKind::CBCONV) std::cout << ",changedIn" << k + 1 << ",changedOut" << k + 1;
+        std::cout << ",labelChecksum\n";
+        for (size_t f = 0; f < frames.size(); ++f) {
+            const auto t0 = std::chrono::steady_clock::now();
+            cb::ForwardResult r = cb::forward_frame(net, frames[f], eng);
+            const auto t1 = std::chrono::steady_clock::now();
+            uint64_t sum = 0;
+            for (size_t i = 0; i < r.labels.labels.size(); ++i) sum += uint64_t(r.labels.labels[i]) * (i % 9973 + 1);
+            std::cout << f << "," << std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count() << ","
+                      << r.macsTotal;
+            for (size_t k = 0; k < spec.layers.size(); ++k)
+                if (spec.layers[k].kind == cb::LayerKind::CBCONV)
+                    std::cout << "," << r.stats[k].changedInputPixels << "," << r.stats[k].changedOutputPixels;
+            std::cout << "," << sum << "\n";
+        }
+        return 0;
+    } catch (const cb::error& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 2;
+    }
+}
