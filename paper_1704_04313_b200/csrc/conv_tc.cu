@@ -127,24 +127,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // channel order, one rounding per multiply and add -- the reference gemm
 // order), then the final activation is stored and argmax-classified with the
 // reference tie rule (strict >, lowest channel wins).
-__device__ __forceinline__ void run_tail(const TcTail& t, float (&cur)[kTailMaxC], int s, int y, int x, int p) {
+template <int TC>
+__device__ __forceinline__ void run_tail(const TcTail& t, float (&cur)[TC], int s, int y, int x, int p) {
     int C = t.cout[0];
     for (int k = 1; k < t.n; ++k) {
         if (t.kind[k] == 1) {
 #pragma unroll
-            for (int q = 0; q < kTailMaxC; ++q) cur[q] = ref_relu(cur[q]);
+            for (int q = 0; q < TC; ++q) cur[q] = ref_relu(cur[q]);
         } else {
             const int O = t.cout[k];
-            float nxt[kTailMaxC];
+            float nxt[TC];
 #pragma unroll
-            for (int q = 0; q < kTailMaxC; ++q) {
+            for (int q = 0; q < TC; ++q) {
                 float acc = (q < O) ? __ldg(t.b[k] + q) : 0.0f;
-                if (q < O)
-                    for (int c = 0; c < C; ++c) acc = __fadd_rn(acc, __fmul_rn(__ldg(t.W[k] + q * C + c), cur[c]));
+#pragma unroll
+                for (int c = 0; c < TC; ++c)
+                    if (q < O && c < C) acc = __fadd_rn(acc, __fmul_rn(__ldg(t.W[k] + q * C + c), cur[c]));
                 nxt[q] = acc;
             }
 #pragma unroll
-            for (int q = 0; q < kTailMaxC; ++q) cur[q] = nxt[q];
+            for (int q = 0; q < TC; ++q) cur[q] = nxt[q];
             C = O;
         }
     }
@@ -152,12 +154,13 @@ __device__ __forceinline__ void run_tail(const TcTail& t, float (&cur)[kTailMaxC
     int best = 0;
     float bv = cur[0];
 #pragma unroll
-    for (int q = 0; q < kTailMaxC; ++q) {
-        if (q >= C) break;
-        fo[q] = cur[q];
-        if (q > 0 && cur[q] > bv) {
-            bv = cur[q];
-            best = q;
+    for (int q = 0; q < TC; ++q) {
+        if (q < C) {
+            fo[q] = cur[q];
+            if (q > 0 && cur[q] > bv) {
+                bv = cur[q];
+                best = q;
+            }
         }
     }
     t.labels[(int64_t)s * t.l_ss + p] = (uint16_t)best;
@@ -193,7 +196,7 @@ struct TcArgs {
 // when a pixel's taps are 16 B, i.e. 4 channels, so a warp's 32 rows of one
 // tap are 32 neighbouring pixels). Otherwise 8 lanes cooperate on a row's 128
 // contiguous K-block bytes and a warp instruction covers 4 rows.
-template <bool ROWLANE>
+template <bool ROWLANE, int TC>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
     uint8_t* sB = sA + (size_t)NS * kABytes;             // NS x b_bytes
     int* sTab = reinterpret_cast<int*>(sB + (size_t)NS * b_bytes);   // NKB*8 chunk offsets (floats)
     float* sBias = reinterpret_cast<float*>(sTab + a.NKB * kChunksPerKB);
-    float* sTailW = sBias + ((a.O + 3) & ~3);  // first tail conv's filters [c1][O] (16B aligned)
+    float* sTailW = sBias + ((a.O + 3) & ~3);  // first tail conv's filters, transposed [O][TC] (16B aligned)
     uint64_t* bars = reinterpret_cast<uint64_t*>(
         (reinterpret_cast<uintptr_t>(sTailW + a.tail_w_floats) + 7) & ~uintptr_t(7));
     uint64_t* full = bars;
@@ -228,9 +231,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
         sTab[j] = off;
     }
     for (int o = tid; o < a.O; o += kThreads) sBias[o] = a.bias[o];
-    if (a.tail.n) {
-        const int nw = a.tail.cout[0] * a.O;
-        for (int i = tid; i < nw; i += kThreads) sTailW[i] = a.tail.W[0][i];
+    if (TC > 0) {
+        const int c1 = a.tail.cout[0];
+        for (int i = tid; i < a.O * TC; i += kThreads) {
+            const int o = i / TC, q = i - o * TC;
+            sTailW[i] = q < c1 ? a.tail.W[0][q * a.O + o] : 0.0f;
+        }
     }
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -390,11 +396,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
             const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16) + as * a.acc_cols;
             // fused per-pixel tail: first op is a 1x1 CONV over this layer's
             // outputs, accumulated chunk by chunk in ascending channel order
-            const int n_tail = a.tail.n;
-            const int c1 = n_tail ? a.tail.cout[0] : 0;
-            float t1[kTailMaxC];
+            constexpr int TCA = TC > 0 ? TC : 1;
+            float t1[TCA];
 #pragma unroll
-            for (int q = 0; q < kTailMaxC; ++q) t1[q] = (q < c1) ? __ldg(a.tail.b[0] + q) : 0.0f;
+            for (int q = 0; q < TCA; ++q) t1[q] = (TC > 0 && q < a.tail.cout[0]) ? __ldg(a.tail.b[0] + q) : 0.0f;
             for (int c0 = 0; c0 < a.O; c0 += 32) {
                 float v[32];
                 tmem_ld32(trow + c0, v);
@@ -409,28 +414,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
                             const float t = (o + e < a.O) ? __fadd_rn(v[j + e], sBias[o + e]) : 0.0f;
                             w4[e] = a.relu ? ref_relu(t) : t;
                         }
-                        if (n_tail) {
-                            const float* W0 = sTailW;
-                            if ((a.O & 3) == 0) {
-                                // 4 ascending channels per 16-byte weight load (warp-uniform address)
+                        if constexpr (TC > 0) {
+                            // ascending channels; the TC filters of one channel are TC/4 broadcast LDS.128
 #pragma unroll
-                                for (int q = 0; q < kTailMaxC; ++q) {
-                                    if (q >= c1) break;
-                                    const float4 wq = *reinterpret_cast<const float4*>(W0 + q * a.O + o);
-                                    float acc = t1[q];
-                                    acc = __fadd_rn(acc, __fmul_rn(wq.x, w4[0]));
-                                    acc = __fadd_rn(acc, __fmul_rn(wq.y, w4[1]));
-                                    acc = __fadd_rn(acc, __fmul_rn(wq.z, w4[2]));
-                                    acc = __fadd_rn(acc, __fmul_rn(wq.w, w4[3]));
-                                    t1[q] = acc;
-                                }
-                            } else {
+                            for (int e = 0; e < 4; ++e) {
+                                if (o + e >= a.O) break;
+                                const float4* w = reinterpret_cast<const float4*>(sTailW + (o + e) * TC);
 #pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    if (o + e >= a.O) break;
-#pragma unroll
-                                    for (int q = 0; q < kTailMaxC; ++q)
-                                        if (q < c1) t1[q] = __fadd_rn(t1[q], __fmul_rn(W0[q * a.O + o + e], w4[e]));
+                                for (int q4 = 0; q4 < TC / 4; ++q4) {
+                                    const float4 wq = w[q4];
+                                    t1[4 * q4 + 0] = __fadd_rn(t1[4 * q4 + 0], __fmul_rn(wq.x, w4[e]));
+                                    t1[4 * q4 + 1] = __fadd_rn(t1[4 * q4 + 1], __fmul_rn(wq.y, w4[e]));
+                                    t1[4 * q4 + 2] = __fadd_rn(t1[4 * q4 + 2], __fmul_rn(wq.z, w4[e]));
+                                    t1[4 * q4 + 3] = __fadd_rn(t1[4 * q4 + 3], __fmul_rn(wq.w, w4[e]));
                                 }
                             }
                         }
@@ -454,7 +450,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
             }
             tc_fence_before();
             mbar_arrive(&tempty[as]);
-            if (n_tail && valid) run_tail(a.tail, t1, s, y, x, p);
+            if constexpr (TC > 0) {
+                if (valid) run_tail<TC>(a.tail, t1, s, y, x, p);
+            }
             if (a.chg.d) {
                 if (valid && changed) bit_set(a.chg, s, y, x);
                 if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
@@ -524,8 +522,12 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
         throw Error(CBX_E_ARG, "tcgen05 conv: layer too wide for shared memory");
     t->stages = ns;
     t->smem = fixed + (size_t)ns * (kABytes + b_bytes);
-    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CBX_CUDA(cudaMalloc(&t->Bw, (size_t)t->NKB * b_bytes));
     CBX_CUDA(cudaMemset(t->Bw, 0, (size_t)t->NKB * b_bytes));
     return t;
@@ -597,7 +599,7 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.acc_cols = t.acc_cols;
     a.tmem_cols = t.tmem_cols;
     a.tail_w_floats = t.tail_w_floats;
-    if (tail && tail->n && tail->cout[0] * out.C > t.tail_w_floats)
+    if (tail && tail->n && (tail->cout[0] <= 8 ? 8 : 16) * out.C > t.tail_w_floats)
         throw Error(CBX_E_ARG, "tcgen05 conv: fused tail filters exceed the reserved shared memory");
     a.relu = relu;
     a.chg = chg;
@@ -608,10 +610,17 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     if (tail) a.tail = *tail;
     const int64_t max_tiles = (full_count + kTileM - 1) / kTileM;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, kNumSMs));
-    if (in.Cp <= 4)
-        conv_tc_kernel<true><<<grid, kThreads, t.smem, st>>>(a);
-    else
-        conv_tc_kernel<false><<<grid, kThreads, t.smem, st>>>(a);
+    const int tc = (tail && tail->n) ? (tail->cout[0] <= 8 ? 8 : 16) : 0;
+    const bool rowlane = in.Cp <= 4;
+#define CBX_TC_LAUNCH(R, T) conv_tc_kernel<R, T><<<grid, kThreads, t.smem, st>>>(a)
+    if (tc == 0) {
+        if (rowlane) CBX_TC_LAUNCH(true, 0); else CBX_TC_LAUNCH(false, 0);
+    } else if (tc == 8) {
+        if (rowlane) CBX_TC_LAUNCH(true, 8); else CBX_TC_LAUNCH(false, 8);
+    } else {
+        if (rowlane) CBX_TC_LAUNCH(true, 16); else CBX_TC_LAUNCH(false, 16);
+    }
+#undef CBX_TC_LAUNCH
 }
 
 }  // namespace cbx

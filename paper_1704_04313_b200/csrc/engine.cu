@@ -197,7 +197,8 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
             //  usually fused into the epilogue of the preceding tcgen05 layer)
             if (precision_ == CBX_PREC_TF32 && k > 0 && g.outChannels >= 32 && tc_supported(g)) {
                 const int te = tail_end(k);
-                const int tail_floats = te > 0 ? layers_[k + 1].geom.outChannels * g.outChannels : 0;
+                const int c1 = te > 0 ? layers_[k + 1].geom.outChannels : 0;
+                const int tail_floats = te > 0 ? (c1 <= 8 ? 8 : 16) * g.outChannels : 0;
                 tc_[k] = make_tc_layer(g, tail_floats);
             }
         }
