@@ -197,7 +197,7 @@ struct TcArgs {
 // tap are 32 neighbouring pixels). Otherwise 8 lanes cooperate on a row's 128
 // contiguous K-block bytes and a warp instruction covers 4 rows.
 template <bool ROWLANE, int TC>
-__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int NS = a.stages;
@@ -484,6 +484,7 @@ struct TcLayer {
     int Cp = 0, NKB = 0, Npad = 0, N0 = 0, N1 = 0;
     int stages = 0, acc_stages = 1, acc_cols = 0, tmem_cols = 32;
     int tail_w_floats = 0;
+    int ctas_per_sm = 1;
     size_t smem = 0;
     float* Bw = nullptr;
 };
@@ -516,9 +517,13 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     t->tail_w_floats = (int)round_up(tail_floats, 4);
     const size_t fixed = 1024 + (size_t)t->NKB * kChunksPerKB * 4 + round_up(g.outChannels, 4) * 4 +
                          (size_t)t->tail_w_floats * 4 + 16 + 8 * (2 * 16 + 4) + 16;
+    // narrow layers (N <= 128) run two CTAs per SM so that one CTA's gather
+    // latency overlaps the other's MMAs/epilogue; wide ones take the whole SM
+    t->ctas_per_sm = t->Npad <= 128 ? 2 : 1;
+    const size_t budget = t->ctas_per_sm == 2 ? (size_t)kMaxSmem / 2 - 1024 : (size_t)kMaxSmem;
     int ns = 8;
-    while (ns > 2 && fixed + (size_t)ns * (kABytes + b_bytes) > (size_t)kMaxSmem) --ns;
-    if (fixed + (size_t)ns * (kABytes + b_bytes) > (size_t)kMaxSmem)
+    while (ns > 2 && fixed + (size_t)ns * (kABytes + b_bytes) > budget) --ns;
+    if (fixed + (size_t)ns * (kABytes + b_bytes) > budget)
         throw Error(CBX_E_ARG, "tcgen05 conv: layer too wide for shared memory");
     t->stages = ns;
     t->smem = fixed + (size_t)ns * (kABytes + b_bytes);
@@ -609,7 +614,7 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.write_out = !(tail && tail->n && !tail->keep_out);
     if (tail) a.tail = *tail;
     const int64_t max_tiles = (full_count + kTileM - 1) / kTileM;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, kNumSMs));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, (int64_t)kNumSMs * t.ctas_per_sm));
     const int tc = (tail && tail->n) ? (tail->cout[0] <= 8 ? 8 : 16) : 0;
     const bool rowlane = in.Cp <= 4;
 #define CBX_TC_LAUNCH(R, T) conv_tc_kernel<R, T><<<grid, kThreads, t.smem, st>>>(a)

@@ -149,6 +149,8 @@ struct Engine::Plan {
     int launches[2] = {0, 0};
     bool dirty = true;
     int fused_from = -1;            // conv layer whose epilogue runs the per-pixel tail (-1: none)
+    uint2* work = nullptr;          // touched-word list shared by the MAXPOOL/RELU layers
+    int* work_count = nullptr;
 
     ~Plan() {
         for (auto& g : gexec)
@@ -383,6 +385,14 @@ void Engine::build_plan(Plan& p, bool baseline) {
             p.U[k] = p.mask(S, Ho, Wo);
     }
     if (ws) p.ws = p.alloc<uint8_t>(ws);
+    int64_t wk = 0;
+    for (int k = 0; k < nl; ++k)
+        if (layers_[k].kind == CBX_MAXPOOL || layers_[k].kind == CBX_RELU)
+            wk = std::max<int64_t>(wk, (int64_t)S * dims_[6 * k + 4] * ((dims_[6 * k + 5] + 31) / 32));
+    if (wk) {
+        p.work = p.alloc<uint2>((size_t)wk);
+        p.work_count = p.alloc<int>(1);
+    }
 }
 
 void Engine::record(Plan& p, bool full) {
@@ -533,6 +543,8 @@ void Engine::record(Plan& p, bool full) {
                 a.chg_cnt = cnt_next;
                 a.cnt_stride = 2;
                 a.S = S;
+                a.work = p.work;
+                a.work_count = p.work_count;
                 launch_point_bits(a, st);
                 mark(a.relu ? "relu" : "pool", k);
                 break;

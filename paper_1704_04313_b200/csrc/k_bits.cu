@@ -422,91 +422,117 @@ void launch_dilate_bits(BitMask in, BitMask out, int S, int kh, int kw, int sh, 
 // that neighbouring threads read neighbouring 16-byte chunks.
 constexpr int kPtThreads = 256;
 
-// One warp per output word (32 pixels of a row). Lanes first test their
-// pixel's input window against the updated mask (ballot -> touched word);
-// untouched words cost one mask probe and one store. Touched pixels are then
-// swept as (pixel, 4-channel) items so that neighbouring lanes read
-// neighbouring 16-byte chunks of the channels-last input.
-__global__ void __launch_bounds__(kPtThreads) point_bits_kernel(PointBitsArgs a) {
-    __shared__ uint32_t s_changed[kPtThreads / 32];
+// Phase 1 (sparse frames): one warp per output word (32 pixels of a row).
+// Lanes test their pixel's input window against the updated mask (ballot ->
+// touched word), reset the next layer's change word, write U_out, and append
+// touched words to a work list.
+__global__ void __launch_bounds__(kPtThreads) point_scan_kernel(PointBitsArgs a) {
     const int Ho = a.out.H, Wo = a.out.W;
     const int wpr = (Wo + 31) / 32;
     const int64_t nseg = (int64_t)a.S * Ho * wpr;
-    const int c4n = a.in.Cp / 4;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (kPtThreads / 32);
-    for (int64_t seg = (int64_t)blockIdx.x * (kPtThreads / 32) + wib; seg < nseg; seg += warps) {
+    for (int64_t seg = (int64_t)blockIdx.x * (kPtThreads / 32) + (threadIdx.x >> 5); seg < nseg; seg += warps) {
         const int s = (int)(seg / ((int64_t)Ho * wpr));
         const int64_t r = seg - (int64_t)s * Ho * wpr;
         const int y = (int)(r / wpr), w = (int)(r - (int64_t)(r / wpr) * wpr);
         const int x = 32 * w + lane;
-        bool t = x < Wo;
-        if (t && a.upd_in.d) {
-            bool any = false;
-            for (int kj = 0; kj < a.window && !any; ++kj)
+        bool t = false;
+        if (x < Wo) {
+            for (int kj = 0; kj < a.window && !t; ++kj)
                 for (int ki = 0; ki < a.window; ++ki)
                     if (bit_test(a.upd_in, s, y * a.stride + kj, x * a.stride + ki)) {
-                        any = true;
+                        t = true;
                         break;
                     }
-            t = any;
         }
         const uint32_t tw = __ballot_sync(0xffffffffu, t);
-        uint32_t cw = 0;
-        if (tw) {
-            if (lane == 0) s_changed[wib] = 0;
-            __syncwarp();
-            const int items = 32 * c4n;
-            for (int it = lane; it < items; it += 32) {
-                const int j = it / c4n, c4 = it - j * c4n;
-                if (!((tw >> j) & 1u)) continue;
-                const int xj = 32 * w + j;
-                const float4* src = reinterpret_cast<const float4*>(
-                    a.in.d + (int64_t)s * a.in.ss +
-                    ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + xj * a.stride + a.in.hw) * a.in.Cp) + c4;
-                float4* dst = reinterpret_cast<float4*>(
-                    a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + xj + a.out.hw) * a.out.Cp) + c4;
-                float4 m;
-                if (a.relu) {
-                    const float4 v = *src;
-                    m = make_float4(ref_relu(v.x), ref_relu(v.y), ref_relu(v.z), ref_relu(v.w));
-                } else {
-                    m = *src;
-                    const int rowq = a.in.Wp * c4n;
-                    for (int kj = 0; kj < a.window; ++kj)
-                        for (int ki = 0; ki < a.window; ++ki) {
-                            const float4 v = src[kj * rowq + ki * c4n];
-                            m = make_float4(ref_max(m.x, v.x), ref_max(m.y, v.y), ref_max(m.z, v.z), ref_max(m.w, v.w));
-                        }
-                }
-                if (a.chg.d) {
-                    const float4 o = *dst;
-                    if (ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
-                        ref_changed(m.w, o.w, a.tau))
-                        atomicOr(&s_changed[wib], 1u << j);
-                }
-                *dst = m;
-            }
-            __syncwarp();
-            cw = s_changed[wib];
-        }
         if (lane == 0) {
-            if (a.U_out.d) a.U_out.d[(int64_t)s * a.U_out.stride + (int64_t)y * wpr + w] = tw;
-            if (a.chg.d) {
-                a.chg.d[(int64_t)s * a.chg.stride + (int64_t)y * wpr + w] = cw;
-                if (a.chg_cnt && cw) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, (unsigned long long)__popc(cw));
+            const int64_t wo = (int64_t)y * wpr + w;
+            if (a.U_out.d) a.U_out.d[(int64_t)s * a.U_out.stride + wo] = tw;
+            if (a.chg.d) a.chg.d[(int64_t)s * a.chg.stride + wo] = 0u;
+            if (tw) a.work[atomicAdd(a.work_count, 1)] = make_uint2((uint32_t)seg, tw);
+        }
+    }
+}
+
+// Phase 2: one thread per (touched word, pixel, 4-channel quad) -- flat, so
+// the few touched words of a sparse frame are spread over the whole GPU.
+// Max-pool (first element seeds the max, then every window element,
+// baseline.cpp:134-138) or ReLU, compare-before-write for the next CBCONV:
+// the first thread to set a pixel's change bit counts it.
+template <bool FULL>
+__global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a) {
+    const int Ho = a.out.H, Wo = a.out.W;
+    const int wpr = (Wo + 31) / 32;
+    const int c4n = a.in.Cp / 4;
+    const int per_word = 32 * c4n;
+    const int64_t nwords = FULL ? (int64_t)a.S * Ho * wpr : (int64_t)*a.work_count;
+    const int64_t total = nwords * per_word;
+    const int rowq = a.in.Wp * c4n;
+    for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = f / per_word;
+        const int item = (int)(f - e * per_word);
+        const int j = item / c4n, c4 = item - j * c4n;
+        uint32_t seg, tw;
+        if (FULL) {
+            seg = (uint32_t)e;
+            tw = 0xffffffffu;
+        } else {
+            const uint2 wk = a.work[e];
+            seg = wk.x;
+            tw = wk.y;
+        }
+        if (!((tw >> j) & 1u)) continue;
+        const int s = (int)(seg / ((uint32_t)Ho * wpr));
+        const uint32_t r = seg - (uint32_t)s * Ho * wpr;
+        const int y = (int)(r / wpr), w = (int)(r - (r / wpr) * wpr);
+        const int x = 32 * w + j;
+        if (x >= Wo) continue;
+        const float4* src = reinterpret_cast<const float4*>(
+            a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
+        float4* dst = reinterpret_cast<float4*>(
+            a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp) + c4;
+        float4 m = *src;
+        if (a.relu) {
+            m = make_float4(ref_relu(m.x), ref_relu(m.y), ref_relu(m.z), ref_relu(m.w));
+        } else {
+            for (int kj = 0; kj < a.window; ++kj)
+                for (int ki = 0; ki < a.window; ++ki) {
+                    const float4 v = src[kj * rowq + ki * c4n];
+                    m = make_float4(ref_max(m.x, v.x), ref_max(m.y, v.y), ref_max(m.z, v.z), ref_max(m.w, v.w));
+                }
+        }
+        if (!FULL && a.chg.d) {
+            const float4 o = *dst;
+            if (ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
+                ref_changed(m.w, o.w, a.tau)) {
+                const uint32_t bit = 1u << j;
+                const uint32_t old = atomicOr(a.chg.d + (int64_t)s * a.chg.stride + (int64_t)y * wpr + w, bit);
+                if (!(old & bit) && a.chg_cnt) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, 1ull);
             }
         }
-        __syncwarp();
+        *dst = m;
     }
 }
 
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
     const int wpr = (a.out.W + 31) / 32;
     const int64_t nseg = (int64_t)a.S * a.out.H * wpr;
+    const int c4n = a.in.Cp / 4;
+    if (!a.upd_in.d) {  // full frame: every word, no change test (the next layer evaluates in full)
+        const int64_t total = nseg * 32 * c4n;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + kPtThreads - 1) / kPtThreads, (int64_t)kNumSMs * 16));
+        point_work_kernel<true><<<grid, kPtThreads, 0, st>>>(a);
+        return;
+    }
+    cudaMemsetAsync(a.work_count, 0, sizeof(int), st);
     const int64_t blocks = (nseg + kPtThreads / 32 - 1) / (kPtThreads / 32);
-    int grid = (int)std::min<int64_t>(blocks, (int64_t)kNumSMs * 8);
-    point_bits_kernel<<<grid < 1 ? 1 : grid, kPtThreads, 0, st>>>(a);
+    const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)kNumSMs * 8));
+    point_scan_kernel<<<g1, kPtThreads, 0, st>>>(a);
+    // the touched-word count is only known on the device: grid-stride over a
+    // fixed grid sized for the GPU
+    point_work_kernel<false><<<kNumSMs * 8, kPtThreads, 0, st>>>(a);
 }
 
 // ---------------------------------------------------------------------------

@@ -40,6 +40,8 @@ struct PointBitsArgs {  // MAXPOOL (window/stride) or RELU (relu=1, window=strid
     unsigned long long* chg_cnt;
     int cnt_stride;
     int S;
+    uint2* work;      // touched-word list (capacity S*Ho*wpr), sparse mode only
+    int* work_count;
 };
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st);
 void launch_classify_bits(TensorView in, BitMask upd, uint16_t* labels, int S, cudaStream_t st);
