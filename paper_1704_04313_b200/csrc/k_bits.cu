@@ -424,105 +424,132 @@ constexpr int kPtThreads = 256;
 
 // Phase 1 (sparse frames): one warp per output word (32 pixels of a row).
 // Lanes test their pixel's input window against the updated mask (ballot ->
-// touched word), reset the next layer's change word, write U_out, and append
-// touched words to a work list.
+// touched word), reset the next layer's change word and write U_out; touched
+// words are appended to a work list (one atomic per block).
 __global__ void __launch_bounds__(kPtThreads) point_scan_kernel(PointBitsArgs a) {
+    __shared__ int s_n, s_base;
+    __shared__ uint2 s_list[kPtThreads / 32];
     const int Ho = a.out.H, Wo = a.out.W;
     const int wpr = (Wo + 31) / 32;
     const int64_t nseg = (int64_t)a.S * Ho * wpr;
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (kPtThreads / 32);
-    for (int64_t seg = (int64_t)blockIdx.x * (kPtThreads / 32) + (threadIdx.x >> 5); seg < nseg; seg += warps) {
-        const int s = (int)(seg / ((int64_t)Ho * wpr));
-        const int64_t r = seg - (int64_t)s * Ho * wpr;
-        const int y = (int)(r / wpr), w = (int)(r - (int64_t)(r / wpr) * wpr);
-        const int x = 32 * w + lane;
-        bool t = false;
-        if (x < Wo) {
-            for (int kj = 0; kj < a.window && !t; ++kj)
-                for (int ki = 0; ki < a.window; ++ki)
-                    if (bit_test(a.upd_in, s, y * a.stride + kj, x * a.stride + ki)) {
-                        t = true;
-                        break;
-                    }
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    for (int64_t base = (int64_t)blockIdx.x * (kPtThreads / 32); base < nseg; base += (int64_t)gridDim.x * (kPtThreads / 32)) {
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        const int64_t seg = base + wib;
+        uint32_t tw = 0;
+        if (seg < nseg) {
+            const int s = (int)(seg / ((int64_t)Ho * wpr));
+            const int64_t r = seg - (int64_t)s * Ho * wpr;
+            const int y = (int)(r / wpr), w = (int)(r - (int64_t)(r / wpr) * wpr);
+            const int x = 32 * w + lane;
+            bool t = false;
+            if (x < Wo) {
+                for (int kj = 0; kj < a.window && !t; ++kj)
+                    for (int ki = 0; ki < a.window; ++ki)
+                        if (bit_test(a.upd_in, s, y * a.stride + kj, x * a.stride + ki)) {
+                            t = true;
+                            break;
+                        }
+            }
+            tw = __ballot_sync(0xffffffffu, t);
+            if (lane == 0) {
+                const int64_t wo = (int64_t)y * wpr + w;
+                if (a.U_out.d) a.U_out.d[(int64_t)s * a.U_out.stride + wo] = tw;
+                if (a.chg.d) a.chg.d[(int64_t)s * a.chg.stride + wo] = 0u;
+                if (tw) s_list[atomicAdd(&s_n, 1)] = make_uint2((uint32_t)seg, tw);
+            }
         }
-        const uint32_t tw = __ballot_sync(0xffffffffu, t);
-        if (lane == 0) {
-            const int64_t wo = (int64_t)y * wpr + w;
-            if (a.U_out.d) a.U_out.d[(int64_t)s * a.U_out.stride + wo] = tw;
-            if (a.chg.d) a.chg.d[(int64_t)s * a.chg.stride + wo] = 0u;
-            if (tw) a.work[atomicAdd(a.work_count, 1)] = make_uint2((uint32_t)seg, tw);
-        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s_n) s_base = atomicAdd(a.work_count, s_n);
+        __syncthreads();
+        if (threadIdx.x < s_n) a.work[s_base + threadIdx.x] = s_list[threadIdx.x];
     }
 }
 
-// Phase 2: one thread per (touched word, pixel, 4-channel quad) -- flat, so
-// the few touched words of a sparse frame are spread over the whole GPU.
+// Phase 2: a block takes G touched words at a time (G = 256 / (32 * C/4),
+// at least 1) and sweeps their (pixel, 4-channel) items with all its threads.
 // Max-pool (first element seeds the max, then every window element,
-// baseline.cpp:134-138) or ReLU, compare-before-write for the next CBCONV:
-// the first thread to set a pixel's change bit counts it.
+// baseline.cpp:134-138) or ReLU; compare-before-write assembles the next
+// CBCONV's change word in shared memory.
 template <bool FULL>
 __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a) {
+    __shared__ uint32_t s_changed[kPtThreads / 32];
     const int Ho = a.out.H, Wo = a.out.W;
     const int wpr = (Wo + 31) / 32;
     const int c4n = a.in.Cp / 4;
     const int per_word = 32 * c4n;
+    const int G = max(1, min(kPtThreads / 32, kPtThreads / per_word));
     const int64_t nwords = FULL ? (int64_t)a.S * Ho * wpr : (int64_t)*a.work_count;
-    const int64_t total = nwords * per_word;
     const int rowq = a.in.Wp * c4n;
-    for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t e = f / per_word;
-        const int item = (int)(f - e * per_word);
-        const int j = item / c4n, c4 = item - j * c4n;
-        uint32_t seg, tw;
-        if (FULL) {
-            seg = (uint32_t)e;
-            tw = 0xffffffffu;
-        } else {
-            const uint2 wk = a.work[e];
-            seg = wk.x;
-            tw = wk.y;
+    for (int64_t g0 = (int64_t)blockIdx.x * G; g0 < nwords; g0 += (int64_t)gridDim.x * G) {
+        if (threadIdx.x < G) s_changed[threadIdx.x] = 0;
+        __syncthreads();
+        const int items = G * per_word;
+        for (int it = threadIdx.x; it < items; it += kPtThreads) {
+            const int gi = it / per_word, item = it - gi * per_word;
+            const int64_t e = g0 + gi;
+            if (e >= nwords) continue;
+            const int j = item / c4n, c4 = item - j * c4n;
+            uint32_t seg, tw;
+            if (FULL) {
+                seg = (uint32_t)e;
+                tw = 0xffffffffu;
+            } else {
+                const uint2 wk = a.work[e];
+                seg = wk.x;
+                tw = wk.y;
+            }
+            if (!((tw >> j) & 1u)) continue;
+            const int s = (int)(seg / ((uint32_t)Ho * wpr));
+            const uint32_t r = seg - (uint32_t)s * Ho * wpr;
+            const int y = (int)(r / wpr), w = (int)(r - (r / wpr) * wpr);
+            const int x = 32 * w + j;
+            if (x >= Wo) continue;
+            const float4* src = reinterpret_cast<const float4*>(
+                a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
+            float4* dst = reinterpret_cast<float4*>(
+                a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp) + c4;
+            float4 m = *src;
+            if (a.relu) {
+                m = make_float4(ref_relu(m.x), ref_relu(m.y), ref_relu(m.z), ref_relu(m.w));
+            } else {
+                for (int kj = 0; kj < a.window; ++kj)
+                    for (int ki = 0; ki < a.window; ++ki) {
+                        const float4 v = src[kj * rowq + ki * c4n];
+                        m = make_float4(ref_max(m.x, v.x), ref_max(m.y, v.y), ref_max(m.z, v.z), ref_max(m.w, v.w));
+                    }
+            }
+            if (!FULL && a.chg.d) {
+                const float4 o = *dst;
+                if (ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
+                    ref_changed(m.w, o.w, a.tau))
+                    atomicOr(&s_changed[gi], 1u << j);
+            }
+            *dst = m;
         }
-        if (!((tw >> j) & 1u)) continue;
-        const int s = (int)(seg / ((uint32_t)Ho * wpr));
-        const uint32_t r = seg - (uint32_t)s * Ho * wpr;
-        const int y = (int)(r / wpr), w = (int)(r - (r / wpr) * wpr);
-        const int x = 32 * w + j;
-        if (x >= Wo) continue;
-        const float4* src = reinterpret_cast<const float4*>(
-            a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
-        float4* dst = reinterpret_cast<float4*>(
-            a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp) + c4;
-        float4 m = *src;
-        if (a.relu) {
-            m = make_float4(ref_relu(m.x), ref_relu(m.y), ref_relu(m.z), ref_relu(m.w));
-        } else {
-            for (int kj = 0; kj < a.window; ++kj)
-                for (int ki = 0; ki < a.window; ++ki) {
-                    const float4 v = src[kj * rowq + ki * c4n];
-                    m = make_float4(ref_max(m.x, v.x), ref_max(m.y, v.y), ref_max(m.z, v.z), ref_max(m.w, v.w));
-                }
-        }
-        if (!FULL && a.chg.d) {
-            const float4 o = *dst;
-            if (ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
-                ref_changed(m.w, o.w, a.tau)) {
-                const uint32_t bit = 1u << j;
-                const uint32_t old = atomicOr(a.chg.d + (int64_t)s * a.chg.stride + (int64_t)y * wpr + w, bit);
-                if (!(old & bit) && a.chg_cnt) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, 1ull);
+        __syncthreads();
+        if (!FULL && a.chg.d && threadIdx.x < G && g0 + threadIdx.x < nwords) {
+            const uint32_t cw = s_changed[threadIdx.x];
+            if (cw) {
+                const uint32_t seg = a.work[g0 + threadIdx.x].x;
+                const int s = (int)(seg / ((uint32_t)Ho * wpr));
+                const uint32_t r = seg - (uint32_t)s * Ho * wpr;
+                a.chg.d[(int64_t)s * a.chg.stride + r] = cw;
+                if (a.chg_cnt) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, (unsigned long long)__popc(cw));
             }
         }
-        *dst = m;
+        __syncthreads();
     }
 }
 
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
     const int wpr = (a.out.W + 31) / 32;
     const int64_t nseg = (int64_t)a.S * a.out.H * wpr;
-    const int c4n = a.in.Cp / 4;
+    const int per_word = 32 * (a.in.Cp / 4);
+    const int G = std::max(1, std::min(kPtThreads / 32, kPtThreads / per_word));
     if (!a.upd_in.d) {  // full frame: every word, no change test (the next layer evaluates in full)
-        const int64_t total = nseg * 32 * c4n;
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + kPtThreads - 1) / kPtThreads, (int64_t)kNumSMs * 16));
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nseg + G - 1) / G, (int64_t)kNumSMs * 16));
         point_work_kernel<true><<<grid, kPtThreads, 0, st>>>(a);
         return;
     }
@@ -530,8 +557,6 @@ void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
     const int64_t blocks = (nseg + kPtThreads / 32 - 1) / (kPtThreads / 32);
     const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)kNumSMs * 8));
     point_scan_kernel<<<g1, kPtThreads, 0, st>>>(a);
-    // the touched-word count is only known on the device: grid-stride over a
-    // fixed grid sized for the GPU
     point_work_kernel<false><<<kNumSMs * 8, kPtThreads, 0, st>>>(a);
 }
 
