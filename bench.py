@@ -267,6 +267,7 @@ def run_gpu_arm(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     import paper_1704_04313_b200 as cbx
+    from paper_1704_04313_b200 import shard
     log = (lambda *a: print(*a, file=sys.stderr)) if rank == 0 else (lambda *a: None)
 
     S, F = args.streams, args.frames
@@ -276,18 +277,18 @@ def run_gpu_arm(args):
     net = cbx.Network(spec, weights, device=local, streams=S, precision=args.precision)
     dims = net.shapes
     stream = torch.cuda.ExternalStream(net.stream_handle(), device=torch.device("cuda", local))
-    # resident clips: distinct seed per (rank, stream), generated on device
+    # resident clips: this rank's shard of the global stream set (stream g on
+    # rank g % world, distinct seed per stream), generated on device
+    gstreams = shard.streams_for_rank(S, rank, ws)
     clip = torch.empty((F, S, 3, args.height, args.width), dtype=torch.float32, device=f"cuda:{local}")
-    for s in range(S):
-        cfg = clip_cfg(args, 1000 * rank + s + 1)
+    for s, g in enumerate(gstreams):
+        cfg = clip_cfg(args, shard.stream_seed(g))
         for f in range(F):
             cbx.synth_frame_device(cfg, f, clip[f, s].data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     ptrs = lambda i: [clip[pingpong(i, F), s].data_ptr() for s in range(S)]
 
-    def barrier():
-        if ws > 1:
-            torch.distributed.barrier()
+    barrier = shard.barrier
 
     def timed(engine, i0, K):
         barrier()
@@ -299,12 +300,7 @@ def run_gpu_arm(args):
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ms = e0.elapsed_time(e1)
-        if ws > 1:
-            t = torch.tensor([ms], device=f"cuda:{local}")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+        return shard.max_over_ranks(e0.elapsed_time(e1), device=f"cuda:{local}")
 
     clocks = Clocks(local)
     clocks.start()
@@ -329,7 +325,7 @@ def run_gpu_arm(args):
         net.sync()
     clk = clocks.stop()
     clk["note"] = "sampled every 100 ms across warm-up, the timed region and a 0.5 s continuation of the same step"
-    value = ws * S * K / (ms / 1000.0)
+    value = shard.aggregate_rate(ws, S * K, ms)
     log(f"[gpu] cbinfer: {ms / K:.3f} ms/step, {value:.1f} frames/s, {launches} kernels/frame")
 
     # changed fractions of exactly the timed frames: replay the clip from reset
@@ -393,7 +389,7 @@ def run_gpu_arm(args):
     Kd = max(3, K // 4)
     net.forward_device(ptrs(0), "baseline")
     ms_d = timed("baseline", 1, Kd)
-    dense_fps = ws * S * Kd / (ms_d / 1000.0)
+    dense_fps = shard.aggregate_rate(ws, S * Kd, ms_d)
     log(f"[gpu] dense: {ms_d / Kd:.3f} ms/step, {dense_fps:.1f} frames/s")
 
     sweep = None
@@ -403,8 +399,8 @@ def run_gpu_arm(args):
             a2 = argparse.Namespace(**vars(args))
             a2.recipe = r
             c2 = torch.empty_like(clip)
-            for s in range(S):
-                cfg = clip_cfg(a2, 1000 * rank + s + 1)
+            for s, g in enumerate(gstreams):
+                cfg = clip_cfg(a2, shard.stream_seed(g))
                 for f in range(F):
                     cbx.synth_frame_device(cfg, f, c2[f, s].data_ptr(), torch.cuda.current_stream().cuda_stream)
             torch.cuda.synchronize()
@@ -422,10 +418,10 @@ def run_gpu_arm(args):
                 net.forward_device(p2(i))
             e1.record(stream)
             torch.cuda.synchronize()
-            m2 = e0.elapsed_time(e1)
-            sweep[r] = {"fps": round(ws * S * K / (m2 / 1000.0), 1),
+            m2 = shard.max_over_ranks(e0.elapsed_time(e1), device=f"cuda:{local}")
+            sweep[r] = {"fps": round(shard.aggregate_rate(ws, S * K, m2), 1),
                         "l1_input_changed": float(np.mean([s[cb[0]]["changedInputPixels"] for s in stt])) / (args.height * args.width),
-                        "speedup_vs_dense": round(ws * S * K / (m2 / 1000.0) / dense_fps, 2)}
+                        "speedup_vs_dense": round(shard.aggregate_rate(ws, S * K, m2) / dense_fps, 2)}
             del c2
 
     # e2e: public C-ABI with HOST frames (pinned), H2D + compute + labels D2H every step
@@ -444,13 +440,9 @@ def run_gpu_arm(args):
         t = time.perf_counter()
         for i in range(4, 4 + K):
             net.forward(hostnp[pingpong(i, Fe)])
-        wall = time.perf_counter() - t
-        if ws > 1:
-            tt = torch.tensor([wall], device=f"cuda:{local}")
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            wall = float(tt.item())
+        wall = shard.max_over_ranks(time.perf_counter() - t, device=f"cuda:{local}")
         lh, lw = net.label_hw
-        e2e = {"value": ws * S * K / wall, "unit": "frames/s",
+        e2e = {"value": shard.aggregate_rate(ws, S * K, 1000.0 * wall), "unit": "frames/s",
                "h2d_bytes_per_step": S * 3 * args.height * args.width * 4, "d2h_bytes_per_step": S * lh * lw * 2}
         log(f"[gpu] e2e: {1000 * wall / K:.3f} ms/step, {e2e['value']:.1f} frames/s")
 
