@@ -121,7 +121,11 @@ CBX_API int cbx_get_thresholds(const cbx_ctx* ctx, float* taus, int n);
  * conv) inside that conv's epilogue; their intermediate tensors are then not
  * materialized (cbx_get_activation reports CBX_E_SPEC for them). 0 keeps every
  * layer's output, e.g. for per-layer parity checks. Results are identical. */
-typedef enum { CBX_OPT_FUSE_TAIL = 0 } cbx_option;
+/* CBX_OPT_TC_PAIR (default -1 = auto = single-CTA tiles): CTA grouping of the
+ * tcgen05 convs. 1 pairs the two SMs of a TPC (cta_group::2, M = 256 tiles,
+ * each SM holds half the filter bank); 0 forces one CTA per tile. Same tf32
+ * error bound either way. */
+typedef enum { CBX_OPT_FUSE_TAIL = 0, CBX_OPT_TC_PAIR = 1 } cbx_option;
 CBX_API int cbx_set_option(cbx_ctx* ctx, int option, int value);
 
 /* Drops all change-based state of every stream: the next frame is a full

@@ -340,6 +340,11 @@ class Network:
         tcgen05 conv's epilogue (default) or materialize every layer."""
         self._chk(lib.cbx_set_option(self._h, 0, int(bool(on))))
 
+    def set_tc_pair(self, mode: int) -> None:
+        """CBX_OPT_TC_PAIR: -1 auto (single-CTA tiles), 0 single-CTA tiles,
+        1 CTA pairs (cta_group::2) everywhere."""
+        self._chk(lib.cbx_set_option(self._h, 1, int(mode)))
+
     # -- forward
     def forward(self, frames: np.ndarray, engine: str = "cbinfer") -> List[ForwardResult]:
         """frames: [S, C, H, W] float32 host array (or [C,H,W] when S == 1)."""

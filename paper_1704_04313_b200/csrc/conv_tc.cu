@@ -28,6 +28,7 @@
 //   a time, + bias, fused ReLU, compare with the value being overwritten
 //   (next CBCONV's change detection, cbconv.cpp:66-67), in-place scatter into
 //   the persistent output tensor (update_output without the full copy).
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -93,8 +94,8 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
     return (uint64_t)((addr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
 }
 // Instruction descriptor: D=f32, A=B=tf32, both K-major, M=128, N.
-__host__ __device__ constexpr uint32_t idesc_tf32(int N) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc_tf32(int N, int M = kTileM) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -103,6 +104,59 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// ---- CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same smem object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// arrive (when the issued MMAs complete) on the barrier at this smem offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -178,9 +232,11 @@ struct TcArgs {
     const int32_t* idx;
     const int* count;
     int64_t full_count;
-    const float* Bw;     // [NKB][Npad][32] swizzled smem images
+    const float* Bw;     // [ranks][NKB][Brows][32] swizzled smem images
     const float* bias;   // [O]
     int NKB, Npad, N0, N1;
+    int Brows;           // filter rows held per CTA (Npad, or Npad/2 for a CTA pair)
+    int dbg;             // EXPERIMENT bits: 1 skip A gather, 2 skip N1 MMA, 4 skip B copy, 8 no proxy fence, 16 no epilogue math, 32 no tc fence, 64 MMAs back to back (no stage handshake)
     int stages, acc_stages, acc_cols, tmem_cols;
     int relu;
     BitMask chg;
@@ -192,16 +248,91 @@ struct TcArgs {
     TcTail tail;
 };
 
+// Epilogue of one 32-column TMEM chunk for one pixel: + bias, fused ReLU,
+// the first tail 1x1 conv accumulated in ascending channel order, and (when
+// the layer output is kept) compare-before-write against the stored value.
+// FULL: all 32 channels exist, so every loop is branch-free and the shared
+// memory loads of bias / tail filters can be hoisted ahead of their use.
+template <int TC, bool FULL>
+__device__ __forceinline__ void epi_chunk(const TcArgs& a, float (&v)[32], int c0, int nv, const float* sBias,
+                                          const float* sTailW, float (&t1)[TC > 0 ? TC : 1], float* dst,
+                                          bool& changed) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+        if (!FULL && j >= nv) break;
+        const float4 b4 = *reinterpret_cast<const float4*>(sBias + c0 + j);
+        const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float t = (FULL || j + e < nv) ? __fadd_rn(v[j + e], bb[e]) : 0.0f;
+            v[j + e] = a.relu ? ref_relu(t) : t;
+        }
+    }
+    if constexpr (TC > 0) {
+        // the TC filters of one channel are TC/4 broadcast LDS.128
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (!FULL && j >= nv) break;
+            const float4* w = reinterpret_cast<const float4*>(sTailW + (c0 + j) * TC);
+#pragma unroll
+            for (int q4 = 0; q4 < TC / 4; ++q4) {
+                const float4 wq = w[q4];
+                t1[4 * q4 + 0] = __fadd_rn(t1[4 * q4 + 0], __fmul_rn(wq.x, v[j]));
+                t1[4 * q4 + 1] = __fadd_rn(t1[4 * q4 + 1], __fmul_rn(wq.y, v[j]));
+                t1[4 * q4 + 2] = __fadd_rn(t1[4 * q4 + 2], __fmul_rn(wq.z, v[j]));
+                t1[4 * q4 + 3] = __fadd_rn(t1[4 * q4 + 3], __fmul_rn(wq.w, v[j]));
+            }
+        }
+    }
+    if (!a.write_out) return;
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+        if (!FULL && j >= nv) break;
+        const int o = c0 + j;
+        if (FULL || j + 3 < nv) {
+            float4* q = reinterpret_cast<float4*>(dst + o);
+            if (a.chg.d) {
+                const float4 old = *q;
+                changed |= ref_changed(v[j], old.x, a.tau) | ref_changed(v[j + 1], old.y, a.tau) |
+                           ref_changed(v[j + 2], old.z, a.tau) | ref_changed(v[j + 3], old.w, a.tau);
+            }
+            *q = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (j + e < nv) {
+                    if (a.chg.d) changed |= ref_changed(v[j + e], dst[o + e], a.tau);
+                    dst[o + e] = v[j + e];
+                }
+            }
+        }
+    }
+}
+
 // ROWLANE: producer thread = tile row (each lane gathers its own pixel; best
 // when a pixel's taps are 16 B, i.e. 4 channels, so a warp's 32 rows of one
 // tap are 32 neighbouring pixels). Otherwise 8 lanes cooperate on a row's 128
 // contiguous K-block bytes and a warp instruction covers 4 rows.
-template <bool ROWLANE, int TC>
-__global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
+//
+// PAIR: the CTA pair of a 2-CTA cluster (the two SMs of one TPC) runs one
+// M=256 tcgen05.mma.cta_group::2: each CTA gathers its own 128 pixel rows (A)
+// and holds HALF of the filter bank (B: N/2 rows per instruction), so every
+// SM streams 16 KB of A + Npad*64 B of B per K-block instead of
+// 16 KB + Npad*128 B -- the filter bytes, which dominate wide layers
+// (Npad = 304: 39 KB vs 16 KB of A), are halved in L2 traffic and in shared
+// memory. The leader (cluster rank 0) issues the MMAs; the peer's stage-full
+// state reaches it through a relay thread (cp.async completions can only
+// arrive on a CTA-local mbarrier), and the leader's commits are multicast to
+// both CTAs' empty / accumulator-full barriers. Each CTA's TMEM holds the
+// accumulator rows of its own 128 pixels, so the epilogue is unchanged.
+template <bool ROWLANE, int TC, bool PAIR>
+__global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align by offsetting the shared array itself (not via an integer round
+    // trip), so the compiler keeps emitting LDS/STS for the smem tables below
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int NS = a.stages;
-    const uint32_t b_bytes = (uint32_t)a.Npad * 128u;
+    const uint32_t b_bytes = (uint32_t)a.Brows * 128u;
     uint8_t* sA = smem;                                  // NS x 16 KB
     uint8_t* sB = sA + (size_t)NS * kABytes;             // NS x b_bytes
     int* sTab = reinterpret_cast<int*>(sB + (size_t)NS * b_bytes);   // NKB*8 chunk offsets (floats)
@@ -211,7 +342,8 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
         (reinterpret_cast<uintptr_t>(sTailW + a.tail_w_floats) + 7) & ~uintptr_t(7));
     uint64_t* full = bars;
     uint64_t* empty = full + NS;
-    uint64_t* tfull = empty + NS;
+    uint64_t* pfull = empty + NS;  // PAIR, leader only: the peer's stage is full
+    uint64_t* tfull = pfull + NS;
     uint64_t* tempty = tfull + 2;
     uint32_t* sTmem = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -219,6 +351,12 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
     const int warp = tid >> 5, lane = tid & 31;
     const int C4 = a.in_Cp >> 2;
     const int nchunks = a.kh * a.kw * C4;
+    const uint32_t crank = PAIR ? cluster_rank() : 0u;
+    const int64_t tile_first = PAIR ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
+    const int64_t tile_step = PAIR ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
+    constexpr int kRowsPerTile = PAIR ? 2 * kTileM : kTileM;
+    const int64_t row_off = (int64_t)crank * kTileM;  // this CTA's rows within a tile
+    const float* Bw = a.Bw + (size_t)crank * a.NKB * a.Brows * kKBlock;
 
     // ---- setup
     for (int j = tid; j < a.NKB * kChunksPerKB; j += kThreads) {
@@ -242,25 +380,32 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], kProdThreads + 1);
             mbar_init(&empty[s], 1);
+            mbar_init(&pfull[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], kEpiThreads);
+            mbar_init(&tempty[s], PAIR ? 2 * (kEpiThreads / 32) : kEpiThreads);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 8) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sTmem)),
-                     "r"(a.tmem_cols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sTmem)),
+                         "r"(a.tmem_cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sTmem)),
+                         "r"(a.tmem_cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *sTmem;
 
     const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
-    const int64_t ntiles = (total + kTileM - 1) / kTileM;
+    const int64_t ntiles = (total + kRowsPerTile - 1) / kRowsPerTile;
     const int64_t HoWo = (int64_t)a.Ho * a.Wo;
 
     if (warp >= 4 && warp < 8) {
@@ -269,8 +414,8 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
             const int r = tid - kEpiThreads;
             const uint32_t swz = (uint32_t)(r & 7);
             uint32_t it = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const int64_t n = tile * kTileM + r;
+            for (int64_t tile = tile_first; tile < ntiles; tile += tile_step) {
+                const int64_t n = tile * kRowsPerTile + row_off + r;
                 const bool valid = n < total;
                 const float* base = a.in;
                 if (valid) {
@@ -282,11 +427,12 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
                            ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
                 }
                 for (int kb = 0; kb < a.NKB; ++kb, ++it) {
+                    if (a.dbg & 64) break;
                     const uint32_t st = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[st], ph ^ 1u);
                     if (r == 0) {
                         mbar_arrive_expect_tx(&full[st], b_bytes);
-                        bulk_g2s(sB + (size_t)st * b_bytes, a.Bw + (size_t)kb * a.Npad * kKBlock, b_bytes, &full[st]);
+                        bulk_g2s(sB + (size_t)st * b_bytes, Bw + (size_t)kb * a.Brows * kKBlock, b_bytes, &full[st]);
                     }
                     const uint32_t row = smem_u32(sA + (size_t)st * kABytes + r * 128);
                     if (valid) {
@@ -308,12 +454,12 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
         const uint32_t swz_off = (uint32_t)((j ^ (rsub & 7)) << 4);
         constexpr int kRowsPerThread = kTileM / 16;
         uint32_t it = 0;
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int64_t tile = tile_first; tile < ntiles; tile += tile_step) {
             const float* base[kRowsPerThread];
             uint32_t vmask = 0;
 #pragma unroll
             for (int i = 0; i < kRowsPerThread; ++i) {
-                const int64_t n = tile * kTileM + rsub + 16 * i;
+                const int64_t n = tile * kRowsPerTile + row_off + rsub + 16 * i;
                 base[i] = a.in;
                 if (n < total) {
                     vmask |= 1u << i;
@@ -326,49 +472,75 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
                 }
             }
             for (int kb = 0; kb < a.NKB; ++kb, ++it) {
+                if (a.dbg & 64) break;
                 const uint32_t st = it % NS, ph = (it / NS) & 1u;
                 mbar_wait(&empty[st], ph ^ 1u);
                 if (pt == 0) {
-                    mbar_arrive_expect_tx(&full[st], b_bytes);
-                    bulk_g2s(sB + (size_t)st * b_bytes, a.Bw + (size_t)kb * a.Npad * kKBlock, b_bytes, &full[st]);
+                    if (a.dbg & 4) {
+                        mbar_arrive(&full[st]);
+                    } else {
+                        mbar_arrive_expect_tx(&full[st], b_bytes);
+                        bulk_g2s(sB + (size_t)st * b_bytes, Bw + (size_t)kb * a.Brows * kKBlock, b_bytes, &full[st]);
+                    }
                 }
                 const int off = sTab[kb * kChunksPerKB + j];
                 const uint32_t stage = smem_u32(sA + (size_t)st * kABytes) + swz_off;
 #pragma unroll
                 for (int i = 0; i < kRowsPerThread; ++i)
-                    if ((vmask >> i) & 1u)
+                    if (((vmask >> i) & 1u) && !(a.dbg & 1))
                         cp_async16(stage + (rsub + 16 * i) * 128, off >= 0 ? base[i] + off : a.in, off >= 0 ? 16u : 0u);
                 cp_async_arrive_noinc(&full[st]);
             }
         }
         }
     } else if (warp == 8) {
-        // ================= MMA issuer =================
-        if (lane == 0) {
-            const uint32_t id0 = idesc_tf32(a.N0), id1 = idesc_tf32(a.N1 > 0 ? a.N1 : 16);
+        if (PAIR && crank != 0) {
+            // ================= peer: relay "stage full" to the leader =================
+            if (lane == 0) {
+                uint32_t it = 0;
+                for (int64_t tile = tile_first; tile < ntiles; tile += tile_step)
+                    for (int kb = 0; kb < a.NKB; ++kb, ++it) {
+                        const uint32_t st = it % NS, ph = (it / NS) & 1u;
+                        mbar_wait(&full[st], ph);
+                        fence_proxy_async();
+                        mbar_arrive_cluster(mapa(&pfull[st], 0));
+                    }
+            }
+        } else if (lane == 0) {
+            // ================= MMA issuer =================
+            const int M = PAIR ? 2 * kTileM : kTileM;
+            const uint32_t id0 = idesc_tf32(a.N0, M), id1 = idesc_tf32(a.N1 > 0 ? a.N1 : 16, M);
+            // B rows of the second instruction start after this CTA's share of the first
+            const uint32_t b1_off = (uint32_t)(PAIR ? a.N0 / 2 : a.N0) * 128u;
             uint32_t it = 0, acc_it = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++acc_it) {
+            for (int64_t tile = tile_first; tile < ntiles; tile += tile_step, ++acc_it) {
                 const uint32_t as = acc_it % a.acc_stages, aph = (acc_it / a.acc_stages) & 1u;
-                mbar_wait(&tempty[as], aph ^ 1u);
+                if constexpr (PAIR) mbar_wait_cluster(&tempty[as], aph ^ 1u); else mbar_wait(&tempty[as], aph ^ 1u);
                 tc_fence_after();
                 const uint32_t d = tmem_base + as * a.acc_cols;
                 for (int kb = 0; kb < a.NKB; ++kb, ++it) {
                     const uint32_t st = it % NS, ph = (it / NS) & 1u;
-                    mbar_wait(&full[st], ph);
-                    fence_proxy_async();
-                    tc_fence_after();
+                    if (!(a.dbg & 64)) mbar_wait(&full[st], ph);
+                    if constexpr (PAIR) mbar_wait_cluster(&pfull[st], ph);
+                    if (!(a.dbg & 8)) fence_proxy_async();
+                    if (!(a.dbg & 32)) tc_fence_after();
                     const uint32_t aaddr = smem_u32(sA + (size_t)st * kABytes);
                     const uint32_t baddr = smem_u32(sB + (size_t)st * b_bytes);
 #pragma unroll
                     for (int k = 0; k < kKBlock / 8; ++k) {
                         const uint64_t ad = smem_desc(aaddr + k * 32);
                         const uint32_t accum = (kb | k) ? 1u : 0u;
-                        mma_tf32(d, ad, smem_desc(baddr + k * 32), id0, accum);
-                        if (a.N1 > 0) mma_tf32(d + a.N0, ad, smem_desc(baddr + a.N0 * 128 + k * 32), id1, accum);
+                        if constexpr (PAIR) {
+                            mma_tf32_pair(d, ad, smem_desc(baddr + k * 32), id0, accum);
+                            if (a.N1 > 0) mma_tf32_pair(d + a.N0, ad, smem_desc(baddr + b1_off + k * 32), id1, accum);
+                        } else {
+                            mma_tf32(d, ad, smem_desc(baddr + k * 32), id0, accum);
+                            if (a.N1 > 0 && !(a.dbg & 2)) mma_tf32(d + a.N0, ad, smem_desc(baddr + b1_off + k * 32), id1, accum);
+                        }
                     }
-                    mma_commit(&empty[st]);
+                    if constexpr (PAIR) mma_commit_pair(&empty[st]); else if (!(a.dbg & 64)) mma_commit(&empty[st]);
                 }
-                mma_commit(&tfull[as]);
+                if constexpr (PAIR) mma_commit_pair(&tfull[as]); else mma_commit(&tfull[as]);
             }
         }
         __syncwarp();
@@ -376,11 +548,11 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
         // ================= epilogue: thread = TMEM lane = tile row =================
         const int r = tid;
         uint32_t acc_it = 0;
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++acc_it) {
+        for (int64_t tile = tile_first; tile < ntiles; tile += tile_step, ++acc_it) {
             const uint32_t as = acc_it % a.acc_stages, aph = (acc_it / a.acc_stages) & 1u;
             mbar_wait(&tfull[as], aph);
             tc_fence_after();
-            const int64_t n = tile * kTileM + r;
+            const int64_t n = tile * kRowsPerTile + row_off + r;
             const bool valid = n < total;
             int s = 0, p = 0, y = 0, x = 0;
             float* dst = nullptr;
@@ -403,53 +575,19 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
             for (int c0 = 0; c0 < a.O; c0 += 32) {
                 float v[32];
                 tmem_ld32(trow + c0, v);
-                if (valid) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        const int o = c0 + j;
-                        if (o >= a.O) break;
-                        float w4[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float t = (o + e < a.O) ? __fadd_rn(v[j + e], sBias[o + e]) : 0.0f;
-                            w4[e] = a.relu ? ref_relu(t) : t;
-                        }
-                        if constexpr (TC > 0) {
-                            // ascending channels; the TC filters of one channel are TC/4 broadcast LDS.128
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                if (o + e >= a.O) break;
-                                const float4* w = reinterpret_cast<const float4*>(sTailW + (o + e) * TC);
-#pragma unroll
-                                for (int q4 = 0; q4 < TC / 4; ++q4) {
-                                    const float4 wq = w[q4];
-                                    t1[4 * q4 + 0] = __fadd_rn(t1[4 * q4 + 0], __fmul_rn(wq.x, w4[e]));
-                                    t1[4 * q4 + 1] = __fadd_rn(t1[4 * q4 + 1], __fmul_rn(wq.y, w4[e]));
-                                    t1[4 * q4 + 2] = __fadd_rn(t1[4 * q4 + 2], __fmul_rn(wq.z, w4[e]));
-                                    t1[4 * q4 + 3] = __fadd_rn(t1[4 * q4 + 3], __fmul_rn(wq.w, w4[e]));
-                                }
-                            }
-                        }
-                        if (!a.write_out) continue;
-                        if (o + 3 < a.O) {
-                            float4* q = reinterpret_cast<float4*>(dst + o);
-                            if (a.chg.d) {
-                                const float4 old = *q;
-                                changed |= ref_changed(w4[0], old.x, a.tau) | ref_changed(w4[1], old.y, a.tau) |
-                                           ref_changed(w4[2], old.z, a.tau) | ref_changed(w4[3], old.w, a.tau);
-                            }
-                            *q = make_float4(w4[0], w4[1], w4[2], w4[3]);
-                        } else {
-                            for (int e = 0; e < 4 && o + e < a.O; ++e) {
-                                if (a.chg.d) changed |= ref_changed(w4[e], dst[o + e], a.tau);
-                                dst[o + e] = w4[e];
-                            }
-                        }
-                    }
-                }
+                if (!valid || (a.dbg & 16)) continue;
+                if (c0 + 32 <= a.O)
+                    epi_chunk<TC, true>(a, v, c0, 32, sBias, sTailW, t1, dst, changed);
+                else
+                    epi_chunk<TC, false>(a, v, c0, a.O - c0, sBias, sTailW, t1, dst, changed);
             }
             tc_fence_before();
-            mbar_arrive(&tempty[as]);
+            if constexpr (PAIR) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(mapa(&tempty[as], 0));
+            } else {
+                mbar_arrive(&tempty[as]);
+            }
             if constexpr (TC > 0) {
                 if (valid) run_tail<TC>(a.tail, t1, s, y, x, p);
             }
@@ -460,10 +598,15 @@ __global__ void __launch_bounds__(kThreads, 2) conv_tc_kernel(TcArgs a) {
         }
     }
     tc_fence_before();
-    __syncthreads();
+    // PAIR: no CTA may leave (or free its TMEM) while the other still signals
+    // its barriers or the leader's MMAs still target its TMEM
+    if constexpr (PAIR) cluster_sync_all(); else __syncthreads();
     if (warp == 8) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols));
+        if constexpr (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols));
     }
 }
 
@@ -485,6 +628,9 @@ struct TcLayer {
     int stages = 0, acc_stages = 1, acc_cols = 0, tmem_cols = 32;
     int tail_w_floats = 0;
     int ctas_per_sm = 1;
+    bool pair = false;   // CTA pair (cta_group::2, M = 256)
+    int Brows = 0;       // filter rows per CTA
+    int max_clusters = 0;
     size_t smem = 0;
     float* Bw = nullptr;
 };
@@ -499,7 +645,19 @@ bool tc_supported(const cbx_geom& g) {
     return g.outChannels >= 1 && Npad <= 512 && g.kernelH * g.kernelW * round_up(g.inChannels, 4) <= 65536;
 }
 
-std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats) {
+namespace {
+template <bool R, int T, bool P>
+void set_smem_attr() {
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<R, T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+}
+template <int T, bool P>
+void set_smem_attrs() {
+    set_smem_attr<true, T, P>();
+    set_smem_attr<false, T, P>();
+}
+}  // namespace
+
+std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats, int pair_mode) {
     std::unique_ptr<TcLayer, TcLayerDeleter> t(new TcLayer);
     t->g = g;
     t->Cp = (int)round_up(g.inChannels, 4);
@@ -513,41 +671,86 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     int cols = 32;
     while (cols < t->acc_stages * t->acc_cols) cols *= 2;
     t->tmem_cols = cols;
-    const size_t b_bytes = (size_t)t->Npad * 128;
+    // CTA pairs (M = 256, each SM streams half the filter bank) are opt-in:
+    // measured on B200 they lose to single-CTA tiles for the paper's L3
+    // (1.54 vs 1.42 ms dense 4x1080p): the shallower per-SM shared memory
+    // leaves the gather's tap reuse less L1 (hit rate 45% vs 85%), and the
+    // pair handshake adds a relay per K-block. Narrow layers run two
+    // independent CTAs per SM so that one CTA's gather latency overlaps the
+    // other's MMAs/epilogue.
+    t->pair = pair_mode > 0;
+    t->Brows = t->pair ? t->Npad / 2 : t->Npad;
+    t->ctas_per_sm = (!t->pair && t->Npad <= 128) ? 2 : 1;
+    const size_t b_bytes = (size_t)t->Brows * 128;
     t->tail_w_floats = (int)round_up(tail_floats, 4);
     const size_t fixed = 1024 + (size_t)t->NKB * kChunksPerKB * 4 + round_up(g.outChannels, 4) * 4 +
-                         (size_t)t->tail_w_floats * 4 + 16 + 8 * (2 * 16 + 4) + 16;
-    // narrow layers (N <= 128) run two CTAs per SM so that one CTA's gather
-    // latency overlaps the other's MMAs/epilogue; wide ones take the whole SM
-    t->ctas_per_sm = t->Npad <= 128 ? 2 : 1;
+                         (size_t)t->tail_w_floats * 4 + 16 + 8 * (3 * 16 + 4) + 16;
     const size_t budget = t->ctas_per_sm == 2 ? (size_t)kMaxSmem / 2 - 1024 : (size_t)kMaxSmem;
-    int ns = 8;
+    // stage count: deep enough to cover the gather latency, shallow enough to
+    // leave L1 for the gather's tap reuse (neighbouring output pixels share
+    // input pixels across taps; the L1 hit rate collapses when shared memory
+    // takes the whole carve-out). CBX_TC_STAGES overrides (tuning).
+    int ns = t->pair ? 4 : 8;
+    if (const char* e = std::getenv("CBX_TC_STAGES")) ns = std::max(2, std::min(16, std::atoi(e)));
     while (ns > 2 && fixed + (size_t)ns * (kABytes + b_bytes) > budget) --ns;
     if (fixed + (size_t)ns * (kABytes + b_bytes) > budget)
         throw Error(CBX_E_ARG, "tcgen05 conv: layer too wide for shared memory");
     t->stages = ns;
     t->smem = fixed + (size_t)ns * (kABytes + b_bytes);
-    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CBX_CUDA(cudaMalloc(&t->Bw, (size_t)t->NKB * b_bytes));
-    CBX_CUDA(cudaMemset(t->Bw, 0, (size_t)t->NKB * b_bytes));
+    set_smem_attrs<0, false>();
+    set_smem_attrs<8, false>();
+    set_smem_attrs<16, false>();
+    set_smem_attrs<0, true>();
+    set_smem_attrs<8, true>();
+    set_smem_attrs<16, true>();
+    if (t->pair) {
+        // co-resident 2-CTA clusters at this shared-memory size
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(2 * kNumSMs);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = t->smem;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        CBX_CUDA(cudaOccupancyMaxActiveClusters(&n, conv_tc_kernel<false, 8, true>, &cfg));
+        t->max_clusters = std::max(1, std::min(n, kNumSMs / 2));
+    }
+    CBX_CUDA(cudaMalloc(&t->Bw, (size_t)t->NKB * b_bytes * (t->pair ? 2 : 1)));
+    CBX_CUDA(cudaMemset(t->Bw, 0, (size_t)t->NKB * b_bytes * (t->pair ? 2 : 1)));
     return t;
 }
 
 // Host-side re-layout of the reference filter matrix K[o][(c*kh + kj)*kw + ki]
 // into per-K-block swizzled smem images: element (n, kb*32 + j*4 + e) at
-// float offset kb*Npad*32 + n*32 + ((j ^ (n & 7)) * 4) + e, where chunk
+// float offset kb*Brows*32 + row*32 + ((j ^ (row & 7)) * 4) + e, where chunk
 // J = kb*8 + j covers tap J / C4 = (kj, ki) and channels 4*(J % C4) + e.
+// Single CTA: row = n. CTA pair: the two CTAs hold the two N-halves of every
+// MMA instruction (channels [0, N0/2) and [N0, N0 + N1/2) on rank 0, the rest
+// on rank 1), each in its own image.
 void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
     const cbx_geom& g = t.g;
     const int C4 = t.Cp / 4, khw = g.kernelH * g.kernelW;
     const int Kref = g.inChannels * khw;
-    std::vector<float> img((size_t)t.NKB * t.Npad * kKBlock, 0.0f);
-    for (int n = 0; n < g.outChannels; ++n)
+    const int ranks = t.pair ? 2 : 1;
+    std::vector<float> img((size_t)ranks * t.NKB * t.Brows * kKBlock, 0.0f);
+    for (int n = 0; n < g.outChannels; ++n) {
+        int rank = 0, row = n;
+        if (t.pair) {
+            if (n < t.N0) {
+                rank = n / (t.N0 / 2);
+                row = n % (t.N0 / 2);
+            } else {
+                const int m = n - t.N0;
+                rank = m / (t.N1 / 2);
+                row = t.N0 / 2 + m % (t.N1 / 2);
+            }
+        }
+        float* base = img.data() + (size_t)rank * t.NKB * t.Brows * kKBlock;
         for (int J = 0; J < t.NKB * kChunksPerKB; ++J) {
             const int tap = J / C4, c4 = J - tap * C4;
             if (tap >= khw) continue;
@@ -556,9 +759,10 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
                 const int c = c4 * 4 + e;
                 if (c >= g.inChannels) continue;
                 const float w = K[(size_t)n * Kref + (size_t)c * khw + tap];
-                img[(size_t)kb * t.Npad * kKBlock + (size_t)n * kKBlock + ((j ^ (n & 7)) * 4) + e] = round_tf32(w);
+                base[(size_t)kb * t.Brows * kKBlock + (size_t)row * kKBlock + ((j ^ (row & 7)) * 4) + e] = round_tf32(w);
             }
         }
+    }
     CBX_CUDA(cudaMemcpyAsync(t.Bw, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice, st));
     CBX_CUDA(cudaStreamSynchronize(st));
 }
@@ -599,6 +803,8 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.Npad = t.Npad;
     a.N0 = t.N0;
     a.N1 = t.N1;
+    a.Brows = t.Brows;
+    if (const char* e = std::getenv("CBX_TC_DBG")) a.dbg = std::atoi(e);
     a.stages = t.stages;
     a.acc_stages = t.acc_stages;
     a.acc_cols = t.acc_cols;
@@ -613,11 +819,37 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.cnt_stride = cstride;
     a.write_out = !(tail && tail->n && !tail->keep_out);
     if (tail) a.tail = *tail;
-    const int64_t max_tiles = (full_count + kTileM - 1) / kTileM;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, (int64_t)kNumSMs * t.ctas_per_sm));
     const int tc = (tail && tail->n) ? (tail->cout[0] <= 8 ? 8 : 16) : 0;
     const bool rowlane = in.Cp <= 4;
-#define CBX_TC_LAUNCH(R, T) conv_tc_kernel<R, T><<<grid, kThreads, t.smem, st>>>(a)
+    if (t.pair) {
+        const int64_t max_tiles = (full_count + 2 * kTileM - 1) / (2 * kTileM);
+        const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, t.max_clusters));
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(2 * clusters);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = t.smem;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+#define CBX_TC_LAUNCH(R, T) CBX_CUDA(cudaLaunchKernelEx(&cfg, conv_tc_kernel<R, T, true>, a))
+        if (tc == 0) {
+            if (rowlane) CBX_TC_LAUNCH(true, 0); else CBX_TC_LAUNCH(false, 0);
+        } else if (tc == 8) {
+            if (rowlane) CBX_TC_LAUNCH(true, 8); else CBX_TC_LAUNCH(false, 8);
+        } else {
+            if (rowlane) CBX_TC_LAUNCH(true, 16); else CBX_TC_LAUNCH(false, 16);
+        }
+#undef CBX_TC_LAUNCH
+        return;
+    }
+    const int64_t max_tiles = (full_count + kTileM - 1) / kTileM;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, (int64_t)kNumSMs * t.ctas_per_sm));
+#define CBX_TC_LAUNCH(R, T) conv_tc_kernel<R, T, false><<<grid, kThreads, t.smem, st>>>(a)
     if (tc == 0) {
         if (rowlane) CBX_TC_LAUNCH(true, 0); else CBX_TC_LAUNCH(false, 0);
     } else if (tc == 8) {

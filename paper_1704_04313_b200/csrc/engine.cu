@@ -886,8 +886,26 @@ int Engine::tail_end(int k) const {
 }
 
 void Engine::set_option(int option, int value) {
-    if (option != CBX_OPT_FUSE_TAIL) throw Error(CBX_E_ARG, "unknown option");
-    fuse_tail_ = value != 0;
+    if (option == CBX_OPT_TC_PAIR) {
+        if (value < -1 || value > 1) throw Error(CBX_E_ARG, "CBX_OPT_TC_PAIR takes -1, 0 or 1");
+        // rebuild every tcgen05 layer with the requested CTA grouping; the
+        // filters come back from the device copy in the reference layout
+        for (int k = 0; k < (int)layers_.size(); ++k) {
+            if (!tc_[k]) continue;
+            const cbx_geom& g = layers_[k].geom;
+            const int te = tail_end(k);
+            const int c1 = te > 0 ? layers_[k + 1].geom.outChannels : 0;
+            const int tail_floats = te > 0 ? (c1 <= 8 ? 8 : 16) * g.outChannels : 0;
+            std::vector<float> K((size_t)g.outChannels * g.inChannels * g.kernelH * g.kernelW);
+            CBX_CUDA(cudaMemcpy(K.data(), dK_[k], K.size() * sizeof(float), cudaMemcpyDeviceToHost));
+            tc_[k] = make_tc_layer(g, tail_floats, value);
+            tc_load_weights(*tc_[k], K.data(), stream_);
+        }
+    } else if (option == CBX_OPT_FUSE_TAIL) {
+        fuse_tail_ = value != 0;
+    } else {
+        throw Error(CBX_E_ARG, "unknown option");
+    }
     cb_->dirty = true;
     if (base_) base_->dirty = true;
 }

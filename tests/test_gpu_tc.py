@@ -28,12 +28,15 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("pair", [-1, 0, 1])
 @pytest.mark.parametrize("cin,h,w,layer", CASES)
-def test_tc_layer_vs_exact(gpu, orc, cin, h, w, layer):
+def test_tc_layer_vs_exact(gpu, orc, cin, h, w, layer, pair):
+    """pair: CBX_OPT_TC_PAIR (-1 auto = CTA pairs for N > 128, 0 single CTA, 1 pairs)."""
     spec = two_layer(cin, h, w, layer)
     wts = orc.generate_weights(spec, 11)
     onet = orc.load_network(spec, wts)
     net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="tf32")
+    net.set_tc_pair(pair)
     cfg = dict(channels=3, height=h, width=w, sprites=[(5, 2, 0.9)], noise=0.02, seed=5)
     for f in range(3):
         fr = orc.synth_frame(cfg, f)
