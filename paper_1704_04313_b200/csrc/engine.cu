@@ -149,7 +149,7 @@ struct Engine::Plan {
     int launches[2] = {0, 0};
     bool dirty = true;
     int fused_from = -1;            // conv layer whose epilogue runs the per-pixel tail (-1: none)
-    uint2* work = nullptr;          // touched-word list shared by the MAXPOOL/RELU layers
+    uint32_t* work = nullptr;       // touched-pixel list shared by the MAXPOOL/RELU layers
     int* work_count = nullptr;
 
     ~Plan() {
@@ -388,9 +388,10 @@ void Engine::build_plan(Plan& p, bool baseline) {
     int64_t wk = 0;
     for (int k = 0; k < nl; ++k)
         if (layers_[k].kind == CBX_MAXPOOL || layers_[k].kind == CBX_RELU)
-            wk = std::max<int64_t>(wk, (int64_t)S * dims_[6 * k + 4] * ((dims_[6 * k + 5] + 31) / 32));
+            wk = std::max<int64_t>(wk, (int64_t)S * dims_[6 * k + 4] * dims_[6 * k + 5]);
     if (wk) {
-        p.work = p.alloc<uint2>((size_t)wk);
+        if (wk >= (int64_t)1 << 32) throw Error(CBX_E_ARG, "pooling work list exceeds 2^32 pixels");
+        p.work = p.alloc<uint32_t>((size_t)wk);
         p.work_count = p.alloc<int>(1);
     }
 }

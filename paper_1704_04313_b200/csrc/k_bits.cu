@@ -417,95 +417,132 @@ void launch_dilate_bits(BitMask in, BitMask out, int S, int kh, int kw, int sh, 
 // ---------------------------------------------------------------------------
 // K5: max-pool (window/stride) or ReLU (window 1) recomputed for the output
 // pixels whose input window holds an updated pixel, compare-before-write
-// feeding the next CBCONV's change mask. A block handles one output word (32
-// pixels of a row) at a time; its threads sweep (pixel, 4-channel) items so
-// that neighbouring threads read neighbouring 16-byte chunks.
+// feeding the next CBCONV's change mask.
+//
+// Phase 1 (sparse frames, point_scan_kernel): one thread per output word (32
+// pixels of a row) forms the touched word from the input grid's updated mask
+// with word operations (2x2/2 pooling: OR of two rows, then pairs of bits
+// folded together; ReLU: the word itself; other windows: per-bit window
+// tests), writes U_out, resets the consumer's change word, and appends the
+// touched PIXELS to a flat work list (one atomic per warp).
+// Phase 2 (point_work_kernel): a flat grid-stride loop over (pixel, 4-channel)
+// items of the list; max-pool (first element seeds the max, then every
+// window element, baseline.cpp:134-138) or ReLU (baseline.cpp:115), compare
+// with the stored value, store; the change bits of a warp are merged per
+// mask word (match + OR-reduce) into one atomicOr, which also yields the
+// newly set bits for the per-stream changed-pixel counter.
 constexpr int kPtThreads = 256;
 
-// Phase 1 (sparse frames): one warp per output word (32 pixels of a row).
-// Lanes test their pixel's input window against the updated mask (ballot ->
-// touched word), reset the next layer's change word and write U_out; touched
-// words are appended to a work list (one atomic per block).
+// bit j of the result = bit 2j | bit 2j+1 of v (64 -> 32 bits)
+__device__ __forceinline__ uint32_t fold_pairs(uint64_t v) {
+    v = (v | (v >> 1)) & 0x5555555555555555ull;
+    v = (v | (v >> 1)) & 0x3333333333333333ull;
+    v = (v | (v >> 2)) & 0x0f0f0f0f0f0f0f0full;
+    v = (v | (v >> 4)) & 0x00ff00ff00ff00ffull;
+    v = (v | (v >> 8)) & 0x0000ffff0000ffffull;
+    v = (v | (v >> 16)) & 0x00000000ffffffffull;
+    return (uint32_t)v;
+}
+
+__device__ __forceinline__ uint32_t touched_word(const PointBitsArgs& a, int s, int y, int w) {
+    const BitMask& u = a.upd_in;
+    const uint32_t* row0 = u.d + (int64_t)s * u.stride;
+    uint32_t tw = 0;
+    if (a.window == 1 && a.stride == 1) {
+        tw = row0[(int64_t)y * u.wpr + w];
+    } else if (a.window == 2 && a.stride == 2) {
+        const uint32_t* r0 = row0 + (int64_t)(2 * y) * u.wpr;
+        const uint32_t* r1 = r0 + u.wpr;
+        const int w0 = 2 * w, w1 = 2 * w + 1;
+        const uint32_t lo = r0[w0] | r1[w0];
+        const uint32_t hi = w1 < u.wpr ? (r0[w1] | r1[w1]) : 0u;
+        tw = fold_pairs(((uint64_t)hi << 32) | lo);
+    } else {
+        for (int j = 0; j < 32; ++j) {
+            const int x = 32 * w + j;
+            bool t = false;
+            for (int kj = 0; kj < a.window && !t; ++kj)
+                for (int ki = 0; ki < a.window; ++ki) {
+                    const int xi = x * a.stride + ki;
+                    if (xi < u.W && bit_test(u, s, y * a.stride + kj, xi)) {
+                        t = true;
+                        break;
+                    }
+                }
+            tw |= t ? (1u << j) : 0u;
+        }
+    }
+    const int rem = a.out.W - 32 * w;  // pixels past the last full window do not exist
+    if (rem < 32) tw &= rem > 0 ? ((1u << rem) - 1u) : 0u;
+    return tw;
+}
+
 __global__ void __launch_bounds__(kPtThreads) point_scan_kernel(PointBitsArgs a) {
-    __shared__ int s_n, s_base;
-    __shared__ uint2 s_list[kPtThreads / 32];
     const int Ho = a.out.H, Wo = a.out.W;
     const int wpr = (Wo + 31) / 32;
     const int64_t nseg = (int64_t)a.S * Ho * wpr;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    for (int64_t base = (int64_t)blockIdx.x * (kPtThreads / 32); base < nseg; base += (int64_t)gridDim.x * (kPtThreads / 32)) {
-        if (threadIdx.x == 0) s_n = 0;
-        __syncthreads();
-        const int64_t seg = base + wib;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = (int64_t)blockIdx.x * kPtThreads; base < nseg; base += (int64_t)gridDim.x * kPtThreads) {
+        const int64_t seg = base + threadIdx.x;
         uint32_t tw = 0;
+        int s = 0, y = 0, w = 0;
         if (seg < nseg) {
-            const int s = (int)(seg / ((int64_t)Ho * wpr));
+            s = (int)(seg / ((int64_t)Ho * wpr));
             const int64_t r = seg - (int64_t)s * Ho * wpr;
-            const int y = (int)(r / wpr), w = (int)(r - (int64_t)(r / wpr) * wpr);
-            const int x = 32 * w + lane;
-            bool t = false;
-            if (x < Wo) {
-                for (int kj = 0; kj < a.window && !t; ++kj)
-                    for (int ki = 0; ki < a.window; ++ki)
-                        if (bit_test(a.upd_in, s, y * a.stride + kj, x * a.stride + ki)) {
-                            t = true;
-                            break;
-                        }
-            }
-            tw = __ballot_sync(0xffffffffu, t);
-            if (lane == 0) {
-                const int64_t wo = (int64_t)y * wpr + w;
-                if (a.U_out.d) a.U_out.d[(int64_t)s * a.U_out.stride + wo] = tw;
-                if (a.chg.d) a.chg.d[(int64_t)s * a.chg.stride + wo] = 0u;
-                if (tw) s_list[atomicAdd(&s_n, 1)] = make_uint2((uint32_t)seg, tw);
-            }
+            y = (int)(r / wpr);
+            w = (int)(r - (int64_t)y * wpr);
+            tw = touched_word(a, s, y, w);
+            const int64_t wo = (int64_t)y * wpr + w;
+            if (a.U_out.d) a.U_out.d[(int64_t)s * a.U_out.stride + wo] = tw;
+            if (a.chg.d) a.chg.d[(int64_t)s * a.chg.stride + wo] = 0u;
         }
-        __syncthreads();
-        if (threadIdx.x == 0 && s_n) s_base = atomicAdd(a.work_count, s_n);
-        __syncthreads();
-        if (threadIdx.x < s_n) a.work[s_base + threadIdx.x] = s_list[threadIdx.x];
+        // warp-aggregated append of the touched pixels
+        const int n = __popc(tw);
+        int incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int wtotal = __shfl_sync(0xffffffffu, incl, 31);
+        if (!wtotal) continue;
+        int wbase = 0;
+        if (lane == 31) wbase = atomicAdd(a.work_count, wtotal);
+        wbase = __shfl_sync(0xffffffffu, wbase, 31);
+        int pos = wbase + incl - n;
+        const uint32_t gbase = (uint32_t)((int64_t)s * Ho * Wo + (int64_t)y * Wo + 32 * w);
+        while (tw) {
+            const int j = __ffs(tw) - 1;
+            tw &= tw - 1;
+            a.work[pos++] = gbase + (uint32_t)j;
+        }
     }
 }
 
-// Phase 2: a block takes G touched words at a time (G = 256 / (32 * C/4),
-// at least 1) and sweeps their (pixel, 4-channel) items with all its threads.
-// Max-pool (first element seeds the max, then every window element,
-// baseline.cpp:134-138) or ReLU; compare-before-write assembles the next
-// CBCONV's change word in shared memory.
 template <bool FULL>
 __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a) {
-    __shared__ uint32_t s_changed[kPtThreads / 32];
     const int Ho = a.out.H, Wo = a.out.W;
     const int wpr = (Wo + 31) / 32;
     const int c4n = a.in.Cp / 4;
-    const int per_word = 32 * c4n;
-    const int G = max(1, min(kPtThreads / 32, kPtThreads / per_word));
-    const int64_t nwords = FULL ? (int64_t)a.S * Ho * wpr : (int64_t)*a.work_count;
+    const int64_t HoWo = (int64_t)Ho * Wo;
+    const int64_t npix = FULL ? (int64_t)a.S * HoWo : (int64_t)*a.work_count;
+    const int64_t items = npix * c4n;
     const int rowq = a.in.Wp * c4n;
-    for (int64_t g0 = (int64_t)blockIdx.x * G; g0 < nwords; g0 += (int64_t)gridDim.x * G) {
-        if (threadIdx.x < G) s_changed[threadIdx.x] = 0;
-        __syncthreads();
-        const int items = G * per_word;
-        for (int it = threadIdx.x; it < items; it += kPtThreads) {
-            const int gi = it / per_word, item = it - gi * per_word;
-            const int64_t e = g0 + gi;
-            if (e >= nwords) continue;
-            const int j = item / c4n, c4 = item - j * c4n;
-            uint32_t seg, tw;
-            if (FULL) {
-                seg = (uint32_t)e;
-                tw = 0xffffffffu;
-            } else {
-                const uint2 wk = a.work[e];
-                seg = wk.x;
-                tw = wk.y;
-            }
-            if (!((tw >> j) & 1u)) continue;
-            const int s = (int)(seg / ((uint32_t)Ho * wpr));
-            const uint32_t r = seg - (uint32_t)s * Ho * wpr;
-            const int y = (int)(r / wpr), w = (int)(r - (r / wpr) * wpr);
-            const int x = 32 * w + j;
-            if (x >= Wo) continue;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = (int64_t)blockIdx.x * kPtThreads; base < items; base += (int64_t)gridDim.x * kPtThreads) {
+        const int64_t it = base + threadIdx.x;
+        const bool act = it < items;
+        bool ch = false;
+        uint32_t* waddr = nullptr;
+        int s = 0, x = 0;
+        if (act) {
+            const int64_t pi = it / c4n;
+            const int c4 = (int)(it - pi * c4n);
+            const int64_t g = FULL ? pi : (int64_t)__ldg(a.work + pi);
+            s = (int)(g / HoWo);
+            const int p = (int)(g - (int64_t)s * HoWo);
+            const int y = p / Wo;
+            x = p - y * Wo;
             const float4* src = reinterpret_cast<const float4*>(
                 a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
             float4* dst = reinterpret_cast<float4*>(
@@ -522,40 +559,37 @@ __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a)
             }
             if (!FULL && a.chg.d) {
                 const float4 o = *dst;
-                if (ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
-                    ref_changed(m.w, o.w, a.tau))
-                    atomicOr(&s_changed[gi], 1u << j);
+                ch = ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
+                     ref_changed(m.w, o.w, a.tau);
+                waddr = a.chg.d + (int64_t)s * a.chg.stride + (int64_t)y * wpr + (x >> 5);
             }
             *dst = m;
         }
-        __syncthreads();
-        if (!FULL && a.chg.d && threadIdx.x < G && g0 + threadIdx.x < nwords) {
-            const uint32_t cw = s_changed[threadIdx.x];
-            if (cw) {
-                const uint32_t seg = a.work[g0 + threadIdx.x].x;
-                const int s = (int)(seg / ((uint32_t)Ho * wpr));
-                const uint32_t r = seg - (uint32_t)s * Ho * wpr;
-                a.chg.d[(int64_t)s * a.chg.stride + r] = cw;
-                if (a.chg_cnt) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, (unsigned long long)__popc(cw));
+        if (!FULL && a.chg.d) {
+            // one atomicOr per distinct mask word in the warp
+            const unsigned peers = __match_any_sync(0xffffffffu, reinterpret_cast<unsigned long long>(waddr));
+            const uint32_t bits = __reduce_or_sync(peers, ch ? (1u << (x & 31)) : 0u);
+            if (act && bits && lane == __ffs(peers) - 1) {
+                const uint32_t old = atomicOr(waddr, bits);
+                const uint32_t fresh = bits & ~old;
+                if (fresh && a.chg_cnt) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, (unsigned long long)__popc(fresh));
             }
         }
-        __syncthreads();
     }
 }
 
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
     const int wpr = (a.out.W + 31) / 32;
     const int64_t nseg = (int64_t)a.S * a.out.H * wpr;
-    const int per_word = 32 * (a.in.Cp / 4);
-    const int G = std::max(1, std::min(kPtThreads / 32, kPtThreads / per_word));
-    if (!a.upd_in.d) {  // full frame: every word, no change test (the next layer evaluates in full)
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nseg + G - 1) / G, (int64_t)kNumSMs * 16));
+    const int c4n = a.in.Cp / 4;
+    if (!a.upd_in.d) {  // full frame: every pixel, no change test (the next layer evaluates in full)
+        const int64_t items = (int64_t)a.S * a.out.H * a.out.W * c4n;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + kPtThreads - 1) / kPtThreads, (int64_t)kNumSMs * 16));
         point_work_kernel<true><<<grid, kPtThreads, 0, st>>>(a);
         return;
     }
     cudaMemsetAsync(a.work_count, 0, sizeof(int), st);
-    const int64_t blocks = (nseg + kPtThreads / 32 - 1) / (kPtThreads / 32);
-    const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)kNumSMs * 8));
+    const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>((nseg + kPtThreads - 1) / kPtThreads, (int64_t)kNumSMs * 8));
     point_scan_kernel<<<g1, kPtThreads, 0, st>>>(a);
     point_work_kernel<false><<<kNumSMs * 8, kPtThreads, 0, st>>>(a);
 }

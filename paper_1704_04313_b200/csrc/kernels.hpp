@@ -40,7 +40,7 @@ struct PointBitsArgs {  // MAXPOOL (window/stride) or RELU (relu=1, window=strid
     unsigned long long* chg_cnt;
     int cnt_stride;
     int S;
-    uint2* work;      // touched-word list (capacity S*Ho*wpr), sparse mode only
+    uint32_t* work;   // touched-pixel list s*Ho*Wo + y*Wo + x (capacity S*Ho*Wo), sparse mode only
     int* work_count;
 };
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st);
