@@ -2,7 +2,7 @@
 TAG=${1:-l}; RX=${2:-}
 mkdir -p gpurun_out
 B="python bench.py --steps 3 --warmup 2 --no-cpu --no-e2e"
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none -c 300 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none --cache-control none -c 300 --csv \
   --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_launches.out 2>&1
 echo "launch list rc=$?"
 if [ -n "$RX" ]; then
