@@ -185,6 +185,8 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
     const int nl = (int)layers_.size();
     dK_.assign(nl, nullptr);
     dBias_.assign(nl, nullptr);
+    hK_.assign(nl, {});
+    hB_.assign(nl, {});
     tc_.resize(nl);
     for (int k = 0; k < nl; ++k) {
         if (layers_[k].kind == CBX_CBCONV) cb_layers_.push_back(k);
@@ -524,6 +526,8 @@ void Engine::record(Plan& p, bool full) {
                     a.chg_cnt = cnt_next;
                     a.cnt_stride = 2;
                     a.S = S;
+                    a.hK = hK_[k].data();
+                    a.hB = hB_[k].data();
                     launch_conv_exact(a, st); mark("conv_exact", k);
                 }
                 break;
@@ -721,6 +725,11 @@ void Engine::load_layer(int layer, const float* K, const float* bias) {
     CBX_CUDA(cudaSetDevice(device_));
     CBX_CUDA(cudaMemcpy(dK_[layer], K, kd * g.outChannels * sizeof(float), cudaMemcpyHostToDevice));
     CBX_CUDA(cudaMemcpy(dBias_[layer], bias, g.outChannels * sizeof(float), cudaMemcpyHostToDevice));
+    hK_[layer].assign(K, K + kd * g.outChannels);
+    hB_[layer].assign(bias, bias + g.outChannels);
+    // recorded graphs may carry filters as kernel parameters: re-record
+    if (cb_) cb_->dirty = true;
+    if (base_) base_->dirty = true;
     if (tc_[layer]) tc_load_weights(*tc_[layer], K, stream_);
     CBX_CUDA(cudaStreamSynchronize(stream_));
 }

@@ -97,6 +97,7 @@ private:
 
     // weights (reference layout), per layer
     std::vector<float*> dK_, dBias_;
+    std::vector<std::vector<float>> hK_, hB_;  // host copies (kernel-parameter filters)
     std::vector<std::unique_ptr<TcLayer, TcLayerDeleter>> tc_;
 
     std::unique_ptr<Plan> cb_, base_;

@@ -519,72 +519,62 @@ __global__ void __launch_bounds__(kPtThreads) point_scan_kernel(PointBitsArgs a)
     }
 }
 
-// Recomputes channels [4*c4, 4*c4+4) of output pixel (s, y, x); returns
-// whether they changed by more than tau (only when `test`).
-__device__ __forceinline__ bool point_update(const PointBitsArgs& a, int s, int y, int x, int c4, int c4n, bool test) {
-    const int rowq = a.in.Wp * c4n;
-    const float4* src = reinterpret_cast<const float4*>(
-        a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
-    float4* dst = reinterpret_cast<float4*>(
-        a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp) + c4;
-    float4 m = *src;
-    if (a.relu) {
-        m = make_float4(ref_relu(m.x), ref_relu(m.y), ref_relu(m.z), ref_relu(m.w));
-    } else {
-        for (int kj = 0; kj < a.window; ++kj)
-            for (int ki = 0; ki < a.window; ++ki) {
-                const float4 v = src[kj * rowq + ki * c4n];
-                m = make_float4(ref_max(m.x, v.x), ref_max(m.y, v.y), ref_max(m.z, v.z), ref_max(m.w, v.w));
-            }
-    }
-    bool ch = false;
-    if (test) {
-        const float4 o = *dst;
-        ch = ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
-             ref_changed(m.w, o.w, a.tau);
-    }
-    *dst = m;
-    return ch;
-}
-
-// Merges the change bits of a warp per mask word (one atomicOr per distinct
-// word) and counts the newly set bits per stream. All lanes must call it.
-__device__ __forceinline__ void merge_change_bits(const PointBitsArgs& a, bool act, bool ch, int s, int y, int x) {
-    const int wpr = (a.out.W + 31) / 32;
-    uint32_t* waddr = act ? a.chg.d + (int64_t)s * a.chg.stride + (int64_t)y * wpr + (x >> 5) : nullptr;
-    const unsigned peers = __match_any_sync(0xffffffffu, reinterpret_cast<unsigned long long>(waddr));
-    const uint32_t bits = __reduce_or_sync(peers, ch ? (1u << (x & 31)) : 0u);
-    if (act && bits && (int)(threadIdx.x & 31) == __ffs(peers) - 1) {
-        const uint32_t old = atomicOr(waddr, bits);
-        const uint32_t fresh = bits & ~old;
-        if (fresh && a.chg_cnt) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, (unsigned long long)__popc(fresh));
-    }
-}
-
 template <bool FULL>
 __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a) {
     const int Ho = a.out.H, Wo = a.out.W;
+    const int wpr = (Wo + 31) / 32;
     const int c4n = a.in.Cp / 4;
     const int64_t HoWo = (int64_t)Ho * Wo;
     const int64_t npix = FULL ? (int64_t)a.S * HoWo : (int64_t)*a.work_count;
     const int64_t items = npix * c4n;
-    const bool test = !FULL && a.chg.d;
+    const int rowq = a.in.Wp * c4n;
+    const int lane = threadIdx.x & 31;
     for (int64_t base = (int64_t)blockIdx.x * kPtThreads; base < items; base += (int64_t)gridDim.x * kPtThreads) {
         const int64_t it = base + threadIdx.x;
         const bool act = it < items;
         bool ch = false;
-        int s = 0, y = 0, x = 0;
+        uint32_t* waddr = nullptr;
+        int s = 0, x = 0;
         if (act) {
             const int64_t pi = it / c4n;
             const int c4 = (int)(it - pi * c4n);
             const int64_t g = FULL ? pi : (int64_t)__ldg(a.work + pi);
             s = (int)(g / HoWo);
             const int p = (int)(g - (int64_t)s * HoWo);
-            y = p / Wo;
+            const int y = p / Wo;
             x = p - y * Wo;
-            ch = point_update(a, s, y, x, c4, c4n, test);
+            const float4* src = reinterpret_cast<const float4*>(
+                a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
+            float4* dst = reinterpret_cast<float4*>(
+                a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp) + c4;
+            float4 m = *src;
+            if (a.relu) {
+                m = make_float4(ref_relu(m.x), ref_relu(m.y), ref_relu(m.z), ref_relu(m.w));
+            } else {
+                for (int kj = 0; kj < a.window; ++kj)
+                    for (int ki = 0; ki < a.window; ++ki) {
+                        const float4 v = src[kj * rowq + ki * c4n];
+                        m = make_float4(ref_max(m.x, v.x), ref_max(m.y, v.y), ref_max(m.z, v.z), ref_max(m.w, v.w));
+                    }
+            }
+            if (!FULL && a.chg.d) {
+                const float4 o = *dst;
+                ch = ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
+                     ref_changed(m.w, o.w, a.tau);
+                waddr = a.chg.d + (int64_t)s * a.chg.stride + (int64_t)y * wpr + (x >> 5);
+            }
+            *dst = m;
         }
-        if (test) merge_change_bits(a, act, ch, s, y, x);
+        if (!FULL && a.chg.d) {
+            // one atomicOr per distinct mask word in the warp
+            const unsigned peers = __match_any_sync(0xffffffffu, reinterpret_cast<unsigned long long>(waddr));
+            const uint32_t bits = __reduce_or_sync(peers, ch ? (1u << (x & 31)) : 0u);
+            if (act && bits && lane == __ffs(peers) - 1) {
+                const uint32_t old = atomicOr(waddr, bits);
+                const uint32_t fresh = bits & ~old;
+                if (fresh && a.chg_cnt) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, (unsigned long long)__popc(fresh));
+            }
+        }
     }
 }
 

@@ -14,6 +14,8 @@
 //                  by comparing against the value it overwrites.
 //   relu        <- relu (baseline.cpp:113-117), same in-place scheme.
 //   classify    <- argmax_classify (baseline.cpp:147-163).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -229,6 +231,93 @@ __global__ void __launch_bounds__(kConvThreads) conv_planar_kernel(ConvArgs a) {
     }
 }
 
+// Planar first layer with the paper's geometry fixed at compile time (C in,
+// KHxKW taps, OC out, stride 1): the filters and biases travel as a kernel
+// parameter, so every multiply reads its weight straight from the constant
+// bank (no shared-memory loads), the 7x7x3 window is fully unrolled, and
+// interior pixels (whole window inside the frame, the common case) load
+// their taps without bounds predicates. Same arithmetic as the generic
+// kernels: bias first, ascending (c, kj, ki), __fmul_rn / __fadd_rn.
+template <int C, int KH, int KW, int OC>
+struct PlanarFilters {
+    float w[C * KH * KW][OC];
+    float b[OC];
+};
+
+template <int C, int KH, int KW, int OC>
+__global__ void __launch_bounds__(kConvThreads) conv_planar_fixed_kernel(ConvArgs a,
+                                                                         const __grid_constant__ PlanarFilters<C, KH, KW, OC> f) {
+    const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
+    const int Wo = a.out.W, H = a.in.H, W = a.in.W;
+    const int64_t HoWo = (int64_t)a.out.H * Wo, HW = (int64_t)H * W;
+    for (int64_t base = (int64_t)blockIdx.x * kConvThreads; base < total; base += (int64_t)gridDim.x * kConvThreads) {
+        const int64_t n = base + threadIdx.x;
+        const bool valid = n < total;
+        int s = 0, y = 0, x = 0;
+        bool changed = false;
+        if (valid) {
+            const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
+            s = (int)(g / HoWo);
+            const int p = (int)(g - (int64_t)s * HoWo);
+            y = p / Wo;
+            x = p - y * Wo;
+            const int y0 = y - a.ph, x0 = x - a.pw;
+            const float* src = a.in_ptrs[s];
+            float acc[OC];
+#pragma unroll
+            for (int j = 0; j < OC; ++j) acc[j] = f.b[j];
+            if (y0 >= 0 && y0 + KH <= H && x0 >= 0 && x0 + KW <= W) {
+                const float* win = src + (int64_t)y0 * W + x0;
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+#pragma unroll
+                    for (int kj = 0; kj < KH; ++kj) {
+                        const float* rp = win + c * HW + (int64_t)kj * W;
+                        float v[KW];
+#pragma unroll
+                        for (int ki = 0; ki < KW; ++ki) v[ki] = __ldg(rp + ki);
+#pragma unroll
+                        for (int ki = 0; ki < KW; ++ki)
+#pragma unroll
+                            for (int j = 0; j < OC; ++j)
+                                acc[j] = __fadd_rn(acc[j], __fmul_rn(f.w[(c * KH + kj) * KW + ki][j], v[ki]));
+                    }
+            } else {
+#pragma unroll 1
+                for (int c = 0; c < C; ++c)
+#pragma unroll 1
+                    for (int kj = 0; kj < KH; ++kj) {
+                        const int yy = y0 + kj;
+                        const bool rowok = (unsigned)yy < (unsigned)H;
+                        const float* rp = src + c * HW + (int64_t)(rowok ? yy : 0) * W;
+#pragma unroll
+                        for (int ki = 0; ki < KW; ++ki) {
+                            const int xx = x0 + ki;
+                            const float v = (rowok && (unsigned)xx < (unsigned)W) ? __ldg(rp + xx) : 0.0f;
+                            const int r = (c * KH + kj) * KW + ki;
+#pragma unroll
+                            for (int j = 0; j < OC; ++j) {
+                                // dynamic r: read the parameter copy through a generic load
+                                acc[j] = __fadd_rn(acc[j], __fmul_rn(f.w[r][j], v));
+                            }
+                        }
+                    }
+            }
+            float* dst = a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + (x + a.out.hw)) * a.out.Cp;
+#pragma unroll
+            for (int j = 0; j < OC; ++j) {
+                const float v = a.relu ? ref_relu(acc[j]) : acc[j];
+                if (a.chg.d) changed |= ref_changed(v, dst[j], a.tau);
+                dst[j] = v;
+            }
+        }
+        if (a.chg.d) {
+            if (valid && changed) bit_set(a.chg, s, y, x);
+            if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
+        }
+    }
+}
+
 template <int OC>
 static void launch_conv_exact_oc(const ConvArgs& a, int grid, cudaStream_t st) {
     const size_t smem = (size_t)a.in.C * a.kh * a.kw * OC * sizeof(float);
@@ -244,6 +333,16 @@ void launch_conv_exact(const ConvArgs& a, cudaStream_t st) {
     const int64_t max_tiles = (a.full_count + kConvThreads - 1) / kConvThreads;
     int grid = (int)std::min<int64_t>(max_tiles, (int64_t)kNumSMs * 12);
     if (grid < 1) grid = 1;
+    if (!std::getenv("CBX_NO_FIXED_PLANAR") && a.in_ptrs && a.hK && a.hB && a.in.C == 3 && a.kh == 7 && a.kw == 7 && a.sh == 1 && a.sw == 1 && a.out.C == 4 &&
+        a.out.Cp >= 4) {
+        // the paper's first layer (3 -> 4, 7x7, stride 1)
+        PlanarFilters<3, 7, 7, 4> f;
+        for (int r = 0; r < 3 * 7 * 7; ++r)
+            for (int j = 0; j < 4; ++j) f.w[r][j] = a.hK[(size_t)j * 147 + r];
+        for (int j = 0; j < 4; ++j) f.b[j] = a.hB[j];
+        conv_planar_fixed_kernel<3, 7, 7, 4><<<grid, kConvThreads, 0, st>>>(a, f);
+        return;
+    }
     if (a.out.C <= 4)
         launch_conv_exact_oc<4>(a, grid, st);
     else if (a.out.C <= 8)

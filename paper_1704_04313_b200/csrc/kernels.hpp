@@ -68,6 +68,10 @@ struct ConvArgs {
     unsigned long long* chg_cnt;
     int cnt_stride;
     int S;
+    // host copies of K / bias (optional): lets a geometry-specialised kernel
+    // carry the filters as kernel parameters (constant-bank FMUL operands)
+    const float* hK;
+    const float* hB;
 };
 void launch_conv_exact(const ConvArgs& a, cudaStream_t st);
 
