@@ -242,14 +242,36 @@ template <int C, int KH, int KW, int OC>
 struct PlanarFilters {
     float w[C * KH * KW][OC];
     float b[OC];
+    // 1.0f and -0.0f as RUNTIME values: the paired-fp32 path writes a rounded
+    // multiply as fma(w, x, -0) and a rounded add as fma(p, 1, acc); with
+    // compile-time constants ptxas would contract the pair into one fused
+    // multiply-add (one rounding instead of the reference's two).
+    float one, nzero;
 };
 
+// Two fp32 lanes per instruction (FFMA2), each IEEE round-to-nearest.
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 template <int C, int KH, int KW, int OC>
-__global__ void __launch_bounds__(kConvThreads) conv_planar_fixed_kernel(ConvArgs a,
-                                                                         const __grid_constant__ PlanarFilters<C, KH, KW, OC> f) {
+__global__ void __launch_bounds__(kConvThreads, 8) conv_planar_fixed_kernel(ConvArgs a,
+                                                                            const __grid_constant__ PlanarFilters<C, KH, KW, OC> f) {
+    static_assert(OC % 2 == 0, "paired accumulators");
     const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
     const int Wo = a.out.W, H = a.in.H, W = a.in.W;
     const int64_t HoWo = (int64_t)a.out.H * Wo, HW = (int64_t)H * W;
+    const unsigned long long one2 = f2_pack(f.one, f.one), nz2 = f2_pack(f.nzero, f.nzero);
     for (int64_t base = (int64_t)blockIdx.x * kConvThreads; base < total; base += (int64_t)gridDim.x * kConvThreads) {
         const int64_t n = base + threadIdx.x;
         const bool valid = n < total;
@@ -264,25 +286,36 @@ __global__ void __launch_bounds__(kConvThreads) conv_planar_fixed_kernel(ConvArg
             const int y0 = y - a.ph, x0 = x - a.pw;
             const float* src = a.in_ptrs[s];
             float acc[OC];
-#pragma unroll
-            for (int j = 0; j < OC; ++j) acc[j] = f.b[j];
             if (y0 >= 0 && y0 + KH <= H && x0 >= 0 && x0 + KW <= W) {
+                // interior: a channel's KHxKW taps in flight at once, then
+                // acc = round(acc + round(w * x)) two output channels per instruction
+                unsigned long long a2[OC / 2];
+#pragma unroll
+                for (int j = 0; j < OC / 2; ++j) a2[j] = f2_pack(f.b[2 * j], f.b[2 * j + 1]);
                 const float* win = src + (int64_t)y0 * W + x0;
 #pragma unroll
-                for (int c = 0; c < C; ++c)
+                for (int c = 0; c < C; ++c) {
+                    float v[KH * KW];
 #pragma unroll
-                    for (int kj = 0; kj < KH; ++kj) {
-                        const float* rp = win + c * HW + (int64_t)kj * W;
-                        float v[KW];
+                    for (int kj = 0; kj < KH; ++kj)
 #pragma unroll
-                        for (int ki = 0; ki < KW; ++ki) v[ki] = __ldg(rp + ki);
+                        for (int ki = 0; ki < KW; ++ki) v[kj * KW + ki] = __ldg(win + c * HW + (int64_t)kj * W + ki);
 #pragma unroll
-                        for (int ki = 0; ki < KW; ++ki)
+                    for (int t = 0; t < KH * KW; ++t) {
+                        const int r = c * KH * KW + t;
+                        const unsigned long long vv = f2_pack(v[t], v[t]);
 #pragma unroll
-                            for (int j = 0; j < OC; ++j)
-                                acc[j] = __fadd_rn(acc[j], __fmul_rn(f.w[(c * KH + kj) * KW + ki][j], v[ki]));
+                        for (int j = 0; j < OC / 2; ++j) {
+                            const unsigned long long prod = f2_fma(f2_pack(f.w[r][2 * j], f.w[r][2 * j + 1]), vv, nz2);
+                            a2[j] = f2_fma(prod, one2, a2[j]);
+                        }
                     }
+                }
+#pragma unroll
+                for (int j = 0; j < OC / 2; ++j) f2_unpack(a2[j], acc[2 * j], acc[2 * j + 1]);
             } else {
+#pragma unroll
+                for (int j = 0; j < OC; ++j) acc[j] = f.b[j];
 #pragma unroll 1
                 for (int c = 0; c < C; ++c)
 #pragma unroll 1
@@ -296,10 +329,7 @@ __global__ void __launch_bounds__(kConvThreads) conv_planar_fixed_kernel(ConvArg
                             const float v = (rowok && (unsigned)xx < (unsigned)W) ? __ldg(rp + xx) : 0.0f;
                             const int r = (c * KH + kj) * KW + ki;
 #pragma unroll
-                            for (int j = 0; j < OC; ++j) {
-                                // dynamic r: read the parameter copy through a generic load
-                                acc[j] = __fadd_rn(acc[j], __fmul_rn(f.w[r][j], v));
-                            }
+                            for (int j = 0; j < OC; ++j) acc[j] = __fadd_rn(acc[j], __fmul_rn(f.w[r][j], v));
                         }
                     }
             }
@@ -340,6 +370,8 @@ void launch_conv_exact(const ConvArgs& a, cudaStream_t st) {
         for (int r = 0; r < 3 * 7 * 7; ++r)
             for (int j = 0; j < 4; ++j) f.w[r][j] = a.hK[(size_t)j * 147 + r];
         for (int j = 0; j < 4; ++j) f.b[j] = a.hB[j];
+        f.one = 1.0f;
+        f.nzero = -0.0f;
         conv_planar_fixed_kernel<3, 7, 7, 4><<<grid, kConvThreads, 0, st>>>(a, f);
         return;
     }
