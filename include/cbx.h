@@ -8,6 +8,7 @@
  *   cbx_create + cbx_load_layer  <- load_network            core/include/cbinfer/network.hpp:88
  *                                   (+ read_weights_f32le   core/include/cbinfer/io.hpp:29)
  *   cbx_forward / _device        <- forward_frame           core/include/cbinfer/network.hpp:93-94
+ *   cbx_submit / cbx_wait        <- forward_frame, pipelined (host frames; copy overlaps compute)
  *   cbx_reset                    <- reset_state             core/include/cbinfer/network.hpp:97
  *   cbx_set_thresholds           <- Network::set_thresholds core/include/cbinfer/network.hpp:67
  *   cbx_get_thresholds           <- Network::thresholds     core/include/cbinfer/network.hpp:66
@@ -149,6 +150,19 @@ CBX_API int cbx_forward(cbx_ctx* ctx, int engine, const float* frames, uint16_t*
  * reference, i.e. prevInput of the first CBCONV). Asynchronous on the context
  * stream; use cbx_sync / cbx_read_* afterwards. */
 CBX_API int cbx_forward_device(cbx_ctx* ctx, int engine, const float* const* frames_dev);
+/* Pipelined host-frame serving (forward_frame, network.hpp:93-94, split in
+ * two): cbx_submit enqueues one frame of every stream -- host -> device copy
+ * on a copy stream into a staging ring, the change-based evaluation on the
+ * context stream once the copy has landed, labels copied back into `labels`
+ * -- and returns at once with a ticket; the copy of the next submission
+ * overlaps the kernels of this one. cbx_wait(ticket) blocks until that frame
+ * is done; `labels` is then valid and stats/macs (nullable) are filled as by
+ * cbx_forward. Frames are consumed in submission order (each is the next
+ * frame of every stream). `frames` and `labels` must stay valid until the
+ * wait returns; pin them (cudaHostAlloc) for the copies to overlap. Only the
+ * last 3 tickets can be waited on. Change-based engine only. */
+CBX_API int cbx_submit(cbx_ctx* ctx, int engine, const float* frames, uint16_t* labels, int64_t* ticket);
+CBX_API int cbx_wait(cbx_ctx* ctx, int64_t ticket, cbx_layer_stats* stats, uint64_t* macs);
 CBX_API int cbx_sync(cbx_ctx* ctx);
 CBX_API int cbx_read_labels(cbx_ctx* ctx, int engine, uint16_t* labels);
 CBX_API int cbx_read_stats(cbx_ctx* ctx, int engine, cbx_layer_stats* stats, uint64_t* macs);

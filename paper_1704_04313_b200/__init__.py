@@ -365,6 +365,37 @@ class Network:
             out.append(ForwardResult(labels[s], st, macs[s]))
         return out
 
+    def submit(self, frames: np.ndarray, labels: np.ndarray) -> int:
+        """cbx_submit: enqueue the next frame of every stream ([S, C, H, W]
+        float32 host array) without waiting; labels ([S, Hl, Wl] uint16 host
+        array) is filled by the time wait(ticket) returns. Both must stay
+        alive and unchanged until then; pinned host memory lets the copy of
+        the next submission overlap this frame's kernels."""
+        if frames.dtype != np.float32 or not frames.flags.c_contiguous or frames.size != self._frame_elems * self.streams:
+            raise ShapeError("submit: frames must be a contiguous float32 [S, C, H, W] array of the network input")
+        want = (self.streams,) + tuple(self.label_hw)
+        if labels.dtype != np.uint16 or not labels.flags.c_contiguous or labels.shape != want:
+            raise ShapeError(f"submit: labels must be a contiguous uint16 array of shape {want}")
+        t = C.c_int64()
+        self._chk(lib.cbx_submit(self._h, ENGINES["cbinfer"], frames.ctypes.data_as(C.POINTER(C.c_float)),
+                                 labels.ctypes.data_as(C.POINTER(C.c_uint16)), C.byref(t)))
+        return t.value
+
+    def wait(self, ticket: int, with_stats: bool = True):
+        """cbx_wait: block until submission `ticket` is done; returns its
+        per-stream LayerStats lists (or None) and macsTotal per stream."""
+        S = self.streams
+        if not with_stats:
+            self._chk(lib.cbx_wait(self._h, ticket, None, None))
+            return None
+        stats = (LayerStats * (S * self.nl))()
+        macs = (C.c_uint64 * S)()
+        self._chk(lib.cbx_wait(self._h, ticket, stats, macs))
+        return [[dict(changedInputPixels=stats[s * self.nl + k].changedInputPixels,
+                      changedOutputPixels=stats[s * self.nl + k].changedOutputPixels,
+                      gemmMacs=stats[s * self.nl + k].gemmMacs) for k in range(self.nl)]
+                for s in range(S)], list(macs)
+
     def forward_frame(self, frame: np.ndarray, engine: str = "cbinfer") -> ForwardResult:
         return self.forward(frame, engine)[0]
 

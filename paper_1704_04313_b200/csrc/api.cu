@@ -156,6 +156,17 @@ CBX_API int cbx_forward_device(cbx_ctx* ctx, int engine, const float* const* fra
     return guarded(ctx, [&] { E(ctx).forward_device(engine, frames_dev); });
 }
 
+CBX_API int cbx_submit(cbx_ctx* ctx, int engine, const float* frames, uint16_t* labels, int64_t* ticket) {
+    return guarded(ctx, [&] {
+        if (!ticket) throw cbx::Error(CBX_E_ARG, "null ticket");
+        *ticket = E(ctx).submit(engine, frames, labels);
+    });
+}
+
+CBX_API int cbx_wait(cbx_ctx* ctx, int64_t ticket, cbx_layer_stats* stats, uint64_t* macs) {
+    return guarded(ctx, [&] { E(ctx).wait(ticket, stats, macs); });
+}
+
 CBX_API int cbx_sync(cbx_ctx* ctx) {
     return guarded(ctx, [&] { E(ctx).sync(); });
 }

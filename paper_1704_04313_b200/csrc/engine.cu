@@ -237,6 +237,14 @@ Engine::~Engine() {
     cudaFree(d_cur_);
     for (auto& s : slots_) cudaFree(s);
     cudaFreeHost(h_stats_);
+    if (copy_st_) cudaStreamSynchronize(copy_st_);
+    for (int q = 0; q < kRing; ++q) {
+        if (ring_[q]) cudaFree(ring_[q]);
+        if (copied_[q]) cudaEventDestroy(copied_[q]);
+        if (done_[q]) cudaEventDestroy(done_[q]);
+    }
+    if (h_ring_stats_) cudaFreeHost(h_ring_stats_);
+    if (copy_st_) cudaStreamDestroy(copy_st_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -637,6 +645,14 @@ void Engine::forward_host(int engine, const float* frames, uint16_t* labels, cbx
 }
 
 void Engine::forward_device(int engine, const float* const* frames_dev) {
+    const int nl = (int)layers_.size();
+    enqueue(engine, frames_dev, h_stats_ + (size_t)engine * 2 * S_ * nl);
+    pending_engine_ = engine;
+}
+
+// Enqueues one frame on the context stream (pointer table, graph, counter
+// readback into stats_dst); returns whether it is a full evaluation.
+bool Engine::enqueue(int engine, const float* const* frames_dev, unsigned long long* stats_dst) {
     if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
     if (!frames_dev) throw Error(CBX_E_ARG, "frames is null");
     CBX_CUDA(cudaSetDevice(device_));
@@ -645,14 +661,65 @@ void Engine::forward_device(int engine, const float* const* frames_dev) {
     stage_frame_pointers(engine, frames_dev, engine == CBX_ENGINE_CBINFER && has_history_ ? last_cb_frames_.data() : nullptr);
     launch(p, full);
     const int nl = (int)layers_.size();
-    CBX_CUDA(cudaMemcpyAsync(h_stats_ + (size_t)engine * 2 * S_ * nl, p.stats, sizeof(unsigned long long) * 2 * S_ * nl,
-                             cudaMemcpyDeviceToHost, stream_));
+    CBX_CUDA(cudaMemcpyAsync(stats_dst, p.stats, sizeof(unsigned long long) * 2 * S_ * nl, cudaMemcpyDeviceToHost, stream_));
     last_full_[engine] = full;
     if (engine == CBX_ENGINE_CBINFER) {
         has_history_ = true;
         last_cb_frames_.assign(frames_dev, frames_dev + S_);
     }
-    pending_engine_ = engine;
+    return full;
+}
+
+// Pipelined host-frame path (cbx_submit / cbx_wait). Frame j is copied into
+// ring slot j % 3 on a copy stream and evaluated on the context stream once
+// the copy has landed, so the H2D copy of frame j+1 overlaps the kernels of
+// frame j. Slot j % 3 was last read by frame j-2 (as its detection
+// reference), hence the copy of frame j waits for frame j-2 only.
+int64_t Engine::submit(int engine, const float* frames, uint16_t* labels) {
+    if (engine != CBX_ENGINE_CBINFER)
+        throw Error(CBX_E_ARG, "cbx_submit runs the change-based engine (use cbx_forward for the dense comparator)");
+    if (!frames || !labels) throw Error(CBX_E_ARG, "null frames or labels");
+    CBX_CUDA(cudaSetDevice(device_));
+    const int nl = (int)layers_.size();
+    const size_t per = (size_t)net_.inputChannels * net_.inputHeight * net_.inputWidth;
+    if (!ring_[0]) {
+        for (auto& r : ring_) r = dmalloc<float>(per * S_);
+        CBX_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
+        for (int q = 0; q < kRing; ++q) {
+            CBX_CUDA(cudaEventCreateWithFlags(&copied_[q], cudaEventDisableTiming));
+            CBX_CUDA(cudaEventCreateWithFlags(&done_[q], cudaEventDisableTiming));
+        }
+        CBX_CUDA(cudaMallocHost(&h_ring_stats_, sizeof(unsigned long long) * kRing * 2 * S_ * nl));
+    }
+    const int64_t j = submitted_;
+    const int q = (int)(j % kRing);
+    if (j >= 2) CBX_CUDA(cudaStreamWaitEvent(copy_st_, done_[(j - 2) % kRing], 0));
+    CBX_CUDA(cudaMemcpyAsync(ring_[q], frames, per * S_ * sizeof(float), cudaMemcpyHostToDevice, copy_st_));
+    CBX_CUDA(cudaEventRecord(copied_[q], copy_st_));
+    CBX_CUDA(cudaStreamWaitEvent(stream_, copied_[q], 0));
+    std::vector<const float*> cur(S_);
+    for (int s = 0; s < S_; ++s) cur[s] = ring_[q] + per * s;
+    ring_full_[q] = enqueue(engine, cur.data(), h_ring_stats_ + (size_t)q * 2 * S_ * nl);
+    CBX_CUDA(cudaMemcpyAsync(labels, plan(engine).labels, sizeof(uint16_t) * S_ * lh_ * lw_, cudaMemcpyDeviceToHost,
+                             stream_));
+    CBX_CUDA(cudaEventRecord(done_[q], stream_));
+    ring_ticket_[q] = j;
+    submitted_ = j + 1;
+    return j;
+}
+
+void Engine::wait(int64_t ticket, cbx_layer_stats* stats, uint64_t* macs) {
+    const int q = (int)(((ticket % kRing) + kRing) % kRing);
+    if (ticket < 0 || ticket >= submitted_ || ring_ticket_[q] != ticket)
+        throw Error(CBX_E_ARG, "cbx_wait: unknown or expired ticket (at most the last 3 submissions can be waited on)");
+    CBX_CUDA(cudaSetDevice(device_));
+    CBX_CUDA(cudaEventSynchronize(done_[q]));
+    const int nl = (int)layers_.size();
+    std::vector<cbx_layer_stats> st((size_t)S_ * nl);
+    std::vector<uint64_t> mc(S_);
+    stats_from(h_ring_stats_ + (size_t)q * 2 * S_ * nl, ring_full_[q], CBX_ENGINE_CBINFER, st.data(), mc.data());
+    if (stats) std::memcpy(stats, st.data(), sizeof(cbx_layer_stats) * st.size());
+    if (macs) std::memcpy(macs, mc.data(), sizeof(uint64_t) * S_);
 }
 
 void Engine::sync() { CBX_CUDA(cudaStreamSynchronize(stream_)); }
@@ -660,9 +727,13 @@ void Engine::sync() { CBX_CUDA(cudaStreamSynchronize(stream_)); }
 void Engine::finish_stats(Plan& p, bool full, int engine) {
     (void)p;
     const int nl = (int)layers_.size();
-    const unsigned long long* hs = h_stats_ + (size_t)engine * 2 * S_ * nl;
-    auto& out = last_stats_[engine];
-    auto& macs = last_macs_[engine];
+    stats_from(h_stats_ + (size_t)engine * 2 * S_ * nl, full, engine, last_stats_[engine].data(), last_macs_[engine].data());
+}
+
+// Per-stream LayerStats from the device counters (cbconv.cpp:170-192,
+// 212-220; non-CB convs report full-frame work, network.cpp:241-248,290-294).
+void Engine::stats_from(const unsigned long long* hs, bool full, int engine, cbx_layer_stats* out, uint64_t* macs) const {
+    const int nl = (int)layers_.size();
     for (int s = 0; s < S_; ++s) {
         uint64_t total = 0;
         for (int k = 0; k < nl; ++k) {

@@ -51,6 +51,9 @@ public:
     void forward_host(int engine, const float* frames, uint16_t* labels, cbx_layer_stats* stats,
                       uint64_t* macs);
     void forward_device(int engine, const float* const* frames_dev);
+    // pipelined host-frame path (cbx_submit / cbx_wait)
+    int64_t submit(int engine, const float* frames, uint16_t* labels);
+    void wait(int64_t ticket, cbx_layer_stats* stats, uint64_t* macs);
     void sync();
     void read_labels(int engine, uint16_t* labels);
     void read_stats(int engine, cbx_layer_stats* stats, uint64_t* macs);
@@ -75,6 +78,8 @@ private:
     void launch(Plan& p, bool full);
     void stage_frame_pointers(int engine, const float* const* cur, const float* const* prev);
     void finish_stats(Plan& p, bool full, int engine);
+    void stats_from(const unsigned long long* hs, bool full, int engine, cbx_layer_stats* out, uint64_t* macs) const;
+    bool enqueue(int engine, const float* const* frames_dev, unsigned long long* stats_dst);
     void mark(const char* name, int layer);
     int tail_end(int k) const;
     int final_tensor() const;
@@ -110,6 +115,16 @@ private:
     // host-input staging slots: CB ping-pong + baseline
     float* slots_[3] = {nullptr, nullptr, nullptr};
     int parity_ = 0;
+
+    // submit/wait ring: staging slots, copy stream, per-slot events and counters
+    static constexpr int kRing = 3;
+    float* ring_[kRing] = {nullptr, nullptr, nullptr};
+    cudaStream_t copy_st_ = nullptr;
+    cudaEvent_t copied_[kRing] = {nullptr, nullptr, nullptr}, done_[kRing] = {nullptr, nullptr, nullptr};
+    unsigned long long* h_ring_stats_ = nullptr;  // pinned, [kRing][nl][S][2]
+    bool ring_full_[kRing] = {false, false, false};
+    int64_t ring_ticket_[kRing] = {-1, -1, -1};
+    int64_t submitted_ = 0;
 
     // host stats of the last forward, per engine
     std::vector<cbx_layer_stats> last_stats_[2];

@@ -175,3 +175,43 @@ def test_errors(gpu, orc):
         net.set_thresholds([0.1, -0.1, 0.1])
     net.set_thresholds([0.5, 0.25, 0.125])
     assert net.thresholds() == [0.5, 0.25, 0.125]
+
+
+@pytest.mark.parametrize("precision", ["exact", "tf32"])
+def test_submit_wait_pipelined(gpu, orc, precision):
+    """cbx_submit / cbx_wait with two frames in flight reproduces the oracle
+    frame by frame (exact mode bitwise; tf32 labels within tolerance) and
+    matches the synchronous forward exactly."""
+    spec = paper_spec(48, 64)
+    w = orc.generate_weights(spec, 1)
+    S = 2
+    cfgs = [dict(channels=3, height=48, width=64, sprites=[(10, 2 + s, 0.9)], noise=0.01, seed=3 + s) for s in range(S)]
+    onets = [orc.load_network(spec, w) for _ in range(S)]
+    pipe = gpu.Network(to_pkg_spec(gpu, spec), w, streams=S, precision=precision)
+    sync = gpu.Network(to_pkg_spec(gpu, spec), w, streams=S, precision=precision)
+    F = 6
+    frames = [np.ascontiguousarray(np.stack([orc.synth_frame(c, f) for c in cfgs])) for f in range(F)]
+    labels = [np.zeros((S,) + tuple(pipe.label_hw), np.uint16) for _ in range(F)]
+    tickets, results = [], []
+    for f in range(F):
+        tickets.append(pipe.submit(frames[f], labels[f]))
+        if f >= 1:
+            results.append(pipe.wait(tickets[f - 1]))
+    results.append(pipe.wait(tickets[-1]))
+    for f in range(F):
+        ref = sync.forward(frames[f])
+        stats, macs = results[f]
+        for s in range(S):
+            want = onets[s].forward_frame(frames[f][s])
+            assert np.array_equal(labels[f][s], ref[s].labels), (f, s)
+            assert np.array_equal(stats_arr(stats[s]), stats_arr(ref[s].stats)), (f, s)
+            assert macs[s] == ref[s].macsTotal
+            if precision == "exact":
+                assert np.array_equal(labels[f][s], want["labels"]), (f, s)
+                assert np.array_equal(stats_arr(stats[s]), stats_arr(want["stats"])), (f, s)
+            else:
+                assert (labels[f][s] != want["labels"]).mean() <= 1e-3
+    with pytest.raises(gpu.CbxError):
+        pipe.wait(tickets[0])  # expired: only the last 3 submissions can be waited on
+    with pytest.raises(gpu.CbxError):
+        pipe.wait(F + 5)
