@@ -282,6 +282,31 @@ public:
         r.macsTotal = macs;
         return r;
     }
+    // Pipelined serving (cbx_submit / cbx_wait): enqueue the next frame and
+    // return at once; the upload of the next submission overlaps this one's
+    // kernels. `frame` and `labels` must stay alive until wait(ticket).
+    std::int64_t submit(const FrameTensor& frame, LabelMap& labels) {
+        if (frame.channels != spec_.inputChannels || frame.height != spec_.inputHeight ||
+            frame.width != spec_.inputWidth)
+            throw shape_error("forward_frame: frame does not match network input dimensions");
+        labels.height = lh_;
+        labels.width = lw_;
+        labels.labels.resize(size_t(lh_) * lw_);
+        std::int64_t t = -1;
+        check(cbx_submit(ctx_, static_cast<int>(Engine::CBInfer), frame.data.data(), labels.labels.data(), &t), ctx_);
+        return t;
+    }
+    void wait(std::int64_t ticket, std::vector<LayerStats>* stats = nullptr, std::uint64_t* macsTotal = nullptr) {
+        std::vector<cbx_layer_stats> st(spec_.layers.size());
+        std::uint64_t macs = 0;
+        check(cbx_wait(ctx_, ticket, st.data(), &macs), ctx_);
+        if (stats) {
+            stats->resize(st.size());
+            for (size_t k = 0; k < st.size(); ++k)
+                (*stats)[k] = {st[k].changedInputPixels, st[k].changedOutputPixels, st[k].gemmMacs};
+        }
+        if (macsTotal) *macsTotal = macs;
+    }
     void reset() { check(cbx_reset(ctx_), ctx_); }
     const NetworkSpec& spec() const { return spec_; }
     cbx_ctx* handle() { return ctx_; }
