@@ -236,7 +236,6 @@ struct TcArgs {
     const float* bias;   // [O]
     int NKB, Npad, N0, N1;
     int Brows;           // filter rows held per CTA (Npad, or Npad/2 for a CTA pair)
-    int dbg;             // EXPERIMENT bits: 1 skip A gather, 2 skip N1 MMA, 4 skip B copy, 8 no proxy fence, 16 no epilogue math, 32 no tc fence, 64 MMAs back to back (no stage handshake)
     int stages, acc_stages, acc_cols, tmem_cols;
     int relu;
     BitMask chg;
@@ -427,7 +426,6 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                            ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
                 }
                 for (int kb = 0; kb < a.NKB; ++kb, ++it) {
-                    if (a.dbg & 64) break;
                     const uint32_t st = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[st], ph ^ 1u);
                     if (r == 0) {
@@ -472,22 +470,17 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 }
             }
             for (int kb = 0; kb < a.NKB; ++kb, ++it) {
-                if (a.dbg & 64) break;
                 const uint32_t st = it % NS, ph = (it / NS) & 1u;
                 mbar_wait(&empty[st], ph ^ 1u);
                 if (pt == 0) {
-                    if (a.dbg & 4) {
-                        mbar_arrive(&full[st]);
-                    } else {
-                        mbar_arrive_expect_tx(&full[st], b_bytes);
-                        bulk_g2s(sB + (size_t)st * b_bytes, Bw + (size_t)kb * a.Brows * kKBlock, b_bytes, &full[st]);
-                    }
+                    mbar_arrive_expect_tx(&full[st], b_bytes);
+                    bulk_g2s(sB + (size_t)st * b_bytes, Bw + (size_t)kb * a.Brows * kKBlock, b_bytes, &full[st]);
                 }
                 const int off = sTab[kb * kChunksPerKB + j];
                 const uint32_t stage = smem_u32(sA + (size_t)st * kABytes) + swz_off;
 #pragma unroll
                 for (int i = 0; i < kRowsPerThread; ++i)
-                    if (((vmask >> i) & 1u) && !(a.dbg & 1))
+                    if ((vmask >> i) & 1u)
                         cp_async16(stage + (rsub + 16 * i) * 128, off >= 0 ? base[i] + off : a.in, off >= 0 ? 16u : 0u);
                 cp_async_arrive_noinc(&full[st]);
             }
@@ -520,10 +513,10 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 const uint32_t d = tmem_base + as * a.acc_cols;
                 for (int kb = 0; kb < a.NKB; ++kb, ++it) {
                     const uint32_t st = it % NS, ph = (it / NS) & 1u;
-                    if (!(a.dbg & 64)) mbar_wait(&full[st], ph);
+                    mbar_wait(&full[st], ph);
                     if constexpr (PAIR) mbar_wait_cluster(&pfull[st], ph);
-                    if (!(a.dbg & 8)) fence_proxy_async();
-                    if (!(a.dbg & 32)) tc_fence_after();
+                    fence_proxy_async();
+                    tc_fence_after();
                     const uint32_t aaddr = smem_u32(sA + (size_t)st * kABytes);
                     const uint32_t baddr = smem_u32(sB + (size_t)st * b_bytes);
 #pragma unroll
@@ -535,10 +528,10 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                             if (a.N1 > 0) mma_tf32_pair(d + a.N0, ad, smem_desc(baddr + b1_off + k * 32), id1, accum);
                         } else {
                             mma_tf32(d, ad, smem_desc(baddr + k * 32), id0, accum);
-                            if (a.N1 > 0 && !(a.dbg & 2)) mma_tf32(d + a.N0, ad, smem_desc(baddr + b1_off + k * 32), id1, accum);
+                            if (a.N1 > 0) mma_tf32(d + a.N0, ad, smem_desc(baddr + b1_off + k * 32), id1, accum);
                         }
                     }
-                    if constexpr (PAIR) mma_commit_pair(&empty[st]); else if (!(a.dbg & 64)) mma_commit(&empty[st]);
+                    if constexpr (PAIR) mma_commit_pair(&empty[st]); else mma_commit(&empty[st]);
                 }
                 if constexpr (PAIR) mma_commit_pair(&tfull[as]); else mma_commit(&tfull[as]);
             }
@@ -575,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             for (int c0 = 0; c0 < a.O; c0 += 32) {
                 float v[32];
                 tmem_ld32(trow + c0, v);
-                if (!valid || (a.dbg & 16)) continue;
+                if (!valid) continue;
                 if (c0 + 32 <= a.O)
                     epi_chunk<TC, true>(a, v, c0, 32, sBias, sTailW, t1, dst, changed);
                 else
@@ -804,7 +797,6 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.N0 = t.N0;
     a.N1 = t.N1;
     a.Brows = t.Brows;
-    if (const char* e = std::getenv("CBX_TC_DBG")) a.dbg = std::atoi(e);
     a.stages = t.stages;
     a.acc_stages = t.acc_stages;
     a.acc_cols = t.acc_cols;
