@@ -657,7 +657,13 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     const int nchunks = g.kernelH * g.kernelW * (t->Cp / 4);
     t->NKB = (nchunks + kChunksPerKB - 1) / kChunksPerKB;
     t->Npad = (int)round_up(g.outChannels, 16);
-    t->N0 = t->Npad > 256 ? 256 : t->Npad;
+    // N > 256 needs two MMAs per K-step; split evenly (304 = 160 + 144, not
+    // 256 + 48): a narrow instruction re-reads the whole A slice for few
+    // columns and is shared-memory-bound, a balanced pair is not.
+    // CBX_TC_NSPLIT=0 keeps the 256 + rest split (tuning).
+    const char* ns_env = std::getenv("CBX_TC_NSPLIT");
+    const bool even = !(ns_env && std::atoi(ns_env) == 0);
+    t->N0 = t->Npad > 256 ? (even ? (int)round_up(t->Npad / 2, 16) : 256) : t->Npad;
     t->N1 = t->Npad - t->N0;
     t->acc_cols = (int)round_up(t->Npad, 32);  // tcgen05.ld reads 32-column groups
     t->acc_stages = (2 * t->acc_cols <= 512) ? 2 : 1;

@@ -24,6 +24,7 @@ ap.add_argument("--recipe", default="2.2")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--only", default="", help="engine filter: cbinfer or baseline")
 ap.add_argument("--stages", default="", help="comma list of CBX_TC_STAGES values to sweep")
+ap.add_argument("--nsplit", default="", help="comma list of CBX_TC_NSPLIT values (1 even split, 0 256+rest)")
 args = ap.parse_args()
 
 S, F, H, W = args.streams, 6, 1080, 1920
@@ -40,10 +41,13 @@ for s in range(S):
 torch.cuda.synchronize()
 ptrs = lambda i: [clip[bench.pingpong(i, F), s].data_ptr() for s in range(S)]
 
-combos = [(int(m), st) for m in args.modes.split(",") for st in (args.stages.split(",") if args.stages else [""])]
-for mode, st in combos:
+combos = [(int(m), st, sp) for m in args.modes.split(",") for st in (args.stages.split(",") if args.stages else [""])
+          for sp in (args.nsplit.split(",") if args.nsplit else [""])]
+for mode, st, sp in combos:
     if st:
         os.environ["CBX_TC_STAGES"] = st
+    if sp:
+        os.environ["CBX_TC_NSPLIT"] = sp
     net.set_tc_pair(mode)
     for engine in ("baseline", "cbinfer"):
         if args.only and engine != args.only:
@@ -57,5 +61,5 @@ for mode, st in combos:
             for kt in net.profile(ptrs(4 + r), engine):
                 acc.setdefault(f"{kt['name']}[{kt['layer']}]", []).append(kt["ms"])
         tot = sum(sum(v) / len(v) for v in acc.values())
-        print(f"pair={mode} stages={st or 'auto'} {engine}: total {tot * 1000:.1f} us  " +
+        print(f"pair={mode} stages={st or 'auto'} nsplit={sp or 'auto'} {engine}: total {tot * 1000:.1f} us  " +
               "  ".join(f"{k}={1000 * sum(v) / len(v):.1f}" for k, v in acc.items()), flush=True)
