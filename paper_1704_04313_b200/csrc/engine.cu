@@ -142,7 +142,6 @@ struct Engine::Plan {
     std::vector<int*> cnt;
     std::vector<int> idx_src;       // conv layer whose list is reused (-1: own)
     std::vector<void*> allocs;
-    void* ws = nullptr;
     uint16_t* labels = nullptr;
     unsigned long long* stats = nullptr;  // [nl][S][2]
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -150,7 +149,13 @@ struct Engine::Plan {
     bool dirty = true;
     int fused_from = -1;            // conv layer whose epilogue runs the per-pixel tail (-1: none)
     uint32_t* work = nullptr;       // touched-pixel list shared by the MAXPOOL/RELU layers
-    int* work_count = nullptr;
+    // Frame scratch zeroed by ONE memset at the start of a steady frame:
+    // stats counters, each compaction's look-back status words, each
+    // MAXPOOL/RELU's work-list counter (no per-kernel memset nodes).
+    uint8_t* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    std::vector<void*> ws_k;        // per conv layer
+    std::vector<int*> wcount_k;     // per MAXPOOL/RELU layer
 
     ~Plan() {
         for (auto& g : gexec)
@@ -326,7 +331,7 @@ void Engine::build_plan(Plan& p, bool baseline) {
 
     // change masks (inputs of CBCONV layers) and updated masks
     const int nt = hasClassify ? nl : nl + 1;
-    size_t ws = 0;
+    std::vector<size_t> ws_bytes(nl, 0);
     for (int t = 0; t < nt; ++t) {
         int c, h, w;
         tensor_dims(t, c, h, w);
@@ -388,13 +393,12 @@ void Engine::build_plan(Plan& p, bool baseline) {
         p.idx[k] = p.alloc<int32_t>((size_t)S * Ho * Wo);
         p.cnt[k] = p.alloc<int>(1);
         const int wpr = (Wo + 31) / 32;
-        ws = std::max(ws, dilate_compact_workspace(BitMask{nullptr, Ho, Wo, wpr, round_up((int64_t)Ho * wpr, 2048)}, S));
+        ws_bytes[k] = round_up(dilate_compact_workspace(BitMask{nullptr, Ho, Wo, wpr, round_up((int64_t)Ho * wpr, 2048)}, S), 256);
         // strided geometries dilate separately, then compact the dilated mask
         if (!identity_geom(l.geom) && (l.geom.strideH != 1 || l.geom.strideW != 1 || l.geom.kernelW - 1 - l.geom.padW > 31 ||
                                        l.geom.padW > 31) && !p.U[k].d)
             p.U[k] = p.mask(S, Ho, Wo);
     }
-    if (ws) p.ws = p.alloc<uint8_t>(ws);
     int64_t wk = 0;
     for (int k = 0; k < nl; ++k)
         if (layers_[k].kind == CBX_MAXPOOL || layers_[k].kind == CBX_RELU)
@@ -402,7 +406,28 @@ void Engine::build_plan(Plan& p, bool baseline) {
     if (wk) {
         if (wk >= (int64_t)1 << 32) throw Error(CBX_E_ARG, "pooling work list exceeds 2^32 pixels");
         p.work = p.alloc<uint32_t>((size_t)wk);
-        p.work_count = p.alloc<int>(1);
+    }
+    // frame scratch: [stats][look-back status per conv][work counter per pool/relu]
+    size_t off = round_up(sizeof(unsigned long long) * 2 * S * nl, 256);
+    std::vector<size_t> ws_off(nl, 0), wc_off(nl, 0);
+    for (int k = 0; k < nl; ++k) {
+        if (ws_bytes[k]) {
+            ws_off[k] = off;
+            off += ws_bytes[k];
+        }
+        if (layers_[k].kind == CBX_MAXPOOL || layers_[k].kind == CBX_RELU) {
+            wc_off[k] = off;
+            off += 256;
+        }
+    }
+    p.scratch_bytes = off;
+    p.scratch = p.alloc<uint8_t>(off);
+    p.stats = reinterpret_cast<unsigned long long*>(p.scratch);
+    p.ws_k.assign(nl, nullptr);
+    p.wcount_k.assign(nl, nullptr);
+    for (int k = 0; k < nl; ++k) {
+        if (ws_bytes[k]) p.ws_k[k] = p.scratch + ws_off[k];
+        if (wc_off[k]) p.wcount_k[k] = reinterpret_cast<int*>(p.scratch + wc_off[k]);
     }
 }
 
@@ -411,7 +436,7 @@ void Engine::record(Plan& p, bool full) {
     cudaStream_t st = stream_;
     auto stats_of = [&](int layer, int field) { return p.stats + (size_t)layer * S * 2 + field; };
     if (!full) {
-        CBX_CUDA(cudaMemsetAsync(p.stats, 0, sizeof(unsigned long long) * 2 * S * nl, st));
+        CBX_CUDA(cudaMemsetAsync(p.scratch, 0, p.scratch_bytes, st));
         for (int t = 0; t <= nl; ++t)
             if (p.chg_by_conv[t] && p.chg[t].d)
                 CBX_CUDA(cudaMemsetAsync(p.chg[t].d, 0, sizeof(uint32_t) * (size_t)(p.chg[t].stride * S), st));
@@ -455,17 +480,18 @@ void Engine::record(Plan& p, bool full) {
                                            g.kernelW - 1 - g.padW <= 31 && 2 * g.padW <= g.kernelW - 1;
                         if (identity_geom(g)) {
                             const bool own = p.U[k].d != nullptr;  // CBCONV 1x1: U_k is its own mask
-                            launch_dilate_compact(src, own ? p.U[k] : src, own, S, 1, 1, 0, 0, p.idx[k], p.cnt[k], p.ws,
-                                                  cnt, 2, st);
+                            launch_dilate_compact(src, own ? p.U[k] : src, own, S, 1, 1, 0, 0, p.idx[k], p.cnt[k], p.ws_k[k],
+                                                  cnt, 2, st, true);
                             mark("compact", k);
                         } else if (fused) {
                             launch_dilate_compact(src, p.U[k], true, S, g.kernelH, g.kernelW, g.padH, g.padW, p.idx[k],
-                                                  p.cnt[k], p.ws, cnt, 2, st);
+                                                  p.cnt[k], p.ws_k[k], cnt, 2, st, true);
                             mark("dilate_compact", k);
                         } else {
                             launch_dilate_bits(src, p.U[k], S, g.kernelH, g.kernelW, g.strideH, g.strideW, g.padH, g.padW, st);
                             mark("dilate", k);
-                            launch_dilate_compact(p.U[k], p.U[k], false, S, 1, 1, 0, 0, p.idx[k], p.cnt[k], p.ws, cnt, 2, st);
+                            launch_dilate_compact(p.U[k], p.U[k], false, S, 1, 1, 0, 0, p.idx[k], p.cnt[k], p.ws_k[k], cnt, 2,
+                                                  st, true);
                             mark("compact", k);
                         }
                     }
@@ -557,7 +583,8 @@ void Engine::record(Plan& p, bool full) {
                 a.cnt_stride = 2;
                 a.S = S;
                 a.work = p.work;
-                a.work_count = p.work_count;
+                a.work_count = p.wcount_k.empty() ? nullptr : p.wcount_k[k];  // (sparse frames only)
+                a.count_zeroed = 1;
                 launch_point_bits(a, st);
                 mark(a.relu ? "relu" : "pool", k);
                 break;

@@ -311,10 +311,8 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
         const long long b = lookback(status, tile, agg);
         if (threadIdx.x == 0) {
             s_base = b;
-            if (agg) {
-                atomicAdd(total, agg);
-                if (cnt) atomicAdd(cnt + (int64_t)s * cstride, (unsigned long long)agg);
-            }
+            if (agg && cnt) atomicAdd(cnt + (int64_t)s * cstride, (unsigned long long)agg);
+            if (tile == gridDim.x - 1) *total = (int)(b + agg);  // the last tile holds the inclusive total
         }
     }
     __syncthreads();
@@ -359,7 +357,7 @@ static void launch_dc(BitMask in, BitMask out, bool write_out, int S, int kh, in
 
 void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw,
                            int32_t* idx, int* total, void* workspace, unsigned long long* cnt, int cstride,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool ws_zeroed) {
     unsigned long long* status = reinterpret_cast<unsigned long long*>(workspace);
     const bool identity = kh == 1 && kw == 1 && ph == 0 && pw == 0;
     const int64_t words = (int64_t)S * out.stride;
@@ -367,8 +365,7 @@ void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int k
     int wpt = 8;
     while (wpt > 1 && words / (kDcThreads * wpt) < 2 * kNumSMs) wpt /= 2;
     const int64_t tiles = words / (kDcThreads * wpt);
-    cudaMemsetAsync(workspace, 0, tiles * 8 + 16, st);
-    cudaMemsetAsync(total, 0, sizeof(int), st);
+    if (!ws_zeroed) cudaMemsetAsync(workspace, 0, tiles * 8 + 16, st);
     switch (wpt) {
         case 8: launch_dc<8>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st); break;
         case 4: launch_dc<4>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st); break;
@@ -588,7 +585,7 @@ void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
         point_work_kernel<true><<<grid, kPtThreads, 0, st>>>(a);
         return;
     }
-    cudaMemsetAsync(a.work_count, 0, sizeof(int), st);
+    if (!a.count_zeroed) cudaMemsetAsync(a.work_count, 0, sizeof(int), st);
     const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>((nseg + kPtThreads - 1) / kPtThreads, (int64_t)kNumSMs * 8));
     point_scan_kernel<<<g1, kPtThreads, 0, st>>>(a);
     point_work_kernel<false><<<kNumSMs * 8, kPtThreads, 0, st>>>(a);

@@ -24,9 +24,11 @@ void launch_compact(MaskView m, int S, int32_t* idx, int* total, void* workspace
 void launch_detect_bits(const float* const* cur, const float* const* prev, int S, int C, int H, int W, float tau,
                         int mode, BitMask m, unsigned long long* cnt, int cstride, cudaStream_t st);
 size_t dilate_compact_workspace(const BitMask& out, int S);
+// ws_zeroed: the caller zeroed `workspace` (the look-back status words) in
+// the same stream, e.g. with the frame's single scratch memset.
 void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw,
                            int32_t* idx, int* total, void* workspace, unsigned long long* cnt, int cstride,
-                           cudaStream_t st);
+                           cudaStream_t st, bool ws_zeroed = false);
 void launch_dilate_bits(BitMask in, BitMask out, int S, int kh, int kw, int sh, int sw, int ph, int pw,
                         cudaStream_t st);
 
@@ -42,6 +44,7 @@ struct PointBitsArgs {  // MAXPOOL (window/stride) or RELU (relu=1, window=strid
     int S;
     uint32_t* work;   // touched-pixel list s*Ho*Wo + y*Wo + x (capacity S*Ho*Wo), sparse mode only
     int* work_count;
+    int count_zeroed;  // work_count already zeroed in-stream (frame scratch memset)
 };
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st);
 void launch_classify_bits(TensorView in, BitMask upd, uint16_t* labels, int S, cudaStream_t st);
