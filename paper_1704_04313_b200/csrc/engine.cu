@@ -672,9 +672,10 @@ void Engine::forward_host(int engine, const float* frames, uint16_t* labels, cbx
 }
 
 void Engine::forward_device(int engine, const float* const* frames_dev) {
-    const int nl = (int)layers_.size();
-    enqueue(engine, frames_dev, h_stats_ + (size_t)engine * 2 * S_ * nl);
-    pending_engine_ = engine;
+    // counters stay on the device until cbx_read_stats asks for them (the
+    // frame scratch holds the last frame's counters until the next frame)
+    enqueue(engine, frames_dev, nullptr);
+    stats_pending_[engine] = true;
 }
 
 // Enqueues one frame on the context stream (pointer table, graph, counter
@@ -688,7 +689,9 @@ bool Engine::enqueue(int engine, const float* const* frames_dev, unsigned long l
     stage_frame_pointers(engine, frames_dev, engine == CBX_ENGINE_CBINFER && has_history_ ? last_cb_frames_.data() : nullptr);
     launch(p, full);
     const int nl = (int)layers_.size();
-    CBX_CUDA(cudaMemcpyAsync(stats_dst, p.stats, sizeof(unsigned long long) * 2 * S_ * nl, cudaMemcpyDeviceToHost, stream_));
+    if (stats_dst)
+        CBX_CUDA(cudaMemcpyAsync(stats_dst, p.stats, sizeof(unsigned long long) * 2 * S_ * nl, cudaMemcpyDeviceToHost,
+                                 stream_));
     last_full_[engine] = full;
     if (engine == CBX_ENGINE_CBINFER) {
         has_history_ = true;
@@ -792,10 +795,16 @@ void Engine::stats_from(const unsigned long long* hs, bool full, int engine, cbx
 }
 
 void Engine::read_stats(int engine, cbx_layer_stats* stats, uint64_t* macs) {
-    sync();
-    if (pending_engine_ == engine) {
+    if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
+    if (stats_pending_[engine]) {
+        const int nl = (int)layers_.size();
+        CBX_CUDA(cudaMemcpyAsync(h_stats_ + (size_t)engine * 2 * S_ * nl, plan(engine).stats,
+                                 sizeof(unsigned long long) * 2 * S_ * nl, cudaMemcpyDeviceToHost, stream_));
+        sync();
         finish_stats(plan(engine), last_full_[engine], engine);
-        pending_engine_ = -1;
+        stats_pending_[engine] = false;
+    } else {
+        sync();
     }
     const int nl = (int)layers_.size();
     if (stats) std::memcpy(stats, last_stats_[engine].data(), sizeof(cbx_layer_stats) * S_ * nl);
@@ -951,7 +960,8 @@ void Engine::profile(int engine, const float* const* frames_dev, std::vector<cbx
     }
     for (auto& m : marks) cudaEventDestroy(m.ev);
     last_full_[engine] = full;
-    pending_engine_ = engine;
+    finish_stats(p, full, engine);  // h_stats_ was filled above
+    stats_pending_[engine] = false;
     if (engine == CBX_ENGINE_CBINFER) {
         has_history_ = true;
         last_cb_frames_.assign(frames_dev, frames_dev + S_);

@@ -130,7 +130,7 @@ private:
     std::vector<cbx_layer_stats> last_stats_[2];
     std::vector<uint64_t> last_macs_[2];
     unsigned long long* h_stats_ = nullptr;  // pinned mirror, [engine][nl][S][2]
-    int pending_engine_ = -1;
+    bool stats_pending_[2] = {false, false};  // device counters not yet read back
     int last_launches_ = 0;
     bool last_full_[2] = {true, true};
 };
