@@ -307,6 +307,15 @@ public:
         }
         if (macsTotal) *macsTotal = macs;
     }
+    // cbench analyze-prop (cbench.cpp:242-302) for the last change-based frame:
+    // worst-case updated count of every CBCONV after the first.
+    std::vector<std::int64_t> worst_case_counts() {
+        int ncb = 0;
+        for (const auto& l : spec_.layers) ncb += l.kind == LayerKind::CBCONV;
+        std::vector<std::int64_t> w(ncb > 1 ? ncb - 1 : 0);
+        check(cbx_worst_case_counts(ctx_, w.data()), ctx_);
+        return w;
+    }
     void reset() { check(cbx_reset(ctx_), ctx_); }
     const NetworkSpec& spec() const { return spec_; }
     cbx_ctx* handle() { return ctx_; }

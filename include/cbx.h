@@ -9,6 +9,7 @@
  *                                   (+ read_weights_f32le   core/include/cbinfer/io.hpp:29)
  *   cbx_forward / _device        <- forward_frame           core/include/cbinfer/network.hpp:93-94
  *   cbx_submit / cbx_wait        <- forward_frame, pipelined (host frames; copy overlaps compute)
+ *   cbx_worst_case_counts        <- worst_case_propagation  cbconv.cpp:84-97 (cbench analyze-prop)
  *   cbx_reset                    <- reset_state             core/include/cbinfer/network.hpp:97
  *   cbx_set_thresholds           <- Network::set_thresholds core/include/cbinfer/network.hpp:67
  *   cbx_get_thresholds           <- Network::thresholds     core/include/cbinfer/network.hpp:66
@@ -163,6 +164,13 @@ CBX_API int cbx_forward_device(cbx_ctx* ctx, int engine, const float* const* fra
  * last 3 tickets can be waited on. Change-based engine only. */
 CBX_API int cbx_submit(cbx_ctx* ctx, int engine, const float* frames, uint16_t* labels, int64_t* ticket);
 CBX_API int cbx_wait(cbx_ctx* ctx, int64_t ticket, cbx_layer_stats* stats, uint64_t* macs);
+/* cbench analyze-prop (tools/cbench.cpp:242-302) for the last change-based
+ * frame (not a full one): for every CBCONV k >= 1 (0-based among CBCONVs), the
+ * worst-case updated count of layer k -- the updated set of CBCONV k-1 pushed
+ * through the layers in between and dilated by layer k's geometry
+ * (worst_case_propagation / dilate_changes, cbconv.cpp:73-97) -- per stream:
+ * worst[s * (numCB - 1) + k - 1]. Compare with changedOutputPixels of layer k. */
+CBX_API int cbx_worst_case_counts(cbx_ctx* ctx, int64_t* worst);
 CBX_API int cbx_sync(cbx_ctx* ctx);
 CBX_API int cbx_read_labels(cbx_ctx* ctx, int engine, uint16_t* labels);
 CBX_API int cbx_read_stats(cbx_ctx* ctx, int engine, cbx_layer_stats* stats, uint64_t* macs);

@@ -396,6 +396,16 @@ class Network:
                       gemmMacs=stats[s * self.nl + k].gemmMacs) for k in range(self.nl)]
                 for s in range(S)], list(macs)
 
+    def worst_case_counts(self) -> np.ndarray:
+        """cbench analyze-prop (cbench.cpp:242-302) on the device for the last
+        change-based frame: [S, numCB-1] worst-case updated counts of CBCONV
+        layers 1.. (the previous CB layer's updated set pushed through the
+        layers in between, worst_case_propagation cbconv.cpp:84-97)."""
+        ncb = len(self.spec.cb_layers())
+        out = np.zeros((self.streams, max(0, ncb - 1)), np.int64)
+        self._chk(lib.cbx_worst_case_counts(self._h, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out
+
     def forward_frame(self, frame: np.ndarray, engine: str = "cbinfer") -> ForwardResult:
         return self.forward(frame, engine)[0]
 

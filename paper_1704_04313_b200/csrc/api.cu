@@ -167,6 +167,10 @@ CBX_API int cbx_wait(cbx_ctx* ctx, int64_t ticket, cbx_layer_stats* stats, uint6
     return guarded(ctx, [&] { E(ctx).wait(ticket, stats, macs); });
 }
 
+CBX_API int cbx_worst_case_counts(cbx_ctx* ctx, int64_t* worst) {
+    return guarded(ctx, [&] { E(ctx).worst_case_counts(worst); });
+}
+
 CBX_API int cbx_sync(cbx_ctx* ctx) {
     return guarded(ctx, [&] { E(ctx).sync(); });
 }

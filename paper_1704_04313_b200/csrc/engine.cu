@@ -1003,6 +1003,69 @@ int Engine::tail_end(int k) const {
     return nl - 1;
 }
 
+// cbench analyze-prop (tools/cbench.cpp:242-302) on the device: for every
+// CBCONV k >= 1, the previous CBCONV's updated set (its U mask of the last
+// frame) pushed through the layers in between (MAXPOOL: pooling support,
+// CONV: its receptive field, RELU: unchanged) and dilated by layer k's
+// geometry -- worst_case_propagation / dilate_changes (cbconv.cpp:73-97) --
+// counted per stream. worst[s * (ncb - 1) + (k - 1)].
+void Engine::worst_case_counts(int64_t* worst) {
+    const int ncb = (int)cb_layers_.size();
+    if (ncb < 2) throw Error(CBX_E_SPEC, "analyze-prop needs at least two CBCONV layers");
+    if (!has_history_ || last_full_[CBX_ENGINE_CBINFER])
+        throw Error(CBX_E_ARG, "analyze-prop: the last change-based frame was a full evaluation (no propagation)");
+    if (!worst) throw Error(CBX_E_ARG, "null output");
+    CBX_CUDA(cudaSetDevice(device_));
+    Plan& p = *cb_;
+    std::vector<void*> tmp;
+    auto mask = [&](int H, int W) {
+        const int wpr = (W + 31) / 32;
+        BitMask m{nullptr, H, W, wpr, round_up((int64_t)H * wpr, 2048)};
+        m.d = dmalloc<uint32_t>((size_t)(m.stride * S_));
+        tmp.push_back(m.d);
+        return m;
+    };
+    unsigned long long* cnt = dmalloc<unsigned long long>((size_t)S_ * (ncb - 1));
+    tmp.push_back(cnt);
+    try {
+        CBX_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * S_ * (ncb - 1), stream_));
+        for (int k = 1; k < ncb; ++k) {
+            const int prev = cb_layers_[k - 1], next = cb_layers_[k];
+            BitMask wave = p.U[prev];
+            for (int li = prev + 1; li < next; ++li) {
+                const auto& l = layers_[li];
+                const int Ho = dims_[6 * li + 4], Wo = dims_[6 * li + 5];
+                if (l.kind == CBX_MAXPOOL) {
+                    BitMask o = mask(Ho, Wo);
+                    launch_dilate_bits(wave, o, S_, l.window, l.window, l.stride, l.stride, 0, 0, stream_);
+                    wave = o;
+                } else if (l.kind == CBX_CONV) {
+                    const cbx_geom& g = l.geom;
+                    BitMask o = mask(Ho, Wo);
+                    launch_dilate_bits(wave, o, S_, g.kernelH, g.kernelW, g.strideH, g.strideW, g.padH, g.padW, stream_);
+                    wave = o;
+                }
+            }
+            const cbx_geom& g = layers_[next].geom;
+            BitMask w = mask(dims_[6 * next + 4], dims_[6 * next + 5]);
+            launch_dilate_bits(wave, w, S_, g.kernelH, g.kernelW, g.strideH, g.strideW, g.padH, g.padW, stream_);
+            for (int s = 0; s < S_; ++s) {
+                BitMask one = w;
+                one.d = w.d + (int64_t)s * w.stride;
+                launch_popcount_bits(one, 1, cnt + (size_t)s * (ncb - 1) + (k - 1), stream_);
+            }
+        }
+        std::vector<unsigned long long> h((size_t)S_ * (ncb - 1));
+        CBX_CUDA(cudaMemcpyAsync(h.data(), cnt, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, stream_));
+        CBX_CUDA(cudaStreamSynchronize(stream_));
+        for (size_t i = 0; i < h.size(); ++i) worst[i] = (int64_t)h[i];
+    } catch (...) {
+        for (void* q : tmp) cudaFree(q);
+        throw;
+    }
+    for (void* q : tmp) cudaFree(q);
+}
+
 void Engine::set_option(int option, int value) {
     if (option == CBX_OPT_TC_PAIR) {
         if (value < -1 || value > 1) throw Error(CBX_E_ARG, "CBX_OPT_TC_PAIR takes -1, 0 or 1");

@@ -60,6 +60,7 @@ public:
     const uint16_t* labels_device(int engine);
     void get_activation(int engine, int layer, int s, float* out);
     void get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64_t* n, int* first);
+    void worst_case_counts(int64_t* worst);
 
     void profile(int engine, const float* const* frames_dev, std::vector<cbx_kernel_time>& out);
     void set_option(int option, int value);

@@ -620,6 +620,23 @@ void launch_classify_bits(TensorView in, BitMask upd, uint16_t* labels, int S, c
     classify_bits_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(in, upd, labels, S);
 }
 
+// Per-stream number of set bits of a mask (analyze-prop worst-case counts).
+__global__ void popcount_bits_kernel(BitMask m, unsigned long long* out) {
+    const int s = blockIdx.y;
+    const int64_t nw = (int64_t)m.H * m.wpr;
+    unsigned long long c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x)
+        c += __popc(m.d[(int64_t)s * m.stride + i]);
+    c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out + s, c);
+}
+
+void launch_popcount_bits(BitMask m, int S, unsigned long long* out, cudaStream_t st) {
+    const int64_t nw = (int64_t)m.H * m.wpr;
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, 256));
+    popcount_bits_kernel<<<dim3(gx, S), 256, 0, st>>>(m, out);
+}
+
 // Unpacks one stream of a bit mask into bytes (trace readback).
 __global__ void unpack_bits_kernel(BitMask m, int s, uint8_t* out) {
     const int64_t n = (int64_t)m.H * m.W;

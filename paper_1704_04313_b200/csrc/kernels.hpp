@@ -49,6 +49,8 @@ struct PointBitsArgs {  // MAXPOOL (window/stride) or RELU (relu=1, window=strid
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st);
 void launch_classify_bits(TensorView in, BitMask upd, uint16_t* labels, int S, cudaStream_t st);
 void launch_unpack_bits(BitMask m, int s, uint8_t* out, cudaStream_t st);
+// out[s] += number of set bits of stream s (out zeroed by the caller)
+void launch_popcount_bits(BitMask m, int S, unsigned long long* out, cudaStream_t st);
 
 // ---- k_layers.cu ----
 // Gathered convolution over an output-pixel list (or all pixels when idx is

@@ -61,3 +61,27 @@ def test_cpp_tool_matches_oracle(tool, tmp_path, orc):
         assert got == exp
         lab = want["labels"].reshape(-1).astype(np.uint64)
         assert int(row[-1]) == int((lab * (np.arange(lab.size) % 9973 + 1)).sum())
+
+
+@pytest.mark.gpu
+def test_cpp_tool_analyze_prop(tool, tmp_path, orc):
+    """cbx_run --mode analyze-prop (cbench analyze-prop, cbench.cpp:242-302):
+    one row per steady frame and CBCONV layer k >= 2; detected counts equal the
+    oracle's updated counts, worst-case counts bound them."""
+    spec = paper_spec(48, 64)
+    cfg = dict(channels=3, height=48, width=64, sprites=[(10, 2, 0.9)], noise=0.01, seed=3)
+    net, wdir, seq = write_case(tmp_path, orc, spec, 1, cfg, 4)
+    r = subprocess.run([tool, "--net", net, "--weights", wdir, "--seq", seq, "--precision", "exact",
+                        "--mode", "analyze-prop"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    assert lines[0] == "frameIndex,layer,detectedCount,worstCaseCount,detectedFraction,worstCaseFraction"
+    rows = [l.split(",") for l in lines[1:]]
+    assert [(int(a[0]), int(a[1])) for a in rows] == [(f, k) for f in (1, 2, 3) for k in (2, 3)]
+    onet = orc.load_network(spec, orc.generate_weights(spec, 1))
+    cb = [k for k, l in enumerate(spec["layers"]) if l["kind"] == "CBCONV"]
+    stats = [onet.forward_frame(orc.synth_frame(cfg, f))["stats"] for f in range(4)]
+    for row in rows:
+        f, k = int(row[0]), int(row[1])
+        assert int(row[2]) == stats[f][cb[k - 1]]["changedOutputPixels"]
+        assert int(row[3]) >= int(row[2])

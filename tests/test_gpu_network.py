@@ -215,3 +215,58 @@ def test_submit_wait_pipelined(gpu, orc, precision):
         pipe.wait(tickets[0])  # expired: only the last 3 submissions can be waited on
     with pytest.raises(gpu.CbxError):
         pipe.wait(F + 5)
+
+
+def _oracle_worst_counts(orc, spec, onet):
+    """cbench analyze-prop (cbench.cpp:242-302) restated with the oracle's ops on
+    the oracle's own trace of the last frame."""
+    from oracle import make_geom
+    dims, _ = orc.chain_dims(spec)
+    cb = [k for k, l in enumerate(spec["layers"]) if l["kind"] == "CBCONV"]
+    out = []
+    for j in range(1, len(cb)):
+        prev, nxt = cb[j - 1], cb[j]
+        _, upd = onet.trace(j - 1)
+        (_, h, w) = dims[prev][1]
+        wave = np.zeros(h * w, np.uint8)
+        wave[upd] = 1
+        wave = wave.reshape(h, w)
+        for li in range(prev + 1, nxt):
+            l = spec["layers"][li]
+            if l["kind"] == "MAXPOOL":
+                wave = orc.dilate_changes(wave, make_geom(l["window"], l["stride"], 0))
+            elif l["kind"] == "CONV":
+                wave = orc.dilate_changes(wave, make_geom(l["kernelH"], l.get("strideH", 1), l.get("padH", 0),
+                                                          kw=l["kernelW"], stride_w=l.get("strideW", 1),
+                                                          pad_w=l.get("padW", 0)))
+        l = spec["layers"][nxt]
+        g = make_geom(l["kernelH"], l.get("strideH", 1), l.get("padH", 0), kw=l["kernelW"],
+                      stride_w=l.get("strideW", 1), pad_w=l.get("padW", 0))
+        out.append(int(orc.dilate_changes(wave, g).sum()))
+    return out
+
+
+@pytest.mark.parametrize("name,spec,cfg", [
+    ("paper", paper_spec(64, 96), dict(channels=3, height=64, width=96, sprites=[(12, 3, 0.9)], noise=0.01, seed=3)),
+    ("generic", generic_spec(), dict(channels=3, height=37, width=45, sprites=[(6, 2, 0.8)], noise=0.015, seed=9)),
+])
+def test_worst_case_counts(gpu, orc, name, spec, cfg):
+    """analyze-prop worst-case counts on the device == the oracle restatement,
+    and never below the actual updated counts (the superset property)."""
+    w = orc.generate_weights(spec, 1)
+    onet = orc.load_network(spec, w)
+    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="exact")
+    net.forward_frame(orc.synth_frame(cfg, 0))
+    onet.forward_frame(orc.synth_frame(cfg, 0))
+    with pytest.raises(gpu.CbxError):
+        net.worst_case_counts()  # first frame: full evaluation, nothing propagated
+    cb = net.spec.cb_layers()
+    for f in range(1, 4):
+        fr = orc.synth_frame(cfg, f)
+        got_frame = net.forward_frame(fr)
+        onet.forward_frame(fr)
+        worst = net.worst_case_counts()
+        assert worst.shape == (1, len(cb) - 1)
+        assert list(worst[0]) == _oracle_worst_counts(orc, spec, onet), (name, f)
+        for j in range(1, len(cb)):
+            assert worst[0, j - 1] >= got_frame.stats[cb[j]]["changedOutputPixels"]

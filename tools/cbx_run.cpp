@@ -5,6 +5,11 @@
 //
 //   cbx_run --net spec.json --weights DIR [--seq DIR | --synth C,H,W,N,SIZE,VEL,SEED]
 //           [--engine cbinfer|baseline] [--precision tf32|exact] [--thresholds a,b,c]
+//           [--mode run|analyze-prop]
+//
+// --mode analyze-prop is the counterpart of `cbench analyze-prop`
+// (cbench.cpp:242-302): per steady frame and CBCONV layer k >= 2, the actual
+// updated count next to the worst case propagated from layer k-1.
 //
 // --seq reads frame_%04d.f32le + manifest.json (synth.cpp:130-186 layout).
 #include <chrono>
@@ -28,7 +33,7 @@ static std::vector<float> parse_floats(const std::string& s) {
 }
 
 int main(int argc, char** argv) {
-    std::string net_path, wdir, seq, synth, engine = "cbinfer", precision = "tf32", taus;
+    std::string net_path, wdir, seq, synth, engine = "cbinfer", precision = "tf32", taus, mode = "run";
     for (int i = 1; i + 1 < argc; i += 2) {
         const std::string k = argv[i], v = argv[i + 1];
         if (k == "--net") net_path = v;
@@ -38,6 +43,7 @@ int main(int argc, char** argv) {
         else if (k == "--engine") engine = v;
         else if (k == "--precision") precision = v;
         else if (k == "--thresholds") taus = v;
+        else if (k == "--mode") mode = v;
         else {
             std::cerr << "unknown option " << k << "\n";
             return 1;
@@ -76,6 +82,29 @@ int main(int argc, char** argv) {
                 frames.push_back(std::move(t));
             }
         }
+        if (mode == "analyze-prop") {
+            std::vector<size_t> cbl;
+            for (size_t k = 0; k < spec.layers.size(); ++k)
+                if (spec.layers[k].kind == cb::LayerKind::CBCONV) cbl.push_back(k);
+            if (cbl.size() < 2) throw cb::spec_error("analyze-prop needs at least two CBCONV layers");
+            const auto dims = cb::chain_dims(spec);
+            std::cout << "frameIndex,layer,detectedCount,worstCaseCount,detectedFraction,worstCaseFraction\n";
+            for (size_t f = 0; f < frames.size(); ++f) {
+                cb::ForwardResult r = cb::forward_frame(net, frames[f], cb::Engine::CBInfer);
+                if (f == 0) continue;  // full evaluation, no propagation to compare
+                const auto worst = net.worst_case_counts();
+                for (size_t k = 1; k < cbl.size(); ++k) {
+                    const double grid = double(dims[cbl[k]].out.height) * dims[cbl[k]].out.width;
+                    const long long det = (long long)r.stats[cbl[k]].changedOutputPixels;
+                    char buf[160];
+                    std::snprintf(buf, sizeof(buf), "%d,%zu,%lld,%lld,%.9g,%.9g", int(f), k + 1, det,
+                                  (long long)worst[k - 1], 100.0 * det / grid, 100.0 * double(worst[k - 1]) / grid);
+                    std::cout << buf << "\n";
+                }
+            }
+            return 0;
+        }
+        if (mode != "run") throw cb::spec_error("unknown --mode " + mode);
         std::cout << "frame,wallNanos,macsTotal";
         for (size_t k = 0; k < spec.layers.size(); ++k)
             if (spec.layers[k].kind == cb::LayerKind::CBCONV) std::cout << ",changedIn" << k + 1 << ",changedOut" << k + 1;
