@@ -307,6 +307,14 @@ public:
         }
         if (macsTotal) *macsTotal = macs;
     }
+    // Output activation of `layer` (0-based) after the last change-based frame,
+    // planar CHW like the reference's tensors (ForwardTrace, network.hpp:80-83).
+    std::vector<float> activation(int layer) {
+        const auto& sh = shapes_.at(size_t(layer)).out;
+        std::vector<float> out(size_t(sh.channels) * sh.height * sh.width);
+        check(cbx_get_activation(ctx_, static_cast<int>(Engine::CBInfer), layer, 0, out.data()), ctx_);
+        return out;
+    }
     // cbench analyze-prop (cbench.cpp:242-302) for the last change-based frame:
     // worst-case updated count of every CBCONV after the first.
     std::vector<std::int64_t> worst_case_counts() {

@@ -559,6 +559,29 @@ class RefNet:
                       gemmMacs=st[3 * k + 2]) for k in range(self.nl)]
         return dict(labels=labels, stats=stats, macsTotal=macs.value)
 
+    def calibrate(self, frames, grid_size=16, budget=1.0):
+        """Reference default_threshold_grids + calibrate_thresholds over one
+        sequence (calibration.cpp:73-170): (thresholds, [(layer, tau, err)])."""
+        fr = np.ascontiguousarray(np.stack(frames), np.float32)
+        ncb = sum(l["kind"] == "CBCONV" for l in self.spec["layers"])
+        th = (C.c_float * max(1, ncb))()
+        n = ncb * grid_size
+        lay, tau, err = (C.c_int * n)(), (C.c_float * n)(), (C.c_double * n)()
+        self.ref._chk(self.lib.ref_calibrate(self.h, fr.ctypes.data_as(C.POINTER(C.c_float)), len(frames),
+                                             int(grid_size), C.c_double(budget), th, lay, tau, err))
+        return [th[k] for k in range(ncb)], [(lay[i], tau[i], err[i]) for i in range(n)]
+
+    def sweep(self, frames, factors):
+        """Reference sweep_threshold_factor over one sequence
+        (calibration.cpp:172-240): [(errorIncrease, changedPixelsTotal, macsTotal)]."""
+        fr = np.ascontiguousarray(np.stack(frames), np.float32)
+        nf = len(factors)
+        fa = (C.c_double * nf)(*factors)
+        err, ch, macs = (C.c_double * nf)(), (C.c_int64 * nf)(), (C.c_uint64 * nf)()
+        self.ref._chk(self.lib.ref_sweep(self.h, fr.ctypes.data_as(C.POINTER(C.c_float)), len(frames), fa, nf,
+                                         err, ch, macs))
+        return [(err[i], ch[i], macs[i]) for i in range(nf)]
+
     def warm(self, frame, nthreads):
         frame, pf = _f32(frame)
         self.ref._chk(self.lib.ref_net_warm(self.h, pf, int(nthreads)))

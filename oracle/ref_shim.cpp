@@ -16,6 +16,7 @@
 #include "cbinfer/baseline.hpp"
 #include "cbinfer/cbconv.hpp"
 #include "cbinfer/error.hpp"
+#include "cbinfer/calibration.hpp"
 #include "cbinfer/network.hpp"
 #include "cbinfer/synth.hpp"
 
@@ -288,6 +289,54 @@ int ref_net_trace(void* h, int cb, const uint8_t** detected, int* dims, const in
     *updated = t.updated.indices.data();
     *n = t.updated.count();
     return 0;
+}
+
+// calibration.cpp over one sequence of nframes frames (no ground truth):
+// default_threshold_grids(gridSize) + calibrate_thresholds(budget).
+// thresholds[ncb]; sweep arrays of ncb*gridSize entries (layer, tau, err).
+int ref_calibrate(void* h, const float* frames, int nframes, int gridSize, double budget, float* thresholds,
+                  int* sweepLayer, float* sweepTau, double* sweepErr) {
+    GUARD({
+        auto* r = static_cast<RefNet*>(h);
+        const auto& s = r->net.spec;
+        std::vector<Sequence> seqs(1);
+        seqs[0].name = "seq";
+        const size_t per = (size_t)s.inputChannels * s.inputHeight * s.inputWidth;
+        for (int f = 0; f < nframes; ++f)
+            seqs[0].frames.push_back(to_tensor(frames + per * f, s.inputChannels, s.inputHeight, s.inputWidth));
+        const auto grids = default_threshold_grids(r->net, seqs, gridSize);
+        const auto res = calibrate_thresholds(r->net, seqs, grids, budget);
+        for (size_t k = 0; k < res.thresholds.size(); ++k) thresholds[k] = res.thresholds[k];
+        for (size_t i = 0; i < res.sweep.size(); ++i) {
+            sweepLayer[i] = res.sweep[i].layer;
+            sweepTau[i] = res.sweep[i].threshold;
+            sweepErr[i] = res.sweep[i].errorIncrease;
+        }
+        return 0;
+    })
+}
+
+// sweep_threshold_factor over one sequence; per factor: errorIncrease,
+// changedPixelsTotal, macsTotal (framesPerSecond is wall-clock, not compared).
+int ref_sweep(void* h, const float* frames, int nframes, const double* factors, int nf, double* err,
+              int64_t* changed, uint64_t* macs) {
+    GUARD({
+        auto* r = static_cast<RefNet*>(h);
+        const auto& s = r->net.spec;
+        std::vector<Sequence> seqs(1);
+        seqs[0].name = "seq";
+        const size_t per = (size_t)s.inputChannels * s.inputHeight * s.inputWidth;
+        for (int f = 0; f < nframes; ++f)
+            seqs[0].frames.push_back(to_tensor(frames + per * f, s.inputChannels, s.inputHeight, s.inputWidth));
+        const auto pts = sweep_threshold_factor(r->net, seqs, r->net.thresholds(),
+                                                std::vector<double>(factors, factors + nf));
+        for (int i = 0; i < nf; ++i) {
+            err[i] = pts[i].errorIncrease;
+            changed[i] = pts[i].changedPixelsTotal;
+            macs[i] = pts[i].macsTotal;
+        }
+        return 0;
+    })
 }
 
 }  // extern "C"

@@ -85,3 +85,49 @@ def test_cpp_tool_analyze_prop(tool, tmp_path, orc):
         f, k = int(row[0]), int(row[1])
         assert int(row[2]) == stats[f][cb[k - 1]]["changedOutputPixels"]
         assert int(row[3]) >= int(row[2])
+
+
+needs_ref = pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libcbinfer_ref.so")),
+                               reason="oracle/_ref not built")
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_cpp_tool_calibrate_and_sweep_match_reference(tool, tmp_path):
+    """cbx_run --mode calibrate / sweep (cbench calibrate / sweep over the B200
+    engine, exact mode) reproduce the reference's own calibrate_thresholds and
+    sweep_threshold_factor on the same sequence: same grids, chosen thresholds,
+    per-candidate error, changed-pixel and MAC totals."""
+    from oracle import Ref
+    spec = paper_spec(40, 56)
+    cfg = dict(channels=3, height=40, width=56, sprites=[(9, 2, 0.9)], noise=0.004, seed=5)
+    from oracle import Oracle
+    orc = Oracle()
+    net, wdir, seq = write_case(tmp_path, orc, spec, 1, cfg, 5)
+    frames = [orc.synth_frame(cfg, f) for f in range(5)]
+    ref = Ref()
+    rnet = ref.load_network(spec, 1, weights_dir=wdir)
+    want_th, want_sweep = rnet.calibrate(frames, grid_size=6, budget=0.5)
+    r = subprocess.run([tool, "--net", net, "--weights", wdir, "--seq", seq, "--precision", "exact",
+                        "--mode", "calibrate", "--grid", "6", "--budget", "0.5"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    assert lines[0] == "layer,threshold,errorIncrease"
+    got = [l.split(",") for l in lines[1:-1]]
+    assert [(int(a), np.float32(b)) for a, b, _ in got] == [(l, np.float32(t)) for l, t, _ in want_sweep]
+    np.testing.assert_allclose([float(c) for _, _, c in got], [e for _, _, e in want_sweep], rtol=0, atol=1e-7)
+    assert lines[-1] == "thresholds: " + ",".join("%.9g" % t for t in want_th)
+
+    factors = [0.0, 0.5, 1.0, 2.0]
+    rnet.set_thresholds([0.04, 0.05, 0.05])
+    want = rnet.sweep(frames, factors)
+    r = subprocess.run([tool, "--net", net, "--weights", wdir, "--seq", seq, "--precision", "exact",
+                        "--mode", "sweep", "--thresholds", "0.04,0.05,0.05", "--factors", "0,0.5,1,2"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    rows = [l.split(",") for l in r.stdout.strip().splitlines()[1:]]
+    assert len(rows) == len(factors)
+    for row, (err, ch, macs) in zip(rows, want):
+        assert abs(float(row[2]) - err) <= 1e-7
+        assert int(row[3]) == ch and int(row[5]) == macs

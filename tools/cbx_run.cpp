@@ -5,11 +5,13 @@
 //
 //   cbx_run --net spec.json --weights DIR [--seq DIR | --synth C,H,W,N,SIZE,VEL,SEED]
 //           [--engine cbinfer|baseline] [--precision tf32|exact] [--thresholds a,b,c]
-//           [--mode run|analyze-prop]
+//           [--mode run|analyze-prop|sweep|calibrate] [--factors f1,f2,...] [--budget PCT] [--grid N]
 //
 // --mode analyze-prop is the counterpart of `cbench analyze-prop`
 // (cbench.cpp:242-302): per steady frame and CBCONV layer k >= 2, the actual
 // updated count next to the worst case propagated from layer k-1.
+// --mode sweep / calibrate are `cbench sweep` / `cbench calibrate`
+// (cbench.cpp:174-240) over cbinfer_b200_calibration.hpp.
 //
 // --seq reads frame_%04d.f32le + manifest.json (synth.cpp:130-186 layout).
 #include <chrono>
@@ -21,6 +23,7 @@
 #include <vector>
 
 #include "cbinfer_b200.hpp"
+#include "cbinfer_b200_calibration.hpp"
 
 namespace cb = cbinfer_b200;
 
@@ -34,6 +37,9 @@ static std::vector<float> parse_floats(const std::string& s) {
 
 int main(int argc, char** argv) {
     std::string net_path, wdir, seq, synth, engine = "cbinfer", precision = "tf32", taus, mode = "run";
+    std::string factors = "0,0.25,0.5,0.75,1,1.25,1.5,1.75,2";
+    double budget = 1.0;
+    int gridSize = 16;
     for (int i = 1; i + 1 < argc; i += 2) {
         const std::string k = argv[i], v = argv[i + 1];
         if (k == "--net") net_path = v;
@@ -44,6 +50,9 @@ int main(int argc, char** argv) {
         else if (k == "--precision") precision = v;
         else if (k == "--thresholds") taus = v;
         else if (k == "--mode") mode = v;
+        else if (k == "--factors") factors = v;
+        else if (k == "--budget") budget = std::stod(v);
+        else if (k == "--grid") gridSize = std::stoi(v);
         else {
             std::cerr << "unknown option " << k << "\n";
             return 1;
@@ -101,6 +110,39 @@ int main(int argc, char** argv) {
                                   (long long)worst[k - 1], 100.0 * det / grid, 100.0 * double(worst[k - 1]) / grid);
                     std::cout << buf << "\n";
                 }
+            }
+            return 0;
+        }
+        if (mode == "sweep" || mode == "calibrate") {
+            std::vector<cb::Sequence> seqs(1);
+            seqs[0].name = seq.empty() ? std::string("synth") : seq;
+            seqs[0].frames = std::move(frames);
+            char buf[192];
+            if (mode == "sweep") {
+                std::vector<double> fs;
+                for (float f : parse_floats(factors)) fs.push_back(f);
+                const auto pts = cb::sweep_threshold_factor(net, seqs, net.thresholds(), fs);
+                std::cout << "sequence,factor,errorIncrease,numChangeTotal,throughput,macsTotal\n";
+                for (const auto& p : pts) {
+                    std::snprintf(buf, sizeof(buf), "%s,%.9g,%.9g,%lld,%.9g,%llu", seqs[0].name.c_str(),
+                                  p.thresholdFactor, p.errorIncrease, (long long)p.changedPixelsTotal,
+                                  p.framesPerSecond, (unsigned long long)p.macsTotal);
+                    std::cout << buf << "\n";
+                }
+            } else {
+                const auto grids = cb::default_threshold_grids(net, seqs, gridSize);
+                const auto res = cb::calibrate_thresholds(net, seqs, grids, budget);
+                std::cout << "layer,threshold,errorIncrease\n";
+                for (const auto& p : res.sweep) {
+                    std::snprintf(buf, sizeof(buf), "%d,%.9g,%.9g", p.layer, double(p.threshold), p.errorIncrease);
+                    std::cout << buf << "\n";
+                }
+                std::string line;
+                for (size_t k = 0; k < res.thresholds.size(); ++k) {
+                    std::snprintf(buf, sizeof(buf), "%.9g", double(res.thresholds[k]));
+                    line += (k ? "," : "") + std::string(buf);
+                }
+                std::cout << "thresholds: " << line << "\n";
             }
             return 0;
         }
