@@ -90,6 +90,63 @@ __global__ void __launch_bounds__(256) detect_bits_kernel(const float* const* cu
     }
 }
 
+// K1 for 3-channel frames (the paper's RGB input), QPT pixel quads per thread:
+// all 6*QPT 128-bit loads (both frames, every plane) are issued before any
+// compare, so each thread keeps QPT*96 bytes in flight.
+template <int QPT>
+__global__ void __launch_bounds__(256) detect_c3_kernel(const float* const* cur, const float* const* prev, int H, int W,
+                                                        float tau, BitMask m, unsigned long long* cnt, int cstride) {
+    const int s = blockIdx.y;
+    const float* a = cur[s];
+    const float* b = prev[s];
+    const int HW = H * W;
+    const int qpr = m.wpr * 8;
+    const int nq = H * qpr;
+    const int lane = threadIdx.x & 31;
+    uint32_t* dst = m.d + (int64_t)s * m.stride;
+    for (int base = blockIdx.x * blockDim.x * QPT; base < nq; base += gridDim.x * blockDim.x * QPT) {
+        float4 u[QPT][3], v[QPT][3];
+        bool ok[QPT];
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+            const int q = base + k * blockDim.x + threadIdx.x;
+            const int y = q / qpr;
+            const int x0 = (q - y * qpr) * 4;
+            ok[k] = q < nq && x0 < W;
+            if (ok[k]) {
+                const int p0 = y * W + x0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    u[k][c] = __ldcs(reinterpret_cast<const float4*>(a + c * HW + p0));
+                    v[k][c] = __ldcs(reinterpret_cast<const float4*>(b + c * HW + p0));
+                }
+            }
+        }
+        int n = 0;
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+            const int q = base + k * blockDim.x + threadIdx.x;
+            uint32_t flags = 0;
+            if (ok[k]) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    flags |= (ref_changed(u[k][c].x, v[k][c].x, tau) ? 1u : 0u) | (ref_changed(u[k][c].y, v[k][c].y, tau) ? 2u : 0u) |
+                             (ref_changed(u[k][c].z, v[k][c].z, tau) ? 4u : 0u) | (ref_changed(u[k][c].w, v[k][c].w, tau) ? 8u : 0u);
+            }
+            uint32_t word = flags << (4 * (lane & 7));
+            word |= __shfl_xor_sync(0xffffffffu, word, 1);
+            word |= __shfl_xor_sync(0xffffffffu, word, 2);
+            word |= __shfl_xor_sync(0xffffffffu, word, 4);
+            if (q < nq && (lane & 7) == 0) dst[q >> 3] = word;
+            n += __popc(flags);
+        }
+        if (cnt) {
+            n = __reduce_add_sync(0xffffffffu, n);
+            if (lane == 0 && n) atomicAdd(cnt + (int64_t)s * cstride, (unsigned long long)n);
+        }
+    }
+}
+
 void launch_detect_bits(const float* const* cur, const float* const* prev, int S, int C, int H, int W, float tau,
                         int mode, BitMask m, unsigned long long* cnt, int cstride, cudaStream_t st) {
     const int64_t nq = (int64_t)H * m.wpr * 8;
@@ -99,6 +156,14 @@ void launch_detect_bits(const float* const* cur, const float* const* prev, int S
     dim3 grid(gx, S);
     // frame pointers are 16-byte aligned (engine slots; checked for user frames in forward_device)
     const bool vec = W % 4 == 0;
+    if (mode == 0 && vec && C == 3 && (int64_t)H * W < ((int64_t)1 << 31)) {
+        constexpr int QPT = 2;
+        int g3 = (int)((nq + 256 * QPT - 1) / (256 * QPT));
+        const int cap3 = (kNumSMs * 8 + S - 1) / S;
+        if (g3 > cap3) g3 = cap3 < 1 ? 1 : cap3;
+        detect_c3_kernel<QPT><<<dim3(g3, S), 256, 0, st>>>(cur, prev, H, W, tau, m, cnt, cstride);
+        return;
+    }
     if (mode == 0 && vec)
         detect_bits_kernel<0, true><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
     else if (mode == 0)
