@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="cbx", choices=["cbx", "reference"])
-    ap.add_argument("--streams", type=int, default=4, help="camera streams per GPU")
+    ap.add_argument("--streams", type=int, default=8, help="camera streams per GPU")
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--recipe", default="2.2", choices=sorted(RECIPES))
@@ -392,6 +392,28 @@ def run_gpu_arm(args):
     dense_fps = shard.aggregate_rate(ws, S * Kd, ms_d)
     log(f"[gpu] dense: {ms_d / Kd:.3f} ms/step, {dense_fps:.1f} frames/s")
 
+    # BASELINE configs[2]: single-stream per-frame latency (one camera, same
+    # clip as stream 0, device-resident), median of per-frame event timings
+    lat_ms = None
+    if S > 1:
+        net1 = cbx.Network(spec, weights, device=local, streams=1, precision=args.precision)
+        st1 = torch.cuda.ExternalStream(net1.stream_handle(), device=torch.device("cuda", local))
+        p1 = lambda i: [clip[pingpong(i, F), 0].data_ptr()]
+        for i in range(0, args.warmup + 1):
+            net1.forward_device(p1(i))
+        net1.sync()
+        per = []
+        for i in range(args.warmup + 1, args.warmup + 1 + K):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st1)
+            net1.forward_device(p1(i))
+            e1.record(st1)
+            e1.synchronize()
+            per.append(e0.elapsed_time(e1))
+        lat_ms = float(np.median(per))
+        net1.close()
+        log(f"[gpu] single-stream latency: {lat_ms:.3f} ms/frame")
+
     sweep = None
     if args.sweep:
         sweep = {}
@@ -487,7 +509,8 @@ def run_gpu_arm(args):
                                    f"{3 * args.height * args.width * 4 / 1e6:.1f} MB per step)",
                        "streams_per_gpu": S, "taus": list(BASE_TAUS), "precision": args.precision,
                        "l1_input_changed": frac_in, "layer_output_changed": frac_out,
-                       "dense_fps": dense_fps, "speedup_vs_dense": value / dense_fps, "parallelism": f"streams x{ws}"},
+                       "dense_fps": dense_fps, "speedup_vs_dense": value / dense_fps, "parallelism": f"streams x{ws}",
+                       "single_stream_latency_ms": lat_ms},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * K,
             "clocks": clk,
         }
