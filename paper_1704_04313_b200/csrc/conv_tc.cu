@@ -413,12 +413,19 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             const int r = tid - kEpiThreads;
             const uint32_t swz = (uint32_t)(r & 7);
             uint32_t it = 0;
+            // the next tile's index is loaded while this tile's K-blocks are
+            // gathered, so a tile never starts with a dependent index load
+            auto row_index = [&](int64_t t) -> int64_t {
+                const int64_t n = t * kRowsPerTile + row_off + r;
+                return (t < ntiles && n < total) ? (a.idx ? (int64_t)__ldg(a.idx + n) : n) : -1;
+            };
+            int64_t gnext = row_index(tile_first);
             for (int64_t tile = tile_first; tile < ntiles; tile += tile_step) {
-                const int64_t n = tile * kRowsPerTile + row_off + r;
-                const bool valid = n < total;
+                const int64_t g = gnext;
+                gnext = row_index(tile + tile_step);
+                const bool valid = g >= 0;
                 const float* base = a.in;
                 if (valid) {
-                    const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
                     const int s = (int)(g / HoWo);
                     const int p = (int)(g - (int64_t)s * HoWo);
                     const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
@@ -452,16 +459,29 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         const uint32_t swz_off = (uint32_t)((j ^ (rsub & 7)) << 4);
         constexpr int kRowsPerThread = kTileM / 16;
         uint32_t it = 0;
+        // indices of the next tile's rows are loaded during this tile's K-loop
+        int32_t gnext[kRowsPerThread];
+        auto load_rows = [&](int64_t t) {
+#pragma unroll
+            for (int i = 0; i < kRowsPerThread; ++i) {
+                const int64_t n = t * kRowsPerTile + row_off + rsub + 16 * i;
+                gnext[i] = (t < ntiles && n < total) ? (a.idx ? __ldg(a.idx + n) : (int32_t)n) : -1;
+            }
+        };
+        load_rows(tile_first);
         for (int64_t tile = tile_first; tile < ntiles; tile += tile_step) {
             const float* base[kRowsPerThread];
             uint32_t vmask = 0;
+            int32_t gcur[kRowsPerThread];
+#pragma unroll
+            for (int i = 0; i < kRowsPerThread; ++i) gcur[i] = gnext[i];
+            load_rows(tile + tile_step);
 #pragma unroll
             for (int i = 0; i < kRowsPerThread; ++i) {
-                const int64_t n = tile * kRowsPerTile + row_off + rsub + 16 * i;
                 base[i] = a.in;
-                if (n < total) {
+                if (gcur[i] >= 0) {
                     vmask |= 1u << i;
-                    const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
+                    const int64_t g = gcur[i];
                     const int s = (int)(g / HoWo);
                     const int p = (int)(g - (int64_t)s * HoWo);
                     const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
@@ -543,14 +563,15 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         uint32_t acc_it = 0;
         for (int64_t tile = tile_first; tile < ntiles; tile += tile_step, ++acc_it) {
             const uint32_t as = acc_it % a.acc_stages, aph = (acc_it / a.acc_stages) & 1u;
-            mbar_wait(&tfull[as], aph);
-            tc_fence_after();
             const int64_t n = tile * kRowsPerTile + row_off + r;
             const bool valid = n < total;
+            // index (and output address) resolved before waiting for the accumulator
+            const int64_t g = valid ? (a.idx ? (int64_t)__ldg(a.idx + n) : n) : 0;
+            mbar_wait(&tfull[as], aph);
+            tc_fence_after();
             int s = 0, p = 0, y = 0, x = 0;
             float* dst = nullptr;
             if (valid) {
-                const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
                 s = (int)(g / HoWo);
                 p = (int)(g - (int64_t)s * HoWo);
                 y = p / a.Wo;
