@@ -108,6 +108,15 @@ CBX_API int cbx_chain_dims(const cbx_net_desc* net, cbx_layer_desc* layers_out, 
  * camera streams (each with its own change-based state). */
 CBX_API int cbx_create(const cbx_net_desc* net, int device, int num_streams, int precision,
                        cbx_ctx** out);
+/* cbx_create with an explicit lane count: the streams are split into `lanes`
+ * contiguous groups, each evaluated by its own engine on its own CUDA stream
+ * so that the groups' kernels overlap on the GPU (one group's tcgen05
+ * layer-3 conv next to another group's mask / layer-1 / pooling kernels).
+ * lanes <= 0: automatic (2 when num_streams >= 2, else 1); cbx_create uses
+ * automatic. Results are identical for any lane count. */
+CBX_API int cbx_create_ex(const cbx_net_desc* net, int device, int num_streams, int precision, int lanes,
+                          cbx_ctx** out);
+CBX_API int cbx_num_lanes(const cbx_ctx* ctx);
 CBX_API void cbx_destroy(cbx_ctx* ctx);
 
 /* Install the filters of conv layer `layer` (0-based index in the layer
@@ -174,6 +183,7 @@ CBX_API int cbx_worst_case_counts(cbx_ctx* ctx, int64_t* worst);
 CBX_API int cbx_sync(cbx_ctx* ctx);
 CBX_API int cbx_read_labels(cbx_ctx* ctx, int engine, uint16_t* labels);
 CBX_API int cbx_read_stats(cbx_ctx* ctx, int engine, cbx_layer_stats* stats, uint64_t* macs);
+/* Device labels buffer [S][Hl][Wl] (single-lane contexts only: CBX_E_ARG otherwise). */
 CBX_API int cbx_labels_device(cbx_ctx* ctx, int engine, const uint16_t** labels_dev);
 
 /* Context stream as a cudaStream_t (void* here). */

@@ -270,7 +270,7 @@ class Network:
     of reference weight files (read_weights_f32le)."""
 
     def __init__(self, spec: NetworkSpec, weights, device: int = 0, streams: int = 1,
-                 precision: str = "tf32", fuse_tail: bool = True):
+                 precision: str = "tf32", fuse_tail: bool = True, lanes: int = 0):
         self.spec = spec
         self.shapes = chain_dims(spec)
         self.streams = streams
@@ -278,7 +278,9 @@ class Network:
         self.precision = precision
         d, arr = _net_desc(spec)
         h = C.c_void_p()
-        check(lib.cbx_create(C.byref(d), device, streams, PRECISIONS[precision], C.byref(h)))
+        # lanes: independent engines over contiguous stream groups whose kernels
+        # overlap on the GPU (0 = automatic: 2 when streams >= 2)
+        check(lib.cbx_create_ex(C.byref(d), device, streams, PRECISIONS[precision], lanes, C.byref(h)))
         self._h = h
         self.nl = len(spec.layers)
         if isinstance(weights, str):
@@ -312,9 +314,10 @@ class Network:
             check(rc, lib.cbx_last_error(self._h).decode())
 
     def close(self):
-        if getattr(self, "_h", None):
+        # (at interpreter shutdown the module global `lib` may already be gone)
+        if getattr(self, "_h", None) and lib is not None:
             lib.cbx_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         self.close()
@@ -440,6 +443,9 @@ class Network:
         n = C.c_int()
         self._chk(lib.cbx_profile_forward(self._h, ENGINES[engine], arr, out, cap, C.byref(n)))
         return [dict(name=out[i].name.decode(), layer=out[i].layer, ms=out[i].ms) for i in range(min(n.value, cap))]
+
+    def num_lanes(self) -> int:
+        return lib.cbx_num_lanes(self._h)
 
     def stream_handle(self) -> int:
         return lib.cbx_stream(self._h) or 0

@@ -104,10 +104,12 @@ lib.cbx_destroy.argtypes = [VP]
 lib.cbx_submit.argtypes = [VP, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_uint16), C.POINTER(C.c_int64)]
 lib.cbx_wait.argtypes = [VP, C.c_int64, VP, VP]
 lib.cbx_worst_case_counts.argtypes = [VP, C.POINTER(C.c_int64)]
+lib.cbx_num_lanes.argtypes = [VP]
 
 # exported symbols declared in include/cbx.h (checked by tests without a GPU)
 EXPORTS = [
-    "cbx_last_error", "cbx_version", "cbx_chain_dims", "cbx_create", "cbx_destroy", "cbx_load_layer",
+    "cbx_last_error", "cbx_version", "cbx_chain_dims", "cbx_create", "cbx_create_ex", "cbx_num_lanes", "cbx_destroy",
+    "cbx_load_layer",
     "cbx_set_thresholds", "cbx_get_thresholds", "cbx_set_option", "cbx_reset", "cbx_forward", "cbx_forward_device",
     "cbx_submit", "cbx_wait", "cbx_worst_case_counts", "cbx_sync", "cbx_read_labels", "cbx_read_stats", "cbx_labels_device", "cbx_stream",
     "cbx_last_launch_count", "cbx_profile_forward", "cbx_get_activation", "cbx_get_trace", "cbx_op_detect", "cbx_op_dilate",

@@ -9,11 +9,12 @@
 #include <vector>
 
 #include "../../include/cbx.h"
+#include "context.hpp"
 #include "engine.hpp"
 #include "kernels.hpp"
 
 struct cbx_ctx {
-    cbx::Engine* eng = nullptr;
+    cbx::Context* eng = nullptr;
     std::string err;
 };
 
@@ -38,7 +39,7 @@ int guarded(cbx_ctx* ctx, F&& f) {
     }
 }
 
-cbx::Engine& E(cbx_ctx* c) {
+cbx::Context& E(cbx_ctx* c) {
     if (!c || !c->eng) throw cbx::Error(CBX_E_ARG, "null context");
     return *c->eng;
 }
@@ -106,13 +107,15 @@ CBX_API int cbx_chain_dims(const cbx_net_desc* net, cbx_layer_desc* layers_out, 
     });
 }
 
-CBX_API int cbx_create(const cbx_net_desc* net, int device, int num_streams, int precision, cbx_ctx** out) {
+CBX_API int cbx_create_ex(const cbx_net_desc* net, int device, int num_streams, int precision, int lanes,
+                          cbx_ctx** out) {
     return guarded(nullptr, [&] {
         if (!net || !out) throw cbx::Error(CBX_E_ARG, "null argument");
         *out = nullptr;
+        if (lanes <= 0) lanes = num_streams >= 2 ? 2 : 1;
         auto* c = new cbx_ctx;
         try {
-            c->eng = new cbx::Engine(*net, device, num_streams, precision);
+            c->eng = new cbx::Context(*net, device, num_streams, precision, lanes);
         } catch (...) {
             delete c;
             throw;
@@ -120,6 +123,12 @@ CBX_API int cbx_create(const cbx_net_desc* net, int device, int num_streams, int
         *out = c;
     });
 }
+
+CBX_API int cbx_create(const cbx_net_desc* net, int device, int num_streams, int precision, cbx_ctx** out) {
+    return cbx_create_ex(net, device, num_streams, precision, 0, out);
+}
+
+CBX_API int cbx_num_lanes(const cbx_ctx* ctx) { return ctx && ctx->eng ? ctx->eng->lanes() : -1; }
 
 CBX_API void cbx_destroy(cbx_ctx* ctx) {
     if (!ctx) return;

@@ -658,7 +658,16 @@ void Engine::stage_frame_pointers(int engine, const float* const* cur, const flo
 
 void Engine::forward_host(int engine, const float* frames, uint16_t* labels, cbx_layer_stats* stats,
                           uint64_t* macs) {
+    enqueue_host(engine, frames);
+    if (labels) read_labels(engine, labels);
+    read_stats(engine, stats, macs);
+}
+
+// Host frames -> staging slot (CB ping-pong / baseline) -> forward, all
+// asynchronous on the context stream.
+void Engine::enqueue_host(int engine, const float* frames) {
     if (!frames) throw Error(CBX_E_ARG, "frames is null");
+    if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
     CBX_CUDA(cudaSetDevice(device_));
     const size_t per = (size_t)net_.inputChannels * net_.inputHeight * net_.inputWidth;
     float* slot = engine == CBX_ENGINE_CBINFER ? slots_[parity_] : slots_[2];
@@ -667,8 +676,6 @@ void Engine::forward_host(int engine, const float* frames, uint16_t* labels, cbx
     for (int s = 0; s < S_; ++s) cur[s] = slot + per * s;
     forward_device(engine, cur.data());
     if (engine == CBX_ENGINE_CBINFER) parity_ ^= 1;
-    if (labels) read_labels(engine, labels);
-    read_stats(engine, stats, macs);
 }
 
 void Engine::forward_device(int engine, const float* const* frames_dev) {

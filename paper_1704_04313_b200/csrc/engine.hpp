@@ -50,6 +50,8 @@ public:
     // frames: host S*C*H*W floats (pinned or pageable)
     void forward_host(int engine, const float* frames, uint16_t* labels, cbx_layer_stats* stats,
                       uint64_t* macs);
+    void enqueue_host(int engine, const float* frames);  // forward_host without the read-back
+    int num_streams() const { return S_; }
     void forward_device(int engine, const float* const* frames_dev);
     // pipelined host-frame path (cbx_submit / cbx_wait)
     int64_t submit(int engine, const float* frames, uint16_t* labels);

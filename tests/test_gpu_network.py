@@ -270,3 +270,31 @@ def test_worst_case_counts(gpu, orc, name, spec, cfg):
         assert list(worst[0]) == _oracle_worst_counts(orc, spec, onet), (name, f)
         for j in range(1, len(cb)):
             assert worst[0, j - 1] >= got_frame.stats[cb[j]]["changedOutputPixels"]
+
+
+def test_lanes_equivalent(gpu, orc):
+    """Splitting the streams over 1, 2 or 3 lanes (independent engines on their
+    own CUDA streams) gives identical labels, stats, traces and activations."""
+    spec = paper_spec(40, 56)
+    w = orc.generate_weights(spec, 3)
+    S = 5
+    cfgs = [dict(channels=3, height=40, width=56, sprites=[(8, 1 + s, 0.9)], noise=0.004 * s, seed=30 + s)
+            for s in range(S)]
+    nets = [gpu.Network(to_pkg_spec(gpu, spec), w, streams=S, precision="tf32", lanes=l) for l in (1, 2, 3)]
+    assert [n.num_lanes() for n in nets] == [1, 2, 3]
+    for f in range(4):
+        fr = np.stack([orc.synth_frame(c, f) for c in cfgs])
+        outs = [n.forward(fr) for n in nets]
+        for o in outs[1:]:
+            for s in range(S):
+                assert np.array_equal(o[s].labels, outs[0][s].labels), (f, s)
+                assert np.array_equal(stats_arr(o[s].stats), stats_arr(outs[0][s].stats)), (f, s)
+        for s in range(S):
+            ref_act = nets[0].layer_output(3, s)
+            for n in nets[1:]:
+                assert np.array_equal(bits(n.layer_output(3, s)), bits(ref_act))
+                assert np.array_equal(n.trace(1, s)[1], nets[0].trace(1, s)[1])
+    if f:
+        w1 = nets[0].worst_case_counts()
+        for n in nets[1:]:
+            assert np.array_equal(n.worst_case_counts(), w1)
