@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="cbx", choices=["cbx", "reference"])
     ap.add_argument("--streams", type=int, default=8, help="camera streams per GPU")
+    ap.add_argument("--lanes", type=int, default=0, help="engine lanes per GPU (0: automatic)")
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--recipe", default="2.2", choices=sorted(RECIPES))
@@ -274,7 +275,7 @@ def run_gpu_arm(args):
     specd = paper_spec_dict(args.height, args.width)
     spec = cbx.network_spec_from_json(json.dumps(specd))
     weights = cbx.generate_weights(spec, None, 1)
-    net = cbx.Network(spec, weights, device=local, streams=S, precision=args.precision)
+    net = cbx.Network(spec, weights, device=local, streams=S, precision=args.precision, lanes=args.lanes)
     dims = net.shapes
     stream = torch.cuda.ExternalStream(net.stream_handle(), device=torch.device("cuda", local))
     # resident clips: this rank's shard of the global stream set (stream g on
@@ -510,7 +511,7 @@ def run_gpu_arm(args):
                        "streams_per_gpu": S, "taus": list(BASE_TAUS), "precision": args.precision,
                        "l1_input_changed": frac_in, "layer_output_changed": frac_out,
                        "dense_fps": dense_fps, "speedup_vs_dense": value / dense_fps, "parallelism": f"streams x{ws}",
-                       "single_stream_latency_ms": lat_ms},
+                       "single_stream_latency_ms": lat_ms, "lanes": net.num_lanes()},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * K,
             "clocks": clk,
         }
