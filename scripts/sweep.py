@@ -163,7 +163,7 @@ def main():
     ap.add_argument("--which", default="rate,tau,worst")
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--s320", type=int, default=64, help="streams per GPU at 320x240")
-    ap.add_argument("--s1080", type=int, default=4, help="streams per GPU at 1920x1080")
+    ap.add_argument("--s1080", type=int, default=8, help="streams per GPU at 1920x1080")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.json"))
     args = ap.parse_args()
     res = dict(gpu=torch.cuda.get_device_name(0), when=time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
