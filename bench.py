@@ -454,7 +454,7 @@ def run_gpu_arm(args):
     # timed too, for reference).
     e2e = None
     if not args.no_e2e:
-        Fe = min(F, 6)
+        Fe = min(F, 4)  # host clip (pinned): keep it small, one copy per rank
         host = torch.empty((Fe, S, 3, args.height, args.width), dtype=torch.float32, pin_memory=True)
         host.copy_(clip[:Fe].cpu())
         hostnp = host.numpy()
