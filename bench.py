@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="cbx", choices=["cbx", "reference"])
-    ap.add_argument("--streams", type=int, default=8, help="camera streams per GPU")
+    ap.add_argument("--streams", type=int, default=16, help="camera streams per GPU")
     ap.add_argument("--lanes", type=int, default=0, help="engine lanes per GPU (0: automatic)")
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--width", type=int, default=1920)
@@ -374,8 +374,10 @@ def run_gpu_arm(args):
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         ent = tr.get("kernels", {}).get(f"{kname}[{klayer}]")
         if ent:
-            roof["traffic"] = ent["dram_bytes"]
-            roof["traffic_source"] = tr.get("source")
+            # the capture holds one lane's launch; the timed kernel covers every lane
+            lanes = net.num_lanes()
+            roof["traffic"] = ent["dram_bytes"] * lanes
+            roof["traffic_source"] = "%s x %d lanes" % (tr.get("source"), lanes)
     except (OSError, ValueError):
         pass
     roof["kernel"] = f"{kname}[layer {klayer}]"

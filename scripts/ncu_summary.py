@@ -59,7 +59,7 @@ def main(rep, out_md, out_json):
         e["dram_bytes"] += int(rd + wr)
         e["ncu_us"] = round(e["ncu_us"] + t * 1e-3, 3)
     open(out_md, "w").write("\n".join(lines) + "\n")
-    json.dump({"source": f"{out_md} (ncu --set full --clock-control none, steady frame 1, 8x1080p streams; "
+    json.dump({"source": f"{out_md} (ncu --set full --clock-control none, steady frame 1 of one lane = 8 of 16 x 1080p streams; "
                          "default cache control: caches flushed before each kernel)", "kernels": traffic},
               open(out_json, "w"), indent=1)
     print("\n".join(lines))
