@@ -58,6 +58,24 @@ __device__ __forceinline__ bool ref_changed(float now, float before, float tau) 
     return d > tau || -d > tau;
 }
 
+// Two fp32 lanes per instruction (FFMA2), each IEEE round-to-nearest. The
+// reference's separately rounded multiply and add are f2_fma(w, x, -0) and
+// f2_fma(p, 1, acc) with 1 and -0 passed as RUNTIME values: with literal
+// constants ptxas contracts the pair into one fused multiply-add.
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 // Adds `flag` into counters[s*stride] with one atomic per (warp, stream).
 __device__ __forceinline__ void warp_count_add(unsigned long long* counters, int stride, int s,
                                                bool flag, bool active) {

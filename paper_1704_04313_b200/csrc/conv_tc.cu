@@ -243,6 +243,7 @@ struct TcArgs {
     unsigned long long* chg_cnt;
     int cnt_stride;
     int write_out;  // store this layer's output tensor (off when a fused tail consumes it)
+    float one, nzero;  // 1.0f / -0.0f as runtime values (paired-fp32 rounding, common.cuh)
     int tail_w_floats;  // shared memory reserved for the first tail conv's filters
     TcTail tail;
 };
@@ -252,10 +253,13 @@ struct TcArgs {
 // the layer output is kept) compare-before-write against the stored value.
 // FULL: all 32 channels exist, so every loop is branch-free and the shared
 // memory loads of bias / tail filters can be hoisted ahead of their use.
+// t1p: the first tail conv's TC accumulators as TC/2 packed fp32 pairs.
+template <int TC>
+using TailAcc = unsigned long long[TC > 1 ? TC / 2 : 1];
+
 template <int TC, bool FULL>
 __device__ __forceinline__ void epi_chunk(const TcArgs& a, float (&v)[32], int c0, int nv, const float* sBias,
-                                          const float* sTailW, float (&t1)[TC > 0 ? TC : 1], float* dst,
-                                          bool& changed) {
+                                          const float* sTailW, TailAcc<TC>& t1p, float* dst, bool& changed) {
 #pragma unroll
     for (int j = 0; j < 32; j += 4) {
         if (!FULL && j >= nv) break;
@@ -268,18 +272,20 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, float (&v)[32], int c
         }
     }
     if constexpr (TC > 0) {
-        // the TC filters of one channel are TC/4 broadcast LDS.128
+        // the TC filters of one channel are TC/4 broadcast LDS.128 = TC/2
+        // packed pairs; two output channels per paired-fp32 step, each with
+        // the reference's two roundings (common.cuh)
+        const unsigned long long one2 = f2_pack(a.one, a.one), nz2 = f2_pack(a.nzero, a.nzero);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
             if (!FULL && j >= nv) break;
-            const float4* w = reinterpret_cast<const float4*>(sTailW + (c0 + j) * TC);
+            const ulonglong2* w = reinterpret_cast<const ulonglong2*>(sTailW + (c0 + j) * TC);
+            const unsigned long long vv = f2_pack(v[j], v[j]);
 #pragma unroll
             for (int q4 = 0; q4 < TC / 4; ++q4) {
-                const float4 wq = w[q4];
-                t1[4 * q4 + 0] = __fadd_rn(t1[4 * q4 + 0], __fmul_rn(wq.x, v[j]));
-                t1[4 * q4 + 1] = __fadd_rn(t1[4 * q4 + 1], __fmul_rn(wq.y, v[j]));
-                t1[4 * q4 + 2] = __fadd_rn(t1[4 * q4 + 2], __fmul_rn(wq.z, v[j]));
-                t1[4 * q4 + 3] = __fadd_rn(t1[4 * q4 + 3], __fmul_rn(wq.w, v[j]));
+                const ulonglong2 wq = w[q4];
+                t1p[2 * q4 + 0] = f2_fma(f2_fma(wq.x, vv, nz2), one2, t1p[2 * q4 + 0]);
+                t1p[2 * q4 + 1] = f2_fma(f2_fma(wq.y, vv, nz2), one2, t1p[2 * q4 + 1]);
             }
         }
     }
@@ -583,17 +589,26 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             // fused per-pixel tail: first op is a 1x1 CONV over this layer's
             // outputs, accumulated chunk by chunk in ascending channel order
             constexpr int TCA = TC > 0 ? TC : 1;
-            float t1[TCA];
+            TailAcc<TC> t1p;
 #pragma unroll
-            for (int q = 0; q < TCA; ++q) t1[q] = (TC > 0 && q < a.tail.cout[0]) ? __ldg(a.tail.b[0] + q) : 0.0f;
+            for (int q = 0; q < (TC > 1 ? TC / 2 : 1); ++q)
+                t1p[q] = f2_pack((TC > 0 && 2 * q < a.tail.cout[0]) ? __ldg(a.tail.b[0] + 2 * q) : 0.0f,
+                                 (TC > 0 && 2 * q + 1 < a.tail.cout[0]) ? __ldg(a.tail.b[0] + 2 * q + 1) : 0.0f);
             for (int c0 = 0; c0 < a.O; c0 += 32) {
                 float v[32];
                 tmem_ld32(trow + c0, v);
                 if (!valid) continue;
                 if (c0 + 32 <= a.O)
-                    epi_chunk<TC, true>(a, v, c0, 32, sBias, sTailW, t1, dst, changed);
+                    epi_chunk<TC, true>(a, v, c0, 32, sBias, sTailW, t1p, dst, changed);
                 else
-                    epi_chunk<TC, false>(a, v, c0, a.O - c0, sBias, sTailW, t1, dst, changed);
+                    epi_chunk<TC, false>(a, v, c0, a.O - c0, sBias, sTailW, t1p, dst, changed);
+            }
+            float t1[TCA];
+#pragma unroll
+            for (int q = 0; q < TCA; ++q) t1[q] = 0.0f;
+            if constexpr (TC > 1) {
+#pragma unroll
+                for (int q = 0; q < TC / 2; ++q) f2_unpack(t1p[q], t1[2 * q], t1[2 * q + 1]);
             }
             tc_fence_before();
             if constexpr (PAIR) {
@@ -837,6 +852,8 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.chg_cnt = chg.d ? cnt : nullptr;
     a.cnt_stride = cstride;
     a.write_out = !(tail && tail->n && !tail->keep_out);
+    a.one = 1.0f;
+    a.nzero = -0.0f;
     if (tail) a.tail = *tail;
     const int tc = (tail && tail->n) ? (tail->cout[0] <= 8 ? 8 : 16) : 0;
     const bool rowlane = in.Cp <= 4;

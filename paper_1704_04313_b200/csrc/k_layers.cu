@@ -249,21 +249,6 @@ struct PlanarFilters {
     float one, nzero;
 };
 
-// Two fp32 lanes per instruction (FFMA2), each IEEE round-to-nearest.
-__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void f2_unpack(unsigned long long v, float& a, float& b) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
-    unsigned long long r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-
 template <int C, int KH, int KW, int OC>
 __global__ void __launch_bounds__(kConvThreads, 8) conv_planar_fixed_kernel(ConvArgs a,
                                                                             const __grid_constant__ PlanarFilters<C, KH, KW, OC> f) {
