@@ -541,7 +541,10 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                     const uint32_t st = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&full[st], ph);
                     if constexpr (PAIR) mbar_wait_cluster(&pfull[st], ph);
-                    fence_proxy_async();
+                    // no proxy fence here: the cp.async -> mbarrier -> tcgen05.mma
+                    // hand-off is the one CUTLASS's SM100 cp.async UMMA mainloop
+                    // uses (producer_commit with cpasync_barrier_arrive, then
+                    // consumer_wait, then the MMAs); the fence cost 1-2 % of L3
                     tc_fence_after();
                     const uint32_t aaddr = smem_u32(sA + (size_t)st * kABytes);
                     const uint32_t baddr = smem_u32(sB + (size_t)st * b_bytes);
