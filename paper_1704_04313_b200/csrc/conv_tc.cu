@@ -157,6 +157,15 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
         : "memory");
 }
 
+// one lane of a converged warp (elect.sync): the warp runs the MMA issue loop
+// together, so descriptors and loop state stay warp-uniform (uniform
+// registers) and only the tcgen05 instructions themselves are predicated
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -525,12 +534,16 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                         mbar_arrive_cluster(mapa(&pfull[st], 0));
                     }
             }
-        } else if (lane == 0) {
-            // ================= MMA issuer =================
+        } else {
+            // ================= MMA issuer (whole warp, one elected lane issues) =================
             const int M = PAIR ? 2 * kTileM : kTileM;
             const uint32_t id0 = idesc_tf32(a.N0, M), id1 = idesc_tf32(a.N1 > 0 ? a.N1 : 16, M);
+            const bool two = a.N1 > 0;
             // B rows of the second instruction start after this CTA's share of the first
             const uint32_t b1_off = (uint32_t)(PAIR ? a.N0 / 2 : a.N0) * 128u;
+            const uint64_t a_desc0 = smem_desc(smem_u32(sA)), b_desc0 = smem_desc(smem_u32(sB));
+            // descriptor start-address field is in 16-byte units
+            const uint64_t a_st = kABytes >> 4, b_st = b_bytes >> 4, b1_d = b1_off >> 4;
             uint32_t it = 0, acc_it = 0;
             for (int64_t tile = tile_first; tile < ntiles; tile += tile_step, ++acc_it) {
                 const uint32_t as = acc_it % a.acc_stages, aph = (acc_it / a.acc_stages) & 1u;
@@ -546,23 +559,27 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                     // uses (producer_commit with cpasync_barrier_arrive, then
                     // consumer_wait, then the MMAs); the fence cost 1-2 % of L3
                     tc_fence_after();
-                    const uint32_t aaddr = smem_u32(sA + (size_t)st * kABytes);
-                    const uint32_t baddr = smem_u32(sB + (size_t)st * b_bytes);
+                    const uint64_t ad = a_desc0 + st * a_st, bd = b_desc0 + st * b_st;
+                    if (elect_one()) {
 #pragma unroll
-                    for (int k = 0; k < kKBlock / 8; ++k) {
-                        const uint64_t ad = smem_desc(aaddr + k * 32);
-                        const uint32_t accum = (kb | k) ? 1u : 0u;
-                        if constexpr (PAIR) {
-                            mma_tf32_pair(d, ad, smem_desc(baddr + k * 32), id0, accum);
-                            if (a.N1 > 0) mma_tf32_pair(d + a.N0, ad, smem_desc(baddr + b1_off + k * 32), id1, accum);
-                        } else {
-                            mma_tf32(d, ad, smem_desc(baddr + k * 32), id0, accum);
-                            if (a.N1 > 0) mma_tf32(d + a.N0, ad, smem_desc(baddr + b1_off + k * 32), id1, accum);
+                        for (int k = 0; k < kKBlock / 8; ++k) {
+                            const uint32_t accum = (kb | k) ? 1u : 0u;
+                            if constexpr (PAIR) {
+                                mma_tf32_pair(d, ad + 2 * k, bd + 2 * k, id0, accum);
+                                if (two) mma_tf32_pair(d + a.N0, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
+                            } else {
+                                mma_tf32(d, ad + 2 * k, bd + 2 * k, id0, accum);
+                                if (two) mma_tf32(d + a.N0, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
+                            }
                         }
+                        if constexpr (PAIR) mma_commit_pair(&empty[st]); else mma_commit(&empty[st]);
                     }
-                    if constexpr (PAIR) mma_commit_pair(&empty[st]); else mma_commit(&empty[st]);
+                    __syncwarp();
                 }
-                if constexpr (PAIR) mma_commit_pair(&tfull[as]); else mma_commit(&tfull[as]);
+                if (elect_one()) {
+                    if constexpr (PAIR) mma_commit_pair(&tfull[as]); else mma_commit(&tfull[as]);
+                }
+                __syncwarp();
             }
         }
         __syncwarp();
