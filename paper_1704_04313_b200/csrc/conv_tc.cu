@@ -157,6 +157,18 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
         : "memory");
 }
 
+// position in the ring of NS shared-memory stages (stage, barrier parity),
+// advanced without a division per K-block
+struct Ring {
+    uint32_t st = 0, ph = 0;
+    __device__ __forceinline__ void next(int n) {
+        if (++st == (uint32_t)n) {
+            st = 0;
+            ph ^= 1u;
+        }
+    }
+};
+
 // one lane of a converged warp (elect.sync): the warp runs the MMA issue loop
 // together, so descriptors and loop state stay warp-uniform (uniform
 // registers) and only the tcgen05 instructions themselves are predicated
@@ -427,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         if constexpr (ROWLANE) {
             const int r = tid - kEpiThreads;
             const uint32_t swz = (uint32_t)(r & 7);
-            uint32_t it = 0;
+            Ring rg;
             // the next tile's index is loaded while this tile's K-blocks are
             // gathered, so a tile never starts with a dependent index load
             auto row_index = [&](int64_t t) -> int64_t {
@@ -447,8 +459,8 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                     base = a.in + (int64_t)s * a.in_ss +
                            ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
                 }
-                for (int kb = 0; kb < a.NKB; ++kb, ++it) {
-                    const uint32_t st = it % NS, ph = (it / NS) & 1u;
+                for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
+                    const uint32_t st = rg.st, ph = rg.ph;
                     mbar_wait(&empty[st], ph ^ 1u);
                     if (r == 0) {
                         mbar_arrive_expect_tx(&full[st], b_bytes);
@@ -473,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         const int j = pt & 7, rsub = pt >> 3;
         const uint32_t swz_off = (uint32_t)((j ^ (rsub & 7)) << 4);
         constexpr int kRowsPerThread = kTileM / 16;
-        uint32_t it = 0;
+        Ring rg;
         // indices of the next tile's rows are loaded during this tile's K-loop
         int32_t gnext[kRowsPerThread];
         auto load_rows = [&](int64_t t) {
@@ -504,8 +516,8 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                               ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
                 }
             }
-            for (int kb = 0; kb < a.NKB; ++kb, ++it) {
-                const uint32_t st = it % NS, ph = (it / NS) & 1u;
+            for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
+                const uint32_t st = rg.st, ph = rg.ph;
                 mbar_wait(&empty[st], ph ^ 1u);
                 if (pt == 0) {
                     mbar_arrive_expect_tx(&full[st], b_bytes);
@@ -513,10 +525,16 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 }
                 const int off = sTab[kb * kChunksPerKB + j];
                 const uint32_t stage = smem_u32(sA + (size_t)st * kABytes) + swz_off;
+                if (off >= 0) {
 #pragma unroll
-                for (int i = 0; i < kRowsPerThread; ++i)
-                    if ((vmask >> i) & 1u)
-                        cp_async16(stage + (rsub + 16 * i) * 128, off >= 0 ? base[i] + off : a.in, off >= 0 ? 16u : 0u);
+                    for (int i = 0; i < kRowsPerThread; ++i)
+                        if ((vmask >> i) & 1u) cp_async16(stage + (rsub + 16 * i) * 128, base[i] + off, 16u);
+                } else {
+                    // chunk past the real K (last K-block only): zero-fill
+#pragma unroll
+                    for (int i = 0; i < kRowsPerThread; ++i)
+                        if ((vmask >> i) & 1u) cp_async16(stage + (rsub + 16 * i) * 128, a.in, 0u);
+                }
                 cp_async_arrive_noinc(&full[st]);
             }
         }
@@ -525,10 +543,10 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         if (PAIR && crank != 0) {
             // ================= peer: relay "stage full" to the leader =================
             if (lane == 0) {
-                uint32_t it = 0;
+                Ring rg;
                 for (int64_t tile = tile_first; tile < ntiles; tile += tile_step)
-                    for (int kb = 0; kb < a.NKB; ++kb, ++it) {
-                        const uint32_t st = it % NS, ph = (it / NS) & 1u;
+                    for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
+                        const uint32_t st = rg.st, ph = rg.ph;
                         mbar_wait(&full[st], ph);
                         fence_proxy_async();
                         mbar_arrive_cluster(mapa(&pfull[st], 0));
@@ -544,14 +562,15 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             const uint64_t a_desc0 = smem_desc(smem_u32(sA)), b_desc0 = smem_desc(smem_u32(sB));
             // descriptor start-address field is in 16-byte units
             const uint64_t a_st = kABytes >> 4, b_st = b_bytes >> 4, b1_d = b1_off >> 4;
-            uint32_t it = 0, acc_it = 0;
+            Ring rg;
+            uint32_t acc_it = 0;
             for (int64_t tile = tile_first; tile < ntiles; tile += tile_step, ++acc_it) {
                 const uint32_t as = acc_it % a.acc_stages, aph = (acc_it / a.acc_stages) & 1u;
                 if constexpr (PAIR) mbar_wait_cluster(&tempty[as], aph ^ 1u); else mbar_wait(&tempty[as], aph ^ 1u);
                 tc_fence_after();
                 const uint32_t d = tmem_base + as * a.acc_cols;
-                for (int kb = 0; kb < a.NKB; ++kb, ++it) {
-                    const uint32_t st = it % NS, ph = (it / NS) & 1u;
+                for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
+                    const uint32_t st = rg.st, ph = rg.ph;
                     mbar_wait(&full[st], ph);
                     if constexpr (PAIR) mbar_wait_cluster(&pfull[st], ph);
                     // no proxy fence here: the cp.async -> mbarrier -> tcgen05.mma
