@@ -258,6 +258,11 @@ struct TcArgs {
     int NKB, Npad, N0, N1;
     int Brows;           // filter rows held per CTA (Npad, or Npad/2 for a CTA pair)
     int stages, acc_stages, acc_cols, tmem_cols;
+    // split accumulator (N_pad > 256, single CTA): the first instruction's N0
+    // channels always land in the shared columns [ovl_s, ovl_s + N0), the
+    // second's alternate between ovl_b[0] and ovl_b[1] by tile parity, so the
+    // next tile's MMAs wait only for the shared columns to be drained
+    int ovl, ovl_s, ovl_b0, ovl_b1;
     int relu;
     BitMask chg;
     float tau;
@@ -371,7 +376,8 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
     uint64_t* pfull = empty + NS;  // PAIR, leader only: the peer's stage is full
     uint64_t* tfull = pfull + NS;
     uint64_t* tempty = tfull + 2;
-    uint32_t* sTmem = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tshared = tempty + 2;  // ovl: the shared columns of the last tile are drained
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(tshared + 1);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -412,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], PAIR ? 2 * (kEpiThreads / 32) : kEpiThreads);
         }
+        mbar_init(tshared, kEpiThreads);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 8) {
@@ -567,8 +574,10 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             for (int64_t tile = tile_first; tile < ntiles; tile += tile_step, ++acc_it) {
                 const uint32_t as = acc_it % a.acc_stages, aph = (acc_it / a.acc_stages) & 1u;
                 if constexpr (PAIR) mbar_wait_cluster(&tempty[as], aph ^ 1u); else mbar_wait(&tempty[as], aph ^ 1u);
+                if (a.ovl && acc_it > 0) mbar_wait(tshared, (acc_it - 1) & 1u);
                 tc_fence_after();
-                const uint32_t d = tmem_base + as * a.acc_cols;
+                const uint32_t d = tmem_base + (a.ovl ? (uint32_t)a.ovl_s : as * a.acc_cols);
+                const uint32_t d1 = a.ovl ? tmem_base + (uint32_t)(as ? a.ovl_b1 : a.ovl_b0) : d + a.N0;
                 for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
                     const uint32_t st = rg.st, ph = rg.ph;
                     mbar_wait(&full[st], ph);
@@ -588,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                                 if (two) mma_tf32_pair(d + a.N0, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
                             } else {
                                 mma_tf32(d, ad + 2 * k, bd + 2 * k, id0, accum);
-                                if (two) mma_tf32(d + a.N0, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
+                                if (two) mma_tf32(d1, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
                             }
                         }
                         if constexpr (PAIR) mma_commit_pair(&empty[st]); else mma_commit(&empty[st]);
@@ -624,7 +633,11 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 dst = a.out + (int64_t)s * a.out_ss + ((int64_t)(y + a.out_hh) * a.out_Wp + (x + a.out_hw)) * a.out_Cp;
             }
             bool changed = false;
-            const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16) + as * a.acc_cols;
+            const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16);
+            // TMEM column of channel c0: one accumulator per stage, or (ovl)
+            // the shared columns for c0 < N0 and this parity's own after
+            const uint32_t col_lo = a.ovl ? (uint32_t)a.ovl_s : as * a.acc_cols;
+            const uint32_t col_hi = a.ovl ? (uint32_t)(as ? a.ovl_b1 : a.ovl_b0) - (uint32_t)a.N0 : col_lo;
             // fused per-pixel tail: first op is a 1x1 CONV over this layer's
             // outputs, accumulated chunk by chunk in ascending channel order
             constexpr int TCA = TC > 0 ? TC : 1;
@@ -635,7 +648,12 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                                  (TC > 0 && 2 * q + 1 < a.tail.cout[0]) ? __ldg(a.tail.b[0] + 2 * q + 1) : 0.0f);
             for (int c0 = 0; c0 < a.O; c0 += 32) {
                 float v[32];
-                tmem_ld32(trow + c0, v);
+                tmem_ld32(trow + (c0 < a.N0 ? col_lo : col_hi) + c0, v);
+                if (a.ovl && c0 + 32 == a.N0) {
+                    // shared columns drained: the next tile's MMAs may start
+                    tc_fence_before();
+                    mbar_arrive(tshared);
+                }
                 if (!valid) continue;
                 if (c0 + 32 <= a.O)
                     epi_chunk<TC, true>(a, v, c0, 32, sBias, sTailW, t1p, dst, changed);
@@ -697,6 +715,8 @@ struct TcLayer {
     int tail_w_floats = 0;
     int ctas_per_sm = 1;
     bool pair = false;   // CTA pair (cta_group::2, M = 256)
+    bool ovl = false;    // split accumulator (see make_tc_layer)
+    int ovl_s = 0, ovl_b0 = 0, ovl_b1 = 0;
     int Brows = 0;       // filter rows per CTA
     int max_clusters = 0;
     size_t smem = 0;
@@ -745,6 +765,29 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     int cols = 32;
     while (cols < t->acc_stages * t->acc_cols) cols *= 2;
     t->tmem_cols = cols;
+    // A wide layer's accumulator (N_pad > 256) cannot be double-buffered in
+    // 512 TMEM columns, so the MMAs of tile t+1 would wait for the whole
+    // epilogue of tile t. Split accumulator instead: the first instruction
+    // (N0 = 128 channels, drained first by the epilogue) always writes the
+    // shared columns [s, s + 128); the second (N1 = N_pad - 128) alternates
+    // between [0, N1) and [s + 128, s + 128 + N1) by tile parity. Tile t+1
+    // then waits only for tile t's first four 32-channel chunks.
+    // CBX_TC_OVL=0 keeps the single accumulator (tuning).
+    const char* ovl_env = std::getenv("CBX_TC_OVL");
+    if (pair_mode <= 0 && t->Npad > 256 && !(ovl_env && std::atoi(ovl_env) == 0)) {
+        const int n0 = 128, n1 = t->Npad - n0;
+        const int s0 = (int)round_up(n1, 32);
+        if (n1 <= 256 && s0 + t->Npad <= 512) {
+            t->ovl = true;
+            t->N0 = n0;
+            t->N1 = n1;
+            t->acc_stages = 2;
+            t->ovl_s = s0;
+            t->ovl_b0 = 0;
+            t->ovl_b1 = s0 + n0;
+            t->tmem_cols = 512;
+        }
+    }
     // CTA pairs (M = 256, each SM streams half the filter bank) are opt-in:
     // measured on B200 they lose to single-CTA tiles for the paper's L3
     // (1.54 vs 1.42 ms dense 4x1080p): the shallower per-SM shared memory
@@ -758,7 +801,7 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     const size_t b_bytes = (size_t)t->Brows * 128;
     t->tail_w_floats = (int)round_up(tail_floats, 4);
     const size_t fixed = 1024 + (size_t)t->NKB * kChunksPerKB * 4 + round_up(g.outChannels, 4) * 4 +
-                         (size_t)t->tail_w_floats * 4 + 16 + 8 * (3 * 16 + 4) + 16;
+                         (size_t)t->tail_w_floats * 4 + 16 + 8 * (3 * 16 + 5) + 16;
     const size_t budget = t->ctas_per_sm == 2 ? (size_t)kMaxSmem / 2 - 1024 : (size_t)kMaxSmem;
     // stage count: deep enough to cover the gather latency, shallow enough to
     // leave L1 for the gather's tap reuse (neighbouring output pixels share
@@ -882,6 +925,10 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.acc_stages = t.acc_stages;
     a.acc_cols = t.acc_cols;
     a.tmem_cols = t.tmem_cols;
+    a.ovl = t.ovl;
+    a.ovl_s = t.ovl_s;
+    a.ovl_b0 = t.ovl_b0;
+    a.ovl_b1 = t.ovl_b1;
     a.tail_w_floats = t.tail_w_floats;
     if (tail && tail->n && (tail->cout[0] <= 8 ? 8 : 16) * out.C > t.tail_w_floats)
         throw Error(CBX_E_ARG, "tcgen05 conv: fused tail filters exceed the reserved shared memory");
