@@ -475,9 +475,14 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                     }
                     const uint32_t row = smem_u32(sA + (size_t)st * kABytes + r * 128);
                     if (valid) {
+                        // the K-block's 8 chunk offsets in two 16-byte loads, so
+                        // their latencies overlap instead of one LDS per copy
+                        const int4* tab4 = reinterpret_cast<const int4*>(sTab + kb * kChunksPerKB);
+                        const int4 o0 = tab4[0], o1 = tab4[1];
+                        const int offs[kChunksPerKB] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
 #pragma unroll
                         for (int j = 0; j < kChunksPerKB; ++j) {
-                            const int off = sTab[kb * kChunksPerKB + j];
+                            const int off = offs[j];
                             cp_async16(row + ((j ^ swz) << 4), off >= 0 ? base + off : a.in, off >= 0 ? 16u : 0u);
                         }
                     }
