@@ -18,12 +18,14 @@
 // * B = the filter bank, pre-arranged on the host into exactly the smem image
 //   of every K-block (N_pad rows x 128 B, swizzled, tf32-rounded), loaded with
 //   one cp.async.bulk per stage that completes on the stage's mbarrier.
-// * One elected thread issues tcgen05.mma (M=128, N<=256 per instruction; two
-//   instructions when N_pad > 256, e.g. 304 = 256 + 48) into a TMEM
-//   accumulator; tcgen05.commit releases smem stages and hands finished
-//   accumulators to the epilogue. Persistent CTAs walk tiles; with N_pad <= 256
-//   the accumulator is double-buffered so the epilogue of tile t overlaps the
-//   MMAs of tile t+1.
+// * The MMA warp runs its loop converged; one elect.sync lane issues
+//   tcgen05.mma (M=128, N<=256 per instruction; two instructions when
+//   N_pad > 256, e.g. 304 = 128 + 176) into a TMEM accumulator;
+//   tcgen05.commit releases smem stages and hands finished accumulators to
+//   the epilogue. Persistent CTAs walk tiles; with N_pad <= 256 the
+//   accumulator is double-buffered so the epilogue of tile t overlaps the
+//   MMAs of tile t+1, wider layers split it (shared head columns + a tail
+//   region per tile parity, see make_tc_layer).
 // * Epilogue (4 warps, thread = TMEM lane = tile row): tcgen05.ld 32 columns at
 //   a time, + bias, fused ReLU, compare with the value being overwritten
 //   (next CBCONV's change detection, cbconv.cpp:66-67), in-place scatter into
@@ -722,6 +724,7 @@ struct TcLayer {
     bool pair = false;   // CTA pair (cta_group::2, M = 256)
     bool ovl = false;    // split accumulator (see make_tc_layer)
     int ovl_s = 0, ovl_b0 = 0, ovl_b1 = 0;
+    int max_ctas = 0;    // persistent grid cap (0: one per SM x ctas_per_sm)
     int Brows = 0;       // filter rows per CTA
     int max_clusters = 0;
     size_t smem = 0;
@@ -818,6 +821,10 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     if (fixed + (size_t)ns * (kABytes + b_bytes) > budget)
         throw Error(CBX_E_ARG, "tcgen05 conv: layer too wide for shared memory");
     t->stages = ns;
+    // CBX_TC_MAXCTAS caps the persistent grid of one-CTA-per-SM layers (tuning:
+    // SMs left free for the other lane's kernels)
+    if (const char* e = std::getenv("CBX_TC_MAXCTAS"))
+        if (t->ctas_per_sm == 1) t->max_ctas = std::max(1, std::atoi(e));
     t->smem = fixed + (size_t)ns * (kABytes + b_bytes);
     set_smem_attrs<0, false>();
     set_smem_attrs<8, false>();
@@ -975,7 +982,8 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
         return;
     }
     const int64_t max_tiles = (full_count + kTileM - 1) / kTileM;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, (int64_t)kNumSMs * t.ctas_per_sm));
+    const int64_t cap = t.max_ctas > 0 ? t.max_ctas : (int64_t)kNumSMs * t.ctas_per_sm;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, cap));
 #define CBX_TC_LAUNCH(R, T) conv_tc_kernel<R, T, false><<<grid, kThreads, t.smem, st>>>(a)
     if (tc == 0) {
         if (rowlane) CBX_TC_LAUNCH(true, 0); else CBX_TC_LAUNCH(false, 0);
