@@ -250,57 +250,78 @@ struct PlanarFilters {
 };
 
 template <int C, int KH, int KW, int OC>
-__global__ void __launch_bounds__(kConvThreads, 8) conv_planar_fixed_kernel(ConvArgs a,
+__global__ void __launch_bounds__(kConvThreads, 4) conv_planar_fixed_kernel(ConvArgs a,
                                                                             const __grid_constant__ PlanarFilters<C, KH, KW, OC> f) {
-    static_assert(OC % 2 == 0, "paired accumulators");
     const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
     const int Wo = a.out.W, H = a.in.H, W = a.in.W;
     const int64_t HoWo = (int64_t)a.out.H * Wo, HW = (int64_t)H * W;
     const unsigned long long one2 = f2_pack(f.one, f.one), nz2 = f2_pack(f.nzero, f.nzero);
-    for (int64_t base = (int64_t)blockIdx.x * kConvThreads; base < total; base += (int64_t)gridDim.x * kConvThreads) {
-        const int64_t n = base + threadIdx.x;
-        const bool valid = n < total;
-        int s = 0, y = 0, x = 0;
-        bool changed = false;
-        if (valid) {
-            const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
-            s = (int)(g / HoWo);
-            const int p = (int)(g - (int64_t)s * HoWo);
-            y = p / Wo;
-            x = p - y * Wo;
-            const int y0 = y - a.ph, x0 = x - a.pw;
-            const float* src = a.in_ptrs[s];
-            float acc[OC];
-            if (y0 >= 0 && y0 + KH <= H && x0 >= 0 && x0 + KW <= W) {
-                // interior: a channel's KHxKW taps in flight at once, then
-                // acc = round(acc + round(w * x)) two output channels per instruction
-                unsigned long long a2[OC / 2];
+    // each thread evaluates two pixels of the list (n and n + kConvThreads);
+    // the paired-fp32 lanes hold the SAME output channel of the two pixels, so
+    // every filter weight is one uniform scalar operand shared by both
+    constexpr int64_t kStep = 2 * kConvThreads;
+    for (int64_t base = (int64_t)blockIdx.x * kStep; base < total; base += (int64_t)gridDim.x * kStep) {
+        bool valid[2], interior[2];
+        int s[2], y[2], x[2];
 #pragma unroll
-                for (int j = 0; j < OC / 2; ++j) a2[j] = f2_pack(f.b[2 * j], f.b[2 * j + 1]);
-                const float* win = src + (int64_t)y0 * W + x0;
+        for (int h = 0; h < 2; ++h) {
+            const int64_t n = base + h * kConvThreads + threadIdx.x;
+            valid[h] = n < total;
+            s[h] = y[h] = x[h] = 0;
+            if (valid[h]) {
+                const int64_t g = a.idx ? (int64_t)__ldg(a.idx + n) : n;
+                s[h] = (int)(g / HoWo);
+                const int p = (int)(g - (int64_t)s[h] * HoWo);
+                y[h] = p / Wo;
+                x[h] = p - y[h] * Wo;
+            }
+            const int y0 = y[h] - a.ph, x0 = x[h] - a.pw;
+            interior[h] = y0 >= 0 && y0 + KH <= H && x0 >= 0 && x0 + KW <= W;
+        }
+        float acc[2][OC];
+        // Warp-uniform fast path when every live pixel of the warp has its
+        // whole window inside the frame (the common case): converged code,
+        // constant-bank weights as uniform operands, taps of a channel loaded
+        // together. Dead lanes compute on the frame's top-left window.
+        if (__all_sync(0xffffffffu, (interior[0] || !valid[0]) && (interior[1] || !valid[1]))) {
+            const float* win[2];
 #pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    float v[KH * KW];
+            for (int h = 0; h < 2; ++h)
+                win[h] = valid[h] ? a.in_ptrs[s[h]] + (int64_t)(y[h] - a.ph) * W + (x[h] - a.pw) : a.in_ptrs[0];
+            unsigned long long a2[OC];
 #pragma unroll
-                    for (int kj = 0; kj < KH; ++kj)
+            for (int j = 0; j < OC; ++j) a2[j] = f2_pack(f.b[j], f.b[j]);
 #pragma unroll
-                        for (int ki = 0; ki < KW; ++ki) v[kj * KW + ki] = __ldg(win + c * HW + (int64_t)kj * W + ki);
+            for (int c = 0; c < C; ++c) {
+                float v0[KH * KW], v1[KH * KW];
 #pragma unroll
-                    for (int t = 0; t < KH * KW; ++t) {
-                        const int r = c * KH * KW + t;
-                        const unsigned long long vv = f2_pack(v[t], v[t]);
+                for (int kj = 0; kj < KH; ++kj)
 #pragma unroll
-                        for (int j = 0; j < OC / 2; ++j) {
-                            const unsigned long long prod = f2_fma(f2_pack(f.w[r][2 * j], f.w[r][2 * j + 1]), vv, nz2);
-                            a2[j] = f2_fma(prod, one2, a2[j]);
-                        }
+                    for (int ki = 0; ki < KW; ++ki) {
+                        v0[kj * KW + ki] = __ldg(win[0] + c * HW + (int64_t)kj * W + ki);
+                        v1[kj * KW + ki] = __ldg(win[1] + c * HW + (int64_t)kj * W + ki);
+                    }
+#pragma unroll
+                for (int t = 0; t < KH * KW; ++t) {
+                    const int r = c * KH * KW + t;
+                    const unsigned long long xx = f2_pack(v0[t], v1[t]);
+#pragma unroll
+                    for (int j = 0; j < OC; ++j) {
+                        const unsigned long long prod = f2_fma(xx, f2_pack(f.w[r][j], f.w[r][j]), nz2);
+                        a2[j] = f2_fma(prod, one2, a2[j]);
                     }
                 }
+            }
 #pragma unroll
-                for (int j = 0; j < OC / 2; ++j) f2_unpack(a2[j], acc[2 * j], acc[2 * j + 1]);
-            } else {
+            for (int j = 0; j < OC; ++j) f2_unpack(a2[j], acc[0][j], acc[1][j]);
+        } else {
 #pragma unroll
-                for (int j = 0; j < OC; ++j) acc[j] = f.b[j];
+            for (int h = 0; h < 2; ++h) {
+                if (!valid[h]) continue;
+                const float* src = a.in_ptrs[s[h]];
+                const int y0 = y[h] - a.ph, x0 = x[h] - a.pw;
+#pragma unroll
+                for (int j = 0; j < OC; ++j) acc[h][j] = f.b[j];
 #pragma unroll 1
                 for (int c = 0; c < C; ++c)
 #pragma unroll 1
@@ -314,21 +335,28 @@ __global__ void __launch_bounds__(kConvThreads, 8) conv_planar_fixed_kernel(Conv
                             const float v = (rowok && (unsigned)xx < (unsigned)W) ? __ldg(rp + xx) : 0.0f;
                             const int r = (c * KH + kj) * KW + ki;
 #pragma unroll
-                            for (int j = 0; j < OC; ++j) acc[j] = __fadd_rn(acc[j], __fmul_rn(f.w[r][j], v));
+                            for (int j = 0; j < OC; ++j) acc[h][j] = __fadd_rn(acc[h][j], __fmul_rn(f.w[r][j], v));
                         }
                     }
             }
-            float* dst = a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + (x + a.out.hw)) * a.out.Cp;
-#pragma unroll
-            for (int j = 0; j < OC; ++j) {
-                const float v = a.relu ? ref_relu(acc[j]) : acc[j];
-                if (a.chg.d) changed |= ref_changed(v, dst[j], a.tau);
-                dst[j] = v;
-            }
         }
-        if (a.chg.d) {
-            if (valid && changed) bit_set(a.chg, s, y, x);
-            if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            bool changed = false;
+            if (valid[h]) {
+                float* dst = a.out.d + (int64_t)s[h] * a.out.ss +
+                             ((int64_t)(y[h] + a.out.hh) * a.out.Wp + (x[h] + a.out.hw)) * a.out.Cp;
+#pragma unroll
+                for (int j = 0; j < OC; ++j) {
+                    const float v = a.relu ? ref_relu(acc[h][j]) : acc[h][j];
+                    if (a.chg.d) changed |= ref_changed(v, dst[j], a.tau);
+                    dst[j] = v;
+                }
+            }
+            if (a.chg.d) {
+                if (valid[h] && changed) bit_set(a.chg, s[h], y[h], x[h]);
+                if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s[h], changed, valid[h]);
+            }
         }
     }
 }
@@ -349,7 +377,7 @@ void launch_conv_exact(const ConvArgs& a, cudaStream_t st) {
     int grid = (int)std::min<int64_t>(max_tiles, (int64_t)kNumSMs * 12);
     if (grid < 1) grid = 1;
     if (!std::getenv("CBX_NO_FIXED_PLANAR") && a.in_ptrs && a.hK && a.hB && a.in.C == 3 && a.kh == 7 && a.kw == 7 && a.sh == 1 && a.sw == 1 && a.out.C == 4 &&
-        a.out.Cp >= 4) {
+        a.out.Cp >= 4 && a.in.H >= 7 && a.in.W >= 7) {  // (frame >= window: the fast path's dead lanes read its top-left)
         // the paper's first layer (3 -> 4, 7x7, stride 1)
         PlanarFilters<3, 7, 7, 4> f;
         for (int r = 0; r < 3 * 7 * 7; ++r)
