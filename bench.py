@@ -263,9 +263,18 @@ def algorithmic_work(kernel, layer, st, S, dims, spec):
 def run_gpu_arm(args):
     import torch
     ws, rank, local = dist_env()
+    # one process per GPU over NCCL. CBX_BENCH_BACKEND=gloo with fewer GPUs
+    # than ranks (ranks share devices round-robin) exercises the multi-rank
+    # timing path on a one-GPU box; never used for reported numbers.
+    backend = os.environ.get("CBX_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
+    red_dev = f"cuda:{local}" if backend == "nccl" else None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     import paper_1704_04313_b200 as cbx
     from paper_1704_04313_b200 import shard
@@ -301,7 +310,7 @@ def run_gpu_arm(args):
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        return shard.max_over_ranks(e0.elapsed_time(e1), device=f"cuda:{local}")
+        return shard.max_over_ranks(e0.elapsed_time(e1), device=red_dev)
 
     clocks = Clocks(local)
     clocks.start()
@@ -443,7 +452,7 @@ def run_gpu_arm(args):
                 net.forward_device(p2(i))
             e1.record(stream)
             torch.cuda.synchronize()
-            m2 = shard.max_over_ranks(e0.elapsed_time(e1), device=f"cuda:{local}")
+            m2 = shard.max_over_ranks(e0.elapsed_time(e1), device=red_dev)
             sweep[r] = {"fps": round(shard.aggregate_rate(ws, S * K, m2), 1),
                         "l1_input_changed": float(np.mean([s[cb[0]]["changedInputPixels"] for s in stt])) / (args.height * args.width),
                         "speedup_vs_dense": round(shard.aggregate_rate(ws, S * K, m2) / dense_fps, 2)}
@@ -477,7 +486,7 @@ def run_gpu_arm(args):
         torch.cuda.synchronize()
         t = time.perf_counter()
         run_pipelined(4, K)
-        wall = shard.max_over_ranks(time.perf_counter() - t, device=f"cuda:{local}")
+        wall = shard.max_over_ranks(time.perf_counter() - t, device=red_dev)
         # synchronous cbx_forward for comparison
         net.reset_state()
         for i in range(0, 4):
@@ -486,7 +495,7 @@ def run_gpu_arm(args):
         t = time.perf_counter()
         for i in range(4, 4 + K):
             net.forward(hostnp[pingpong(i, Fe)])
-        wall_sync = shard.max_over_ranks(time.perf_counter() - t, device=f"cuda:{local}")
+        wall_sync = shard.max_over_ranks(time.perf_counter() - t, device=red_dev)
         e2e = {"value": shard.aggregate_rate(ws, S * K, 1000.0 * wall), "unit": "frames/s",
                "h2d_bytes_per_step": S * 3 * args.height * args.width * 4, "d2h_bytes_per_step": S * lh * lw * 2,
                "api": "cbx_submit/cbx_wait (2 frames in flight, pinned host buffers)",
