@@ -609,9 +609,19 @@ __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a)
                 a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
             float4* dst = reinterpret_cast<float4*>(
                 a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp) + c4;
+            // the stored value is loaded with the window, so all loads are in flight together
+            const float4 o = (!FULL && a.chg.d) ? *dst : make_float4(0.f, 0.f, 0.f, 0.f);
             float4 m = *src;
             if (a.relu) {
                 m = make_float4(ref_relu(m.x), ref_relu(m.y), ref_relu(m.z), ref_relu(m.w));
+            } else if (a.window == 2) {
+                // 2x2 window (the paper's pools): same max sequence as below
+                const float4 v01 = src[c4n], v10 = src[rowq], v11 = src[rowq + c4n];
+                const float4 w[4] = {m, v01, v10, v11};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    m = make_float4(ref_max(m.x, w[k].x), ref_max(m.y, w[k].y), ref_max(m.z, w[k].z),
+                                    ref_max(m.w, w[k].w));
             } else {
                 for (int kj = 0; kj < a.window; ++kj)
                     for (int ki = 0; ki < a.window; ++ki) {
@@ -620,7 +630,6 @@ __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a)
                     }
             }
             if (!FULL && a.chg.d) {
-                const float4 o = *dst;
                 ch = ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) | ref_changed(m.z, o.z, a.tau) |
                      ref_changed(m.w, o.w, a.tau);
                 waddr = a.chg.d + (int64_t)s * a.chg.stride + (int64_t)y * wpr + (x >> 5);
