@@ -806,6 +806,8 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     t->pair = pair_mode > 0;
     t->Brows = t->pair ? t->Npad / 2 : t->Npad;
     t->ctas_per_sm = (!t->pair && t->Npad <= 128) ? 2 : 1;
+    if (const char* e = std::getenv("CBX_TC_CTAS_PER_SM"))  // tuning
+        if (!t->pair && t->Npad <= 128) t->ctas_per_sm = std::max(1, std::min(2, std::atoi(e)));
     const size_t b_bytes = (size_t)t->Brows * 128;
     t->tail_w_floats = (int)round_up(tail_floats, 4);
     const size_t fixed = 1024 + (size_t)t->NKB * kChunksPerKB * 4 + round_up(g.outChannels, 4) * 4 +
@@ -954,7 +956,8 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.nzero = -0.0f;
     if (tail) a.tail = *tail;
     const int tc = (tail && tail->n) ? (tail->cout[0] <= 8 ? 8 : 16) : 0;
-    const bool rowlane = in.Cp <= 4;
+    static const int rowlane_env = std::getenv("CBX_TC_ROWLANE") ? std::atoi(std::getenv("CBX_TC_ROWLANE")) : -1;
+    const bool rowlane = rowlane_env >= 0 ? rowlane_env != 0 : in.Cp <= 4;  // (env: tuning)
     if (t.pair) {
         const int64_t max_tiles = (full_count + 2 * kTileM - 1) / (2 * kTileM);
         const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, t.max_clusters));
