@@ -823,10 +823,9 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     if (fixed + (size_t)ns * (kABytes + b_bytes) > budget)
         throw Error(CBX_E_ARG, "tcgen05 conv: layer too wide for shared memory");
     t->stages = ns;
-    // CBX_TC_MAXCTAS caps the persistent grid of one-CTA-per-SM layers (tuning:
-    // SMs left free for the other lane's kernels)
-    if (const char* e = std::getenv("CBX_TC_MAXCTAS"))
-        if (t->ctas_per_sm == 1) t->max_ctas = std::max(1, std::atoi(e));
+    // CBX_TC_MAXCTAS caps the persistent grid (tuning: SMs left free for the
+    // other lane's kernels; tests: many tiles per CTA on small frames)
+    if (const char* e = std::getenv("CBX_TC_MAXCTAS")) t->max_ctas = std::max(1, std::atoi(e));
     t->smem = fixed + (size_t)ns * (kABytes + b_bytes);
     set_smem_attrs<0, false>();
     set_smem_attrs<8, false>();
@@ -960,7 +959,9 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     const bool rowlane = rowlane_env >= 0 ? rowlane_env != 0 : in.Cp <= 4;  // (env: tuning)
     if (t.pair) {
         const int64_t max_tiles = (full_count + 2 * kTileM - 1) / (2 * kTileM);
-        const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, t.max_clusters));
+        int64_t ccap = t.max_clusters;
+        if (t.max_ctas > 0) ccap = std::min<int64_t>(ccap, std::max(1, t.max_ctas / 2));
+        const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, ccap));
         cudaLaunchConfig_t cfg{};
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;

@@ -1,7 +1,8 @@
 """GPU: the tcgen05 (tf32) gathered convolution against the exact oracle,
 with an error bound derived from the operands: tf32 keeps 10 mantissa bits,
 so |y_tc - y_exact| <= 2^-9 * sum_r |w_r x_r| (+ fp32 accumulation slack).
-Shapes cover N split (304 = 256 + 48), N padding (52 -> 64, 8 -> 16),
+Shapes cover N split (304 = 128 + 176 with the split accumulator),
+N padding (52 -> 64, 8 -> 16),
 channel padding (Cin % 4 != 0), stride, asymmetric kernels and K-blocks
 straddling taps."""
 import numpy as np
@@ -32,6 +33,21 @@ CASES = [
 @pytest.mark.parametrize("cin,h,w,layer", CASES)
 def test_tc_layer_vs_exact(gpu, orc, cin, h, w, layer, pair):
     """pair: CBX_OPT_TC_PAIR (-1 auto = CTA pairs for N > 128, 0 single CTA, 1 pairs)."""
+    check_tc_layer(gpu, orc, cin, h, w, layer, pair)
+
+
+@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("cin,h,w,layer", [c for c in CASES if c[3]["outChannels"] >= 52])
+def test_tc_layer_many_tiles_per_cta(gpu, orc, monkeypatch, cin, h, w, layer, pair):
+    """The persistent loop across tiles: the grid capped at 2 CTAs
+    (CBX_TC_MAXCTAS, read at layer setup), so every CTA walks several tiles --
+    stage-ring and accumulator-parity continuation, and for N > 256 the split
+    accumulator's alternating tail columns and shared-column hand-off."""
+    monkeypatch.setenv("CBX_TC_MAXCTAS", "2")
+    check_tc_layer(gpu, orc, cin, h, w, layer, pair)
+
+
+def check_tc_layer(gpu, orc, cin, h, w, layer, pair):
     spec = two_layer(cin, h, w, layer)
     wts = orc.generate_weights(spec, 11)
     onet = orc.load_network(spec, wts)
@@ -59,11 +75,15 @@ def test_tc_layer_vs_exact(gpu, orc, cin, h, w, layer, pair):
         assert np.all(err <= bound), (float((err / bound).max()), float(err.max()))
 
 
-def test_fused_tail_equals_unfused(gpu, orc):
+@pytest.mark.parametrize("maxctas", [None, "3"])
+def test_fused_tail_equals_unfused(gpu, orc, monkeypatch, maxctas):
     """The per-pixel head (1x1 CONV, RELU, 1x1 CONV, CLASSIFY) run inside the
     last tcgen05 conv's epilogue gives bitwise the same labels, final
-    activation and stats as running every layer separately."""
+    activation and stats as running every layer separately (maxctas: grid
+    capped so each CTA walks several tiles)."""
     from netutil import paper_spec, stats_arr
+    if maxctas:
+        monkeypatch.setenv("CBX_TC_MAXCTAS", maxctas)
     spec = paper_spec(72, 112)
     w = orc.generate_weights(spec, 1)
     fused = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32", fuse_tail=True)
