@@ -265,6 +265,7 @@ struct TcArgs {
     // second's alternate between ovl_b[0] and ovl_b[1] by tile parity, so the
     // next tile's MMAs wait only for the shared columns to be drained
     int ovl, ovl_s, ovl_b0, ovl_b1;
+    int tap4x7;  // row-lane gather specialised for Cp = 4, 7x7 (NKB = 7)
     int relu;
     BitMask chg;
     float tau;
@@ -467,6 +468,37 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                     const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
                     base = a.in + (int64_t)s * a.in_ss +
                            ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
+                }
+                if (a.tap4x7) {
+                    // 4-channel input, 7x7 window (the paper's layer 2): a tap is
+                    // one 16-byte chunk, K-block kb holds taps 8kb..8kb+7, so
+                    // every copy is a row pointer + a compile-time offset (no
+                    // offset table, no per-copy address registers to recycle)
+                    const float* rowp[7];
+#pragma unroll
+                    for (int kj = 0; kj < 7; ++kj) rowp[kj] = base + (int64_t)kj * a.in_Wp * 4;
+#pragma unroll
+                    for (int kb = 0; kb < 7; ++kb, rg.next(NS)) {
+                        const uint32_t st = rg.st, ph = rg.ph;
+                        mbar_wait(&empty[st], ph ^ 1u);
+                        if (r == 0) {
+                            mbar_arrive_expect_tx(&full[st], b_bytes);
+                            bulk_g2s(sB + (size_t)st * b_bytes, Bw + (size_t)kb * a.Brows * kKBlock, b_bytes, &full[st]);
+                        }
+                        const uint32_t row = smem_u32(sA + (size_t)st * kABytes + r * 128);
+                        if (valid) {
+#pragma unroll
+                            for (int j = 0; j < kChunksPerKB; ++j) {
+                                const int t = kb * kChunksPerKB + j;
+                                if (t < 49)
+                                    cp_async16(row + ((j ^ swz) << 4), rowp[t / 7] + (t % 7) * 4, 16u);
+                                else
+                                    cp_async16(row + ((j ^ swz) << 4), a.in, 0u);
+                            }
+                        }
+                        cp_async_arrive_noinc(&full[st]);
+                    }
+                    continue;
                 }
                 for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
                     const uint32_t st = rg.st, ph = rg.ph;
@@ -939,6 +971,8 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.acc_cols = t.acc_cols;
     a.tmem_cols = t.tmem_cols;
     a.ovl = t.ovl;
+    static const bool no_tap4x7 = std::getenv("CBX_TC_NO_TAP4X7") != nullptr;  // (tuning)
+    a.tap4x7 = !no_tap4x7 && in.Cp == 4 && t.g.kernelH == 7 && t.g.kernelW == 7 && t.NKB == 7;
     a.ovl_s = t.ovl_s;
     a.ovl_b0 = t.ovl_b0;
     a.ovl_b1 = t.ovl_b1;
