@@ -660,8 +660,6 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             const bool valid = n < total;
             // index (and output address) resolved before waiting for the accumulator
             const int64_t g = valid ? (a.idx ? (int64_t)__ldg(a.idx + n) : n) : 0;
-            mbar_wait(&tfull[as], aph);
-            tc_fence_after();
             int s = 0, p = 0, y = 0, x = 0;
             float* dst = nullptr;
             if (valid) {
@@ -670,7 +668,14 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 y = p / a.Wo;
                 x = p - y * a.Wo;
                 dst = a.out + (int64_t)s * a.out_ss + ((int64_t)(y + a.out_hh) * a.out_Wp + (x + a.out_hw)) * a.out_Cp;
+                // the values this pixel overwrites (compare-before-write) are
+                // pulled into L2 while the MMAs run
+                if (a.chg.d && a.write_out)
+                    for (int b = 0; b < a.O * 4; b += 128)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(dst) + b));
             }
+            mbar_wait(&tfull[as], aph);
+            tc_fence_after();
             bool changed = false;
             const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16);
             // TMEM column of channel c0: one accumulator per stage, or (ovl)
