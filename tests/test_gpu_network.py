@@ -30,6 +30,8 @@ def run_pair(cbx, orc, spec, seed, cfg, frames, precision="exact", streams=1, ch
 @pytest.mark.parametrize("name,spec,seed,cfg,frames", [
     ("c1", c1_spec(), 1, dict(channels=16, height=128, width=128, sprites=[(24, 7, 0.9)], seed=2), 8),
     ("paper48", paper_spec(48, 64), 1, dict(channels=3, height=48, width=64, sprites=[(10, 2, 0.9)], noise=0.01, seed=3), 5),
+    # width not a multiple of 4 (scalar detection path), odd pooled sizes (27x37 -> 13x18)
+    ("paper_odd", paper_spec(54, 74), 1, dict(channels=3, height=54, width=74, sprites=[(9, 2, 0.9)], noise=0.01, seed=5), 5),
     ("tiny_tau0", tiny_spec(), 42, dict(channels=2, height=16, width=16, sprites=[(5, 1, 0.9)], noise=0.03, seed=7), 5),
     ("generic", generic_spec(), 5, dict(channels=3, height=37, width=45, sprites=[(6, 2, 0.8)], noise=0.015, seed=9), 6),
 ])
@@ -163,19 +165,20 @@ def test_tf32_tolerance(gpu, orc):
         assert (got.labels != want["labels"]).mean() <= 1e-3
 
 
-def test_tf32_mask_mismatch_counts(gpu, orc):
+@pytest.mark.parametrize("h,w", [(96, 128), (54, 74)])
+def test_tf32_mask_mismatch_counts(gpu, orc, h, w):
     """TF32 mode at the base taus (0.04, 0.05, 0.05) on a sprite clip: the
     per-CBCONV-layer changed-pixel mismatch counts against the oracle --
     popcount(detected_gpu XOR detected_ref) and |updated_gpu symdiff
     updated_ref| -- are 0 for layer 1 and bounded (<= 1% of the reference's
     count) for layers 2-3, where a tf32 activation can cross tau; labels within
-    0.1%. scripts/parity_report.py writes the same counts at 320x240 and 1080p
+    0.1% (at least one pixel). scripts/parity_report.py writes the same counts at 320x240 and 1080p
     against the compiled reference (profiles/r1_parity.json)."""
-    spec = paper_spec(96, 128, (0.04, 0.05, 0.05))
-    w = orc.generate_weights(spec, 1)
-    cfg = dict(channels=3, height=96, width=128, sprites=[(16, 3, 0.9), (10, 2, 0.9)], noise=0.0, seed=3)
-    onet = orc.load_network(spec, w)
-    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32")
+    spec = paper_spec(h, w, (0.04, 0.05, 0.05))
+    wts = orc.generate_weights(spec, 1)
+    cfg = dict(channels=3, height=h, width=w, sprites=[(16, 3, 0.9), (10, 2, 0.9)], noise=0.0, seed=3)
+    onet = orc.load_network(spec, wts)
+    net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="tf32")
     counts = []
     for f in range(5):
         fr = orc.synth_frame(cfg, f)
@@ -194,7 +197,8 @@ def test_tf32_mask_mismatch_counts(gpu, orc):
             else:
                 assert det_mis <= max(1, 0.01 * np.count_nonzero(dr)), (f, cb, det_mis)
                 assert upd_mis <= max(1, 0.01 * ur.size), (f, cb, upd_mis)
-        assert (got.labels != want["labels"]).mean() <= 1e-3
+        # 0.1 % of the label map, but at least one pixel (a 13x18 map has 234)
+        assert (got.labels != want["labels"]).sum() <= max(1, 1e-3 * got.labels.size)
     assert any(c[3] > 0 for c in counts if c[1] == 2)  # the clip reaches layer 3
 
 
