@@ -58,6 +58,7 @@ struct P {
     int iters;         // K-blocks
     int stages;
     int fillA, fillB;  // refill A (16 KB) / B (rows*128 B) per K-block with TMA
+    int sync_each;     // wait for each K-block's commit before the next (MMA round-trip latency)
     const uint8_t* gA; const uint8_t* gB;  // sources of the fills (L2-resident)
     long long* cyc;
 };
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(128, 1) probe(P p) {
                 }
             }
             if (PAIR) commit2(&empty[st]); else commit1(&empty[st]);
+            if (p.sync_each) mbar_wait(&empty[st], ph);
         }
         if (PAIR) commit2(done); else commit1(done);
     }
@@ -166,7 +168,7 @@ int main() {
     CK(cudaMalloc(&cyc, 1024 * sizeof(long long)));
     CK(cudaFuncSetAttribute(probe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
     CK(cudaFuncSetAttribute(probe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    struct Case { const char* name; int pair, N0, N1, fillA, fillB, stages; };
+    struct Case { const char* name; int pair, N0, N1, fillA, fillB, stages, sync_each = 0; };
     const Case cases[] = {
         {"M128 N256", 0, 256, 0, 0, 0, 3},
         {"M128 N128", 0, 128, 0, 0, 0, 3},
@@ -180,11 +182,13 @@ int main() {
         {"M128 N160+144 fillA+B s4", 0, 160, 144, 1, 1, 4},
         {"M256pair N160+144 fillA+B s4", 1, 160, 144, 1, 1, 4},
         {"M256pair N160+144 fillA+B s6", 1, 160, 144, 1, 1, 6},
+        {"M128 N64 commit+wait per K-block", 0, 64, 0, 0, 0, 3, 1},
+        {"M128 N160+144 commit+wait per K-blk", 0, 160, 144, 0, 0, 3, 1},
     };
     cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
     for (const Case& c : cases) {
         P p{}; p.pair = c.pair; p.N0 = c.N0; p.N1 = c.N1; p.iters = 4000; p.stages = c.stages;
-        p.fillA = c.fillA; p.fillB = c.fillB; p.gA = gA; p.gB = gB; p.cyc = cyc;
+        p.fillA = c.fillA; p.fillB = c.fillB; p.gA = gA; p.gB = gB; p.cyc = cyc; p.sync_each = c.sync_each;
         const int Brows = c.pair ? (c.N0 + c.N1) / 2 : c.N0 + c.N1;
         const size_t smem = 1024 + (size_t)c.stages * (16384 + Brows * 128) + 512;
         cudaLaunchConfig_t cfg{}; cudaLaunchAttribute at[1];
@@ -202,8 +206,8 @@ int main() {
         const int M = c.pair ? 256 : 128;
         const double flop_per_cta = 2.0 * M * (c.N0 + c.N1) * 32.0 * p.iters / (c.pair ? 2 : 1);
         const double tf = flop_per_cta * cfg.gridDim.x / (best * 1e-3) / 1e12;
-        printf("%-32s %8.3f ms  %7.1f TFLOP/s  %7.0f flop/clk/SM  (%.2f GHz eff)\n", c.name, best, tf, flop_per_cta / mc,
-               mc / (best * 1e-3) / 1e9);
+        printf("%-36s %8.3f ms  %7.1f TFLOP/s  %7.0f flop/clk/SM  (%.2f GHz eff)  %.0f clk/K-block\n", c.name, best, tf,
+               flop_per_cta / mc, mc / (best * 1e-3) / 1e9, mc / p.iters);
     }
     return 0;
 }
