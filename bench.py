@@ -372,14 +372,18 @@ def run_gpu_arm(args):
     bound = algorithmic_work(kname, klayer, per[(kname, klayer)][0][1], S, dims, specd)[1]
     amount = float(np.mean(amounts))
     peaks, peak_src = load_peaks()
+    # tensor peak per operand format: f16 = the measured dense bf16 rate, tf32 = half of it
+    def tensor_peak(layer):
+        bf16 = peaks.get("bf16_tflops", 1590.0)
+        return bf16 if net.layer_operands(layer) == "f16" else bf16 / 2.0
     if bound == "hbm":
         achieved = amount / (kms / 1000.0) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
     else:
         achieved = amount / (kms / 1000.0) / 1e12
-        tf32 = peaks.get("bf16_tflops", 1590.0) / 2.0
-        peak = tf32 if bound == "tensor" else 75.0
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s"}
+        peak = tensor_peak(klayer) if bound == "tensor" else 75.0
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "operands": net.layer_operands(klayer)}
     roof["frac"] = roof["achieved"] / roof["peak"]
     # DRAM bytes per launch of this kernel from the committed ncu --set full capture
     roof["traffic"] = None
@@ -396,7 +400,8 @@ def run_gpu_arm(args):
     roof["kernel"] = f"{kname}[layer {klayer}]"
     roof["kernel_share_of_step"] = kms / step_ms if step_ms else None
     roof["peak_source"] = (f"{peak_src} MEASURED_PEAKS.json" + ("" if bound == "hbm" else
-                           " (tf32 = bf16/2, tf32 not measured)" if bound == "tensor" else ""))
+                           (" (fp16 operands: the measured dense bf16 rate)" if net.layer_operands(klayer) == "f16"
+                            else " (tf32 = bf16/2, tf32 not measured)") if bound == "tensor" else ""))
     if bound == "fp32":
         roof["peak_source"] = "fp32 CUDA-core peak, nominal 75 TFLOP/s (exact mode)"
     roof["per_kernel_ms"] = {f"{n}[{l}]": round(v, 5) for (n, l), v in sorted(tot.items(), key=lambda kv: -kv[1])}
@@ -407,11 +412,12 @@ def run_gpu_arm(args):
         amt = float(np.mean([algorithmic_work(n, l, st_, S, dims, specd)[0] for _, st_ in v]))
         bnd = algorithmic_work(n, l, v[0][1], S, dims, specd)[1]
         pk = (peaks["hbm_gbs"] * 1e9 if bnd == "hbm" else
-              peaks.get("bf16_tflops", 1590.0) / 2.0 * 1e12 if bnd == "tensor" else 75.0e12)
+              tensor_peak(l) * 1e12 if bnd == "tensor" else 75.0e12)
         t_roof += amt / pk * 1000.0
     roof["frame"] = {"t_roof_ms": t_roof, "t_kernels_ms": step_ms,
                      "frac_vs_kernels": t_roof / step_ms if step_ms else None,
-                     "note": "sum of per-kernel roofline times (HBM 6.55 TB/s, tf32 bf16/2, fp32 75 TFLOP/s) vs the "
+                     "note": "sum of per-kernel roofline times (HBM 6.55 TB/s, tensor: bf16 rate for fp16 operands, "
+                             "half of it for tf32, fp32 75 TFLOP/s) vs the "
                              "serial sum of the kernels' event-timed durations; frac_vs_step is added against the "
                              "graph-timed step with lanes overlapping"}
 
@@ -530,11 +536,14 @@ def run_gpu_arm(args):
 
     roof["frame"]["t_step_ms"] = ms / K
     roof["frame"]["frac_vs_step"] = roof["frame"]["t_roof_ms"] / (ms / K) if ms else None
+    ops = [(k, net.layer_operands(k)) for k in spec.cb_layers()]
+    dtype_str = ("tensor cores, fp32 accumulate: " + ", ".join(f"layer {k} {o}" for k, o in ops)
+                 if args.precision == "tf32" else "f32 (exact)")
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "tf32 (fp32 accumulate; layer 1 exact fp32)" if args.precision == "tf32" else "f32 (exact)",
+            "dtype": dtype_str,
             "data": "synthetic",
             "config": {"workload": f"paper_like {args.width}x{args.height} x {S} streams/GPU, sprite recipe "
                                    f"{args.recipe}% (resident clips, inputs > L2: {S}x2 frames of "

@@ -117,6 +117,11 @@ CBX_API int cbx_create(const cbx_net_desc* net, int device, int num_streams, int
 CBX_API int cbx_create_ex(const cbx_net_desc* net, int device, int num_streams, int precision, int lanes,
                           cbx_ctx** out);
 CBX_API int cbx_num_lanes(const cbx_ctx* ctx);
+/* Operand format of layer `layer`'s convolution: 0 = fp32 on CUDA cores
+ * (exact reference order), 1 = tcgen05 kind::tf32, 2 = tcgen05 kind::f16
+ * (fp16 operands rounded to nearest, fp32 accumulation; wide layers fed by a
+ * MAXPOOL in tensor-core mode unless CBX_TC_F16=0 at creation), -1 = not a conv. */
+CBX_API int cbx_layer_operands(const cbx_ctx* ctx, int layer);
 CBX_API void cbx_destroy(cbx_ctx* ctx);
 
 /* Install the filters of conv layer `layer` (0-based index in the layer

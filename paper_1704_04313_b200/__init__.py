@@ -447,6 +447,10 @@ class Network:
     def num_lanes(self) -> int:
         return lib.cbx_num_lanes(self._h)
 
+    def layer_operands(self, layer: int) -> str:
+        """Operand format of a conv layer: 'fp32' (exact, CUDA cores), 'tf32' or 'f16' (tcgen05)."""
+        return {0: "fp32", 1: "tf32", 2: "f16"}.get(lib.cbx_layer_operands(self._h, layer), "none")
+
     def stream_handle(self) -> int:
         return lib.cbx_stream(self._h) or 0
 

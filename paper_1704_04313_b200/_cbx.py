@@ -105,10 +105,12 @@ lib.cbx_submit.argtypes = [VP, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_uint
 lib.cbx_wait.argtypes = [VP, C.c_int64, VP, VP]
 lib.cbx_worst_case_counts.argtypes = [VP, C.POINTER(C.c_int64)]
 lib.cbx_num_lanes.argtypes = [VP]
+lib.cbx_layer_operands.argtypes = [VP, C.c_int]
 
 # exported symbols declared in include/cbx.h (checked by tests without a GPU)
 EXPORTS = [
-    "cbx_last_error", "cbx_version", "cbx_chain_dims", "cbx_create", "cbx_create_ex", "cbx_num_lanes", "cbx_destroy",
+    "cbx_last_error", "cbx_version", "cbx_chain_dims", "cbx_create", "cbx_create_ex", "cbx_num_lanes", "cbx_layer_operands",
+    "cbx_destroy",
     "cbx_load_layer",
     "cbx_set_thresholds", "cbx_get_thresholds", "cbx_set_option", "cbx_reset", "cbx_forward", "cbx_forward_device",
     "cbx_submit", "cbx_wait", "cbx_worst_case_counts", "cbx_sync", "cbx_read_labels", "cbx_read_stats", "cbx_labels_device", "cbx_stream",

@@ -129,6 +129,9 @@ CBX_API int cbx_create(const cbx_net_desc* net, int device, int num_streams, int
 }
 
 CBX_API int cbx_num_lanes(const cbx_ctx* ctx) { return ctx && ctx->eng ? ctx->eng->lanes() : -1; }
+CBX_API int cbx_layer_operands(const cbx_ctx* ctx, int layer) {
+    return ctx && ctx->eng ? ctx->eng->lane(0).layer_operands(layer) : -1;
+}
 
 CBX_API void cbx_destroy(cbx_ctx* ctx) {
     if (!ctx) return;

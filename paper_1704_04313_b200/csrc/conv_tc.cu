@@ -34,6 +34,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "conv_tc.hpp"
 #include "engine.hpp"
 
@@ -98,6 +100,17 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
 // Instruction descriptor: D=f32, A=B=tf32, both K-major, M=128, N.
 __host__ __device__ constexpr uint32_t idesc_tf32(int N, int M = kTileM) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// Instruction descriptor: D=f32, A=B=f16, both K-major, M=128, N (kind::f16).
+__host__ __device__ constexpr uint32_t idesc_f16(int N, int M = kTileM) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -266,6 +279,8 @@ struct TcArgs {
     // next tile's MMAs wait only for the shared columns to be drained
     int ovl, ovl_s, ovl_b0, ovl_b1;
     int tap4x7;  // row-lane gather specialised for Cp = 4, 7x7 (NKB = 7)
+    int f16;     // operands are fp16 (kind::f16): the input is an fp16 shadow tensor
+                 // addressed in 4-byte units (in_Cp = fp16 channels / 2)
     int relu;
     BitMask chg;
     float tau;
@@ -601,8 +616,10 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         } else {
             // ================= MMA issuer (whole warp, one elected lane issues) =================
             const int M = PAIR ? 2 * kTileM : kTileM;
-            const uint32_t id0 = idesc_tf32(a.N0, M), id1 = idesc_tf32(a.N1 > 0 ? a.N1 : 16, M);
+            const uint32_t id0 = a.f16 ? idesc_f16(a.N0, M) : idesc_tf32(a.N0, M);
+            const uint32_t id1 = a.f16 ? idesc_f16(a.N1 > 0 ? a.N1 : 16, M) : idesc_tf32(a.N1 > 0 ? a.N1 : 16, M);
             const bool two = a.N1 > 0;
+            const bool f16 = a.f16 != 0;
             // B rows of the second instruction start after this CTA's share of the first
             const uint32_t b1_off = (uint32_t)(PAIR ? a.N0 / 2 : a.N0) * 128u;
             const uint64_t a_desc0 = smem_desc(smem_u32(sA)), b_desc0 = smem_desc(smem_u32(sB));
@@ -634,6 +651,9 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                             if constexpr (PAIR) {
                                 mma_tf32_pair(d, ad + 2 * k, bd + 2 * k, id0, accum);
                                 if (two) mma_tf32_pair(d + a.N0, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
+                            } else if (f16) {
+                                mma_f16(d, ad + 2 * k, bd + 2 * k, id0, accum);
+                                if (two) mma_f16(d1, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
                             } else {
                                 mma_tf32(d, ad + 2 * k, bd + 2 * k, id0, accum);
                                 if (two) mma_tf32(d1, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
@@ -760,6 +780,7 @@ struct TcLayer {
     int ctas_per_sm = 1;
     bool pair = false;   // CTA pair (cta_group::2, M = 256)
     bool ovl = false;    // split accumulator (see make_tc_layer)
+    bool f16 = false;    // fp16 operands (kind::f16): Cp counts 4-byte units of the fp16 shadow input
     int ovl_s = 0, ovl_b0 = 0, ovl_b1 = 0;
     int max_ctas = 0;    // persistent grid cap (0: one per SM x ctas_per_sm)
     int Brows = 0;       // filter rows per CTA
@@ -772,6 +793,8 @@ void TcLayerDeleter::operator()(TcLayer* p) const {
     if (p && p->Bw) cudaFree(p->Bw);
     delete p;
 }
+
+bool tc_is_f16(const TcLayer& t) { return t.f16; }
 
 bool tc_supported(const cbx_geom& g) {
     const int Npad = (int)round_up(g.outChannels, 16);
@@ -790,10 +813,14 @@ void set_smem_attrs() {
 }
 }  // namespace
 
-std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats, int pair_mode) {
+std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats, int pair_mode, bool f16) {
     std::unique_ptr<TcLayer, TcLayerDeleter> t(new TcLayer);
     t->g = g;
-    t->Cp = (int)round_up(g.inChannels, 4);
+    // fp16 operands: 8 channels per 16-byte chunk; Cp stays in 4-byte units so
+    // the gather's address arithmetic is the same for both operand types
+    t->f16 = f16;
+    if (f16) pair_mode = 0;
+    t->Cp = f16 ? (int)round_up(g.inChannels, 8) / 2 : (int)round_up(g.inChannels, 4);
     const int nchunks = g.kernelH * g.kernelW * (t->Cp / 4);
     t->NKB = (nchunks + kChunksPerKB - 1) / kChunksPerKB;
     t->Npad = (int)round_up(g.outChannels, 16);
@@ -904,6 +931,27 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
     const int C4 = t.Cp / 4, khw = g.kernelH * g.kernelW;
     const int Kref = g.inChannels * khw;
     const int ranks = t.pair ? 2 : 1;
+    if (t.f16) {
+        // fp16 image (round to nearest even): chunk J = tap * C4 + c4 holds
+        // channels 8*c4 .. 8*c4+7 of that tap; half (n, kb*64 + j*8 + e) at
+        // kb*Npad*64 + n*64 + (j ^ (n & 7))*8 + e
+        std::vector<__half> img((size_t)t.NKB * t.Brows * 64, __float2half_rn(0.0f));
+        for (int n = 0; n < g.outChannels; ++n)
+            for (int J = 0; J < t.NKB * kChunksPerKB; ++J) {
+                const int tap = J / C4, c4 = J - tap * C4;
+                if (tap >= khw) continue;
+                const int kb = J / kChunksPerKB, j = J - kb * kChunksPerKB;
+                for (int e = 0; e < 8; ++e) {
+                    const int c = c4 * 8 + e;
+                    if (c >= g.inChannels) continue;
+                    img[(size_t)kb * t.Brows * 64 + (size_t)n * 64 + ((j ^ (n & 7)) * 8) + e] =
+                        __float2half_rn(K[(size_t)n * Kref + (size_t)c * khw + tap]);
+                }
+            }
+        CBX_CUDA(cudaMemcpyAsync(t.Bw, img.data(), img.size() * sizeof(__half), cudaMemcpyHostToDevice, st));
+        CBX_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
     std::vector<float> img((size_t)ranks * t.NKB * t.Brows * kKBlock, 0.0f);
     for (int n = 0; n < g.outChannels; ++n) {
         int rank = 0, row = n;
@@ -976,6 +1024,7 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.acc_cols = t.acc_cols;
     a.tmem_cols = t.tmem_cols;
     a.ovl = t.ovl;
+    a.f16 = t.f16;
     static const bool no_tap4x7 = std::getenv("CBX_TC_NO_TAP4X7") != nullptr;  // (tuning)
     a.tap4x7 = !no_tap4x7 && in.Cp == 4 && t.g.kernelH == 7 && t.g.kernelW == 7 && t.NKB == 7;
     a.ovl_s = t.ovl_s;

@@ -38,7 +38,11 @@ struct TcTail {
 bool tc_supported(const cbx_geom& g);
 // tail_floats: shared memory (floats) to reserve for a fused tail's first 1x1 conv.
 // pair_mode: -1 = auto (single-CTA tiles), 0 = never, 1 = CTA pairs (cta_group::2).
-std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats = 0, int pair_mode = -1);
+// f16: fp16 operands (kind::f16) read from an fp16 shadow of the input whose
+// TensorView counts channels in 4-byte units (tc_input_cp).
+std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats = 0, int pair_mode = -1,
+                                                       bool f16 = false);
+bool tc_is_f16(const TcLayer& t);
 // K in the reference layout [O][Cin*kh*kw], columns (c,kj,ki); host memory.
 void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st);
 void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float* bias,

@@ -132,6 +132,7 @@ std::vector<int> chain_dims(const cbx_net_desc& net, std::vector<cbx_layer_desc>
 struct Engine::Plan {
     bool baseline = false;
     std::vector<TensorView> T;      // nl+1; T[0] = frame (planar) unless ingested
+    std::vector<TensorView> T16;    // nl+1; fp16 shadows (4-byte channel units) of kind::f16 conv inputs
     bool ingest = false;            // first layer is not a conv: frame copied to HWC T[0]
     std::vector<BitMask> chg;       // nl+1
     std::vector<bool> chg_by_conv;  // chg written with 1s only -> cleared per frame
@@ -208,7 +209,15 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
                 const int te = tail_end(k);
                 const int c1 = te > 0 ? layers_[k + 1].geom.outChannels : 0;
                 const int tail_floats = te > 0 ? (c1 <= 8 ? 8 : 16) * g.outChannels : 0;
-                tc_[k] = make_tc_layer(g, tail_floats);
+                // fp16 operands (kind::f16: 10 explicit mantissa bits like tf32,
+                // twice the rate, half the bytes) for a wide layer fed by a
+                // MAXPOOL, which also writes an fp16 (round-to-nearest) shadow of
+                // its output. Read at construction; CBX_TC_F16=0 keeps tf32.
+                const char* f16_env = std::getenv("CBX_TC_F16");
+                const bool f16 = !(f16_env && std::atoi(f16_env) == 0) && g.outChannels > 128 &&
+                                 layers_[k - 1].kind == CBX_MAXPOOL;
+                if (f16) f16_layers_.push_back(k);
+                tc_[k] = make_tc_layer(g, tail_floats, -1, f16);
             }
         }
     }
@@ -251,6 +260,12 @@ Engine::~Engine() {
     if (h_ring_stats_) cudaFreeHost(h_ring_stats_);
     if (copy_st_) cudaStreamDestroy(copy_st_);
     if (stream_) cudaStreamDestroy(stream_);
+}
+
+int Engine::layer_operands(int layer) const {
+    if (layer < 0 || layer >= (int)layers_.size() || !is_conv(layers_[layer].kind)) return -1;
+    if (!tc_[layer]) return 0;
+    return tc_is_f16(*tc_[layer]) ? 2 : 1;
 }
 
 Engine::Plan& Engine::plan(int engine) {
@@ -319,6 +334,14 @@ void Engine::build_plan(Plan& p, bool baseline) {
             continue;
         }
         alloc_tensor(k + 1);
+    }
+    p.T16.assign(nl + 1, TensorView{});
+    for (int k : f16_layers_) {
+        TensorView v = p.T[k];
+        v.Cp = (int)round_up(v.C, 8) / 2;
+        v.ss = round_up((int64_t)v.Hp * v.Wp * v.Cp, 64);
+        v.d = p.alloc<float>((size_t)(v.ss * S));
+        p.T16[k] = v;
     }
     if (p.T[0].d == nullptr) {
         int c, h, w;
@@ -529,13 +552,13 @@ void Engine::record(Plan& p, bool full) {
                     t.fo_hw = fo.hw;
                     t.labels = p.labels;
                     t.l_ss = (int64_t)lh_ * lw_;
-                    launch_conv_tc(*tc_[k], p.T[k], p.T[k + 1], dBias_[k], idx, count, full_count, relu,
+                    launch_conv_tc(*tc_[k], p.T16[k].d ? p.T16[k] : p.T[k], p.T[k + 1], dBias_[k], idx, count, full_count, relu,
                                    chg_next, tau_next, cnt_next, 2, S, st, &t);
                     mark("conv_tc_tail", k);
                     p.fused_from = k;
                     break;
                 } else if (tc_[k] && !planar_in) {
-                    launch_conv_tc(*tc_[k], p.T[k], p.T[k + 1], dBias_[k], idx, count, full_count, relu,
+                    launch_conv_tc(*tc_[k], p.T16[k].d ? p.T16[k] : p.T[k], p.T[k + 1], dBias_[k], idx, count, full_count, relu,
                                    chg_next, tau_next, cnt_next, 2, S, st);
                     mark("conv_tc", k);
                 } else {
@@ -585,6 +608,7 @@ void Engine::record(Plan& p, bool full) {
                 a.work = p.work;
                 a.work_count = p.wcount_k.empty() ? nullptr : p.wcount_k[k];  // (sparse frames only)
                 a.count_zeroed = 1;
+                a.out16 = p.T16[k + 1];
                 launch_point_bits(a, st);
                 mark(a.relu ? "relu" : "pool", k);
                 break;
@@ -1086,7 +1110,7 @@ void Engine::set_option(int option, int value) {
             const int tail_floats = te > 0 ? (c1 <= 8 ? 8 : 16) * g.outChannels : 0;
             std::vector<float> K((size_t)g.outChannels * g.inChannels * g.kernelH * g.kernelW);
             CBX_CUDA(cudaMemcpy(K.data(), dK_[k], K.size() * sizeof(float), cudaMemcpyDeviceToHost));
-            tc_[k] = make_tc_layer(g, tail_floats, value);
+            tc_[k] = make_tc_layer(g, tail_floats, value, tc_is_f16(*tc_[k]));
             tc_load_weights(*tc_[k], K.data(), stream_);
         }
     } else if (option == CBX_OPT_FUSE_TAIL) {

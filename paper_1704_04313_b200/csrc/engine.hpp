@@ -107,7 +107,13 @@ private:
     std::vector<float*> dK_, dBias_;
     std::vector<std::vector<float>> hK_, hB_;  // host copies (kernel-parameter filters)
     std::vector<std::unique_ptr<TcLayer, TcLayerDeleter>> tc_;
+    std::vector<int> f16_layers_;  // tcgen05 layers with fp16 operands (their input has an fp16 shadow)
 
+public:
+    // 0 = exact fp32 (CUDA cores), 1 = tcgen05 tf32, 2 = tcgen05 f16, -1 = not a conv
+    int layer_operands(int layer) const;
+
+private:
     std::unique_ptr<Plan> cb_, base_;
     bool has_history_ = false;
 

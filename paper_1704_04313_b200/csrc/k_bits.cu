@@ -14,6 +14,7 @@
 //                         baseline.cpp:113-145, fused with the next
 //                         layer's change detection
 //   classify_bits      <- argmax_classify  baseline.cpp:147-163
+#include <cuda_fp16.h>
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -635,6 +636,14 @@ __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a)
                 waddr = a.chg.d + (int64_t)s * a.chg.stride + (int64_t)y * wpr + (x >> 5);
             }
             *dst = m;
+            if (a.out16.d) {
+                const __half2 h01 = __floats2half2_rn(m.x, m.y), h23 = __floats2half2_rn(m.z, m.w);
+                uint2 hv;
+                hv.x = *reinterpret_cast<const uint32_t*>(&h01);
+                hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+                reinterpret_cast<uint2*>(a.out16.d + (int64_t)s * a.out16.ss +
+                                         ((int64_t)(y + a.out16.hh) * a.out16.Wp + x + a.out16.hw) * a.out16.Cp)[c4] = hv;
+            }
         }
         if (!FULL && a.chg.d) {
             // one atomicOr per distinct mask word in the warp

@@ -45,6 +45,9 @@ struct PointBitsArgs {  // MAXPOOL (window/stride) or RELU (relu=1, window=strid
     uint32_t* work;   // touched-pixel list s*Ho*Wo + y*Wo + x (capacity S*Ho*Wo), sparse mode only
     int* work_count;
     int count_zeroed;  // work_count already zeroed in-stream (frame scratch memset)
+    // optional fp16 shadow of `out` (round to nearest even) for a kind::f16
+    // consumer; channels counted in 4-byte units (Cp = fp16 channels / 2)
+    TensorView out16;
 };
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st);
 void launch_classify_bits(TensorView in, BitMask upd, uint16_t* labels, int S, cudaStream_t st);

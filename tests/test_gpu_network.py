@@ -143,10 +143,13 @@ def test_multistream_independent(gpu, orc):
                 assert np.array_equal(net.trace(cb, s)[1], onets[s].trace(cb)[1])
 
 
-def test_tf32_tolerance(gpu, orc):
-    """TF32 (tcgen05) mode at tau=0: layer-1 masks/indices/outputs bit-exact,
+@pytest.mark.parametrize("f16", ["1", "0"])
+def test_tf32_tolerance(gpu, orc, monkeypatch, f16):
+    """Tensor-core mode at tau=0: layer-1 masks/indices/outputs bit-exact,
     final activations within 1e-3 max-abs, labels within 0.1% (tau > 0:
-    test_tf32_mask_mismatch_counts)."""
+    test_tf32_mask_mismatch_counts). f16: layer 3 with fp16 operands (the
+    default) or tf32 (CBX_TC_F16=0)."""
+    monkeypatch.setenv("CBX_TC_F16", f16)
     spec = paper_spec(64, 96, (0.0, 0.0, 0.0))
     w = orc.generate_weights(spec, 1)
     cfg = dict(channels=3, height=64, width=96, sprites=[(12, 2, 0.9)], noise=0.01, seed=3)
@@ -165,8 +168,8 @@ def test_tf32_tolerance(gpu, orc):
         assert (got.labels != want["labels"]).mean() <= 1e-3
 
 
-@pytest.mark.parametrize("h,w", [(96, 128), (54, 74)])
-def test_tf32_mask_mismatch_counts(gpu, orc, h, w):
+@pytest.mark.parametrize("h,w,f16", [(96, 128, "1"), (54, 74, "1"), (96, 128, "0")])
+def test_tf32_mask_mismatch_counts(gpu, orc, monkeypatch, h, w, f16):
     """TF32 mode at the base taus (0.04, 0.05, 0.05) on a sprite clip: the
     per-CBCONV-layer changed-pixel mismatch counts against the oracle --
     popcount(detected_gpu XOR detected_ref) and |updated_gpu symdiff
@@ -174,6 +177,7 @@ def test_tf32_mask_mismatch_counts(gpu, orc, h, w):
     count) for layers 2-3, where a tf32 activation can cross tau; labels within
     0.1% (at least one pixel). scripts/parity_report.py writes the same counts at 320x240 and 1080p
     against the compiled reference (profiles/r1_parity.json)."""
+    monkeypatch.setenv("CBX_TC_F16", f16)
     spec = paper_spec(h, w, (0.04, 0.05, 0.05))
     wts = orc.generate_weights(spec, 1)
     cfg = dict(channels=3, height=h, width=w, sprites=[(16, 3, 0.9), (10, 2, 0.9)], noise=0.0, seed=3)
@@ -200,6 +204,22 @@ def test_tf32_mask_mismatch_counts(gpu, orc, h, w):
         # 0.1 % of the label map, but at least one pixel (a 13x18 map has 234)
         assert (got.labels != want["labels"]).sum() <= max(1, 1e-3 * got.labels.size)
     assert any(c[3] > 0 for c in counts if c[1] == 2)  # the clip reaches layer 3
+
+
+def test_layer_operands(gpu, orc, monkeypatch):
+    """Operand formats reported per conv layer: layer 1 exact fp32 (planar
+    first layer), layer 2 tf32, layer 3 fp16 (fed by a MAXPOOL, default) or
+    tf32 with CBX_TC_F16=0; the head's 1x1 convs exact; exact mode fp32 only."""
+    spec = paper_spec(32, 48)
+    w = orc.generate_weights(spec, 1)
+    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32")
+    assert [net.layer_operands(k) for k in (0, 2, 4, 5)] == ["fp32", "tf32", "f16", "fp32"]
+    assert net.layer_operands(1) == "none"  # MAXPOOL
+    monkeypatch.setenv("CBX_TC_F16", "0")
+    net2 = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32")
+    assert net2.layer_operands(4) == "tf32"
+    ex = gpu.Network(to_pkg_spec(gpu, spec), w, precision="exact")
+    assert all(ex.layer_operands(k) == "fp32" for k in (0, 2, 4))
 
 
 def test_errors(gpu, orc):

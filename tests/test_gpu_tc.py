@@ -75,8 +75,8 @@ def check_tc_layer(gpu, orc, cin, h, w, layer, pair):
         assert np.all(err <= bound), (float((err / bound).max()), float(err.max()))
 
 
-@pytest.mark.parametrize("maxctas", [None, "3"])
-def test_fused_tail_equals_unfused(gpu, orc, monkeypatch, maxctas):
+@pytest.mark.parametrize("maxctas,f16", [(None, "1"), ("3", "1"), (None, "0")])
+def test_fused_tail_equals_unfused(gpu, orc, monkeypatch, maxctas, f16):
     """The per-pixel head (1x1 CONV, RELU, 1x1 CONV, CLASSIFY) run inside the
     last tcgen05 conv's epilogue gives bitwise the same labels, final
     activation and stats as running every layer separately (maxctas: grid
@@ -84,6 +84,7 @@ def test_fused_tail_equals_unfused(gpu, orc, monkeypatch, maxctas):
     from netutil import paper_spec, stats_arr
     if maxctas:
         monkeypatch.setenv("CBX_TC_MAXCTAS", maxctas)
+    monkeypatch.setenv("CBX_TC_F16", f16)
     spec = paper_spec(72, 112)
     w = orc.generate_weights(spec, 1)
     fused = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32", fuse_tail=True)
