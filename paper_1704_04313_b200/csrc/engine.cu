@@ -216,7 +216,10 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
                 const char* f16_env = std::getenv("CBX_TC_F16");
                 const bool f16 = !(f16_env && std::atoi(f16_env) == 0) && g.outChannels > 128 &&
                                  layers_[k - 1].kind == CBX_MAXPOOL;
-                if (f16) f16_layers_.push_back(k);
+                if (f16) {
+                    f16_layers_.push_back(k);
+                    if (!d_f16_ovf_) d_f16_ovf_ = dmalloc<int>(1);
+                }
                 tc_[k] = make_tc_layer(g, tail_floats, -1, f16);
             }
         }
@@ -248,6 +251,7 @@ Engine::~Engine() {
     tc_.clear();
     for (float* p : dK_) cudaFree(p);
     for (float* p : dBias_) cudaFree(p);
+    if (d_f16_ovf_) cudaFree(d_f16_ovf_);
     cudaFree(d_cur_);
     for (auto& s : slots_) cudaFree(s);
     cudaFreeHost(h_stats_);
@@ -609,6 +613,7 @@ void Engine::record(Plan& p, bool full) {
                 a.work_count = p.wcount_k.empty() ? nullptr : p.wcount_k[k];  // (sparse frames only)
                 a.count_zeroed = 1;
                 a.out16 = p.T16[k + 1];
+                a.f16_overflow = p.T16[k + 1].d ? d_f16_ovf_ : nullptr;
                 launch_point_bits(a, st);
                 mark(a.relu ? "relu" : "pool", k);
                 break;
@@ -775,6 +780,7 @@ void Engine::wait(int64_t ticket, cbx_layer_stats* stats, uint64_t* macs) {
         throw Error(CBX_E_ARG, "cbx_wait: unknown or expired ticket (at most the last 3 submissions can be waited on)");
     CBX_CUDA(cudaSetDevice(device_));
     CBX_CUDA(cudaEventSynchronize(done_[q]));
+    check_f16_overflow();
     const int nl = (int)layers_.size();
     std::vector<cbx_layer_stats> st((size_t)S_ * nl);
     std::vector<uint64_t> mc(S_);
@@ -825,6 +831,18 @@ void Engine::stats_from(const unsigned long long* hs, bool full, int engine, cbx
     }
 }
 
+void Engine::check_f16_overflow() {
+    if (!d_f16_ovf_) return;
+    int h = 0;
+    CBX_CUDA(cudaMemcpy(&h, d_f16_ovf_, sizeof(int), cudaMemcpyDeviceToHost));
+    if (h) {
+        CBX_CUDA(cudaMemset(d_f16_ovf_, 0, sizeof(int)));
+        throw Error(CBX_E_ARG,
+                    "fp16 operand overflow: an input of a kind::f16 layer exceeded 65504 in magnitude "
+                    "(create the context with CBX_TC_F16=0 to keep tf32 operands)");
+    }
+}
+
 void Engine::read_stats(int engine, cbx_layer_stats* stats, uint64_t* macs) {
     if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
     if (stats_pending_[engine]) {
@@ -837,6 +855,7 @@ void Engine::read_stats(int engine, cbx_layer_stats* stats, uint64_t* macs) {
     } else {
         sync();
     }
+    check_f16_overflow();
     const int nl = (int)layers_.size();
     if (stats) std::memcpy(stats, last_stats_[engine].data(), sizeof(cbx_layer_stats) * S_ * nl);
     if (macs) std::memcpy(macs, last_macs_[engine].data(), sizeof(uint64_t) * S_);

@@ -637,6 +637,10 @@ __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a)
             }
             *dst = m;
             if (a.out16.d) {
+                // fp16 operands are only valid below 65504 in magnitude: flag it (the
+                // host raises an error when the frame's stats are read)
+                if (a.f16_overflow && fmaxf(fmaxf(fabsf(m.x), fabsf(m.y)), fmaxf(fabsf(m.z), fabsf(m.w))) > 65504.0f)
+                    atomicOr(a.f16_overflow, 1);
                 const __half2 h01 = __floats2half2_rn(m.x, m.y), h23 = __floats2half2_rn(m.z, m.w);
                 uint2 hv;
                 hv.x = *reinterpret_cast<const uint32_t*>(&h01);

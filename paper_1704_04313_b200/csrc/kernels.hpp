@@ -48,6 +48,7 @@ struct PointBitsArgs {  // MAXPOOL (window/stride) or RELU (relu=1, window=strid
     // optional fp16 shadow of `out` (round to nearest even) for a kind::f16
     // consumer; channels counted in 4-byte units (Cp = fp16 channels / 2)
     TensorView out16;
+    int* f16_overflow;  // set to 1 when a value written to out16 exceeds the fp16 range
 };
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st);
 void launch_classify_bits(TensorView in, BitMask upd, uint16_t* labels, int S, cudaStream_t st);

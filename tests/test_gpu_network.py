@@ -222,6 +222,23 @@ def test_layer_operands(gpu, orc, monkeypatch):
     assert all(ex.layer_operands(k) == "fp32" for k in (0, 2, 4))
 
 
+def test_f16_overflow_reported(gpu, orc, monkeypatch):
+    """Layer 3's fp16 operands only cover |x| <= 65504: when its input exceeds
+    that (filters scaled so pool-2 outputs reach ~1e6) the frame reports an
+    error instead of silently computing with inf; tf32 operands
+    (CBX_TC_F16=0) take the same frame."""
+    spec = paper_spec(32, 48, (0.0, 0.0, 0.0))
+    w = orc.generate_weights(spec, 1)
+    big = {k: ((K * 1000.0).astype(K.dtype) if k in (0, 2) else K, b) for k, (K, b) in w.items()}
+    fr = orc.synth_frame(dict(channels=3, height=32, width=48, sprites=[(6, 2, 0.9)], noise=0.0, seed=1), 0)
+    net = gpu.Network(to_pkg_spec(gpu, spec), big, precision="tf32")
+    with pytest.raises(gpu.CbxError, match="fp16 operand overflow"):
+        net.forward_frame(fr)
+    monkeypatch.setenv("CBX_TC_F16", "0")
+    net2 = gpu.Network(to_pkg_spec(gpu, spec), big, precision="tf32")
+    net2.forward_frame(fr)
+
+
 def test_errors(gpu, orc):
     spec = paper_spec(32, 48)
     w = orc.generate_weights(spec, 1)
