@@ -250,7 +250,7 @@ struct PlanarFilters {
 };
 
 template <int C, int KH, int KW, int OC>
-__global__ void __launch_bounds__(kConvThreads, 4) conv_planar_fixed_kernel(ConvArgs a,
+__global__ void __launch_bounds__(kConvThreads, 8) conv_planar_fixed_kernel(ConvArgs a,
                                                                             const __grid_constant__ PlanarFilters<C, KH, KW, OC> f) {
     const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
     const int Wo = a.out.W, H = a.in.H, W = a.in.W;
