@@ -54,12 +54,15 @@ def parse():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--recipe", default="2.2", choices=sorted(RECIPES))
-    ap.add_argument("--precision", default="tf32", choices=["tf32", "exact"])
+    ap.add_argument("--precision", default="f16", choices=["f16", "tf32", "exact"],
+                    help="f16: layer 3 kind::f16 (fp16 operands), layer 2 kind::tf32, layer 1 exact fp32; "
+                         "tf32: kind::tf32 for layers 2-3; exact: fp32 reference order everywhere")
     ap.add_argument("--frames", type=int, default=12, help="resident clip length per stream")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline sampling")
-    ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds for --impl reference timing")
+    ap.add_argument("--ref-budget", type=float, default=60.0, help="seconds for --impl reference timing")
+    ap.add_argument("--no-cudnn", action="store_true", help="skip the torch/cuDNN dense cross-check")
     ap.add_argument("--sweep", action="store_true", help="also report fps at every recipe")
     return ap.parse_args()
 
@@ -149,10 +152,12 @@ def cpu_reference_run(args, budget, max_streams, log=print):
     compiled from its sources; else the oracle's C restatement) on this host:
     P streams, one thread each (the reference is single-threaded; distinct
     Networks may run concurrently), steady-state frames of the
-    same workload. Untimed warm-up: frame 0 evaluated in full with the
-    reference's own ops split over all cores (bitwise equal to its serial
-    first frame), copied into every stream, then one steady frame."""
+    same workload: stream g plays the clip of seed shard.stream_seed(g), as in
+    the GPU arm. Untimed warm-up: each stream's frame 0 evaluated in full with
+    the reference's own ops split over all cores (bitwise equal to its serial
+    first frame), then one steady frame."""
     import oracle
+    from paper_1704_04313_b200 import shard
     nproc = os.cpu_count() or 1
     try:
         import psutil
@@ -177,48 +182,48 @@ def cpu_reference_run(args, budget, max_streams, log=print):
         nets = [orc.load_network(spec, w) for _ in range(P)]
         fwd = lambda n, fr: n.forward_frame(fr)
         synth = orc.synth_frame
-    cfg = clip_cfg(args, 1)
+    cfgs = [clip_cfg(args, shard.stream_seed(g)) for g in range(P)]
     t0 = time.perf_counter()
-    nets[0].warm(synth(cfg, 0), nproc)
-    for n in nets[1:]:
-        n.copy_state_from(nets[0])
+    for n, cfg in zip(nets, cfgs):
+        n.warm(synth(cfg, 0), nproc)
     log(f"[cpu] {kind}: {P} streams, warm-up {time.perf_counter() - t0:.1f}s on {nproc} threads")
 
-    def step(fr):
-        ts = [threading.Thread(target=fwd, args=(n, fr)) for n in nets]
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-
-    step(synth(cfg, 1))  # first steady frame, untimed
-    frames, elapsed, i = 0, 0.0, 2
-    while True:
-        fr = synth(cfg, pingpong(i, args.frames))
+    def step(i):
+        frs = [synth(cfg, pingpong(i, args.frames)) for cfg in cfgs]
         t = time.perf_counter()
-        step(fr)
-        elapsed += time.perf_counter() - t
+        ts = [threading.Thread(target=fwd, args=(n, fr)) for n, fr in zip(nets, frs)]
+        for th in ts:
+            th.start()
+        for th in ts:
+            th.join()
+        return time.perf_counter() - t
+
+    step(1)  # first steady frame, untimed
+    frames, elapsed, timed = 0, 0.0, 0
+    while timed < max(1, args.steps) and (elapsed < budget or timed == 0):
+        elapsed += step(2 + timed)
         frames += P
-        i += 1
-        if elapsed >= budget or i - 2 >= args.steps:
-            break
+        timed += 1
     fps = frames / elapsed
-    sample = (f"{i - 2} steps x {P} streams of {args.width}x{args.height} paper_like, recipe {args.recipe}% "
-              f"(same clip per stream), steady-state frames, {elapsed:.1f}s timed")
-    return dict(value=fps, unit="frames/s", cores=P, kind=kind, sample=sample)
+    sample = (f"{timed} steps x {P} streams of {args.width}x{args.height} paper_like, recipe {args.recipe}% "
+              f"(stream g: clip seed g+1, as the GPU arm), steady-state frames, {elapsed:.1f}s timed")
+    return dict(value=fps, unit="frames/s", cores=P, kind=kind, sample=sample, steps=timed,
+                threads_available=nproc)
 
 
 def run_reference_arm(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return
-    res = cpu_reference_run(args, args.ref_budget, 64, log=lambda *a: print(*a, file=sys.stderr))
+    res = cpu_reference_run(args, args.ref_budget, args.streams, log=lambda *a: print(*a, file=sys.stderr))
     line = {"metric": METRIC, "value": res["value"], "unit": "frames/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * res["cores"] / res["value"],
+            "steps": res["steps"], "warmup": args.warmup, "ms_per_step": 1000.0 * res["cores"] / res["value"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": f"paper_like {args.width}x{args.height}, sprite recipe {args.recipe}% L1 change",
-                       "streams": res["cores"], "taus": list(BASE_TAUS)},
+                       "streams": res["cores"], "taus": list(BASE_TAUS),
+                       "clips": "stream g: synth clip seed g+1 (shard.stream_seed), as the GPU arm",
+                       "steps_requested": args.steps},
             "cpu_baseline": res,
             "e2e": {"value": res["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -229,12 +234,12 @@ def algorithmic_work(kernel, layer, st, S, dims, spec):
     """Algorithmic bytes or flops of one launch, from the
     frame's counters. Returns (amount, 'hbm'|'tensor'|'fp32')."""
     inC, inH, inW = dims[layer][0] if layer >= 0 and layer < len(dims) else (0, 0, 0)
-    if kernel == "detect":
+    if kernel == "detect":  # read both frames, write the change mask as bits
         c, h, w = dims[0][0]
-        return S * (2 * c * h * w * 4 + h * w), "hbm"
-    if kernel == "dilate":
+        return S * (2 * c * h * w * 4 + h * w // 8), "hbm"
+    if kernel == "dilate":  # mask bits in, mask bits out
         (_, h, w), (_, ho, wo) = dims[layer]
-        return S * (h * w + ho * wo), "hbm"
+        return S * (h * w + ho * wo) // 8, "hbm"
     if kernel == "dilate_compact":  # read the input mask bits, write U bits + the index list
         (_, h, w), (_, ho, wo) = dims[layer]
         n = sum(s[layer]["changedOutputPixels"] for s in st)
@@ -264,6 +269,65 @@ def algorithmic_work(kernel, layer, st, S, dims, spec):
     return 0, "hbm"
 
 
+def cudnn_dense_fps(specd, weights, clip, S, K, dt, barrier, red_dev, ws):
+    """Dense per-frame cross-check of the in-repo dense engine: the same
+    network through torch conv2d / max_pool2d (cuDNN), channels_last, batch =
+    the S streams of one step, tf32 math or fp16 tensors (fp32 biases folded by
+    torch), argmax labels at the end; frames/s over K timed steps (CUDA events,
+    inputs read from the resident clip every step). Measurement only."""
+    import torch
+    import torch.nn.functional as Fn
+    from paper_1704_04313_b200 import shard
+    dev = clip.device
+    dtype = torch.float16 if dt == "fp16" else torch.float32
+    prev_tf32 = (torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32)
+    torch.backends.cudnn.allow_tf32 = dt == "tf32"
+    torch.backends.cuda.matmul.allow_tf32 = dt == "tf32"
+    params = {}
+    cin = specd["inputChannels"]
+    for k, l in enumerate(specd["layers"]):
+        if l["kind"] in ("CBCONV", "CONV"):
+            K_, b_ = weights[k]
+            Wt = torch.from_numpy(np.ascontiguousarray(K_)).reshape(l["outChannels"], cin, l["kernelH"], l["kernelW"])
+            params[k] = (Wt.to(dev, dtype).contiguous(memory_format=torch.channels_last),
+                         torch.from_numpy(np.ascontiguousarray(b_)).to(dev, dtype))
+            cin = l["outChannels"]
+
+    def frame(x):
+        x = x.to(dtype).contiguous(memory_format=torch.channels_last)
+        for k, l in enumerate(specd["layers"]):
+            kind = l["kind"]
+            if kind in ("CBCONV", "CONV"):
+                x = Fn.conv2d(x, params[k][0], params[k][1], stride=(l.get("strideH", 1), l.get("strideW", 1)),
+                              padding=(l.get("padH", 0), l.get("padW", 0)))
+                if kind == "CBCONV" and l.get("fuseRelu"):
+                    x = torch.relu(x)
+            elif kind == "RELU":
+                x = torch.relu(x)
+            elif kind == "MAXPOOL":
+                x = Fn.max_pool2d(x, l["window"], l["stride"])
+            elif kind == "CLASSIFY":
+                return x.argmax(dim=1)
+        return x.argmax(dim=1)
+
+    F = clip.shape[0]
+    with torch.no_grad():
+        for i in range(3):
+            frame(clip[pingpong(i, F)])
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(3, 3 + K):
+            frame(clip[pingpong(i, F)])
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+    ms = shard.max_over_ranks(e0.elapsed_time(e1), device=red_dev)
+    return round(shard.aggregate_rate(ws, S * K, ms), 1)
+
+
 def run_gpu_arm(args):
     import torch
     ws, rank, local = dist_env()
@@ -275,6 +339,8 @@ def run_gpu_arm(args):
     red_dev = f"cuda:{local}" if backend == "nccl" else None
     if ws > 1:
         import torch.distributed as dist
+        # communicator setup lines (rank count, transport) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -398,7 +464,9 @@ def run_gpu_arm(args):
     except (OSError, ValueError):
         pass
     roof["kernel"] = f"{kname}[layer {klayer}]"
-    roof["kernel_share_of_step"] = kms / step_ms if step_ms else None
+    # share of the serial sum of the frame's kernel times (graph-free pass,
+    # lanes one after the other); the graph-timed step overlaps the lanes
+    roof["kernel_share_of_kernel_sum"] = kms / step_ms if step_ms else None
     roof["peak_source"] = (f"{peak_src} MEASURED_PEAKS.json" + ("" if bound == "hbm" else
                            (" (fp16 operands: the measured dense bf16 rate)" if net.layer_operands(klayer) == "f16"
                             else " (tf32 = bf16/2, tf32 not measured)") if bound == "tensor" else ""))
@@ -527,18 +595,52 @@ def run_gpu_arm(args):
         log(f"[gpu] e2e: {1000 * wall / K:.3f} ms/step, {e2e['value']:.1f} frames/s "
             f"(synchronous cbx_forward {e2e['sync_api_value']:.1f})")
 
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    # tf32-only operands (layer 3 on kind::tf32 too), same workload and timing
+    tf32_value = None
+    if args.precision == "f16":
+        net_t = cbx.Network(spec, weights, device=local, streams=S, precision="tf32", lanes=args.lanes)
+        st_t = torch.cuda.ExternalStream(net_t.stream_handle(), device=torch.device("cuda", local))
+        for i in range(0, args.warmup + 1):
+            net_t.forward_device(ptrs(i))
+        net_t.sync()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st_t)
+        for i in range(i0, i0 + K):
+            net_t.forward_device(ptrs(i))
+        e1.record(st_t)
+        torch.cuda.synchronize()
+        barrier()
+        tf32_value = shard.aggregate_rate(ws, S * K, shard.max_over_ranks(e0.elapsed_time(e1), device=red_dev))
+        net_t.close()
+        del net_t
+        log(f"[gpu] tf32-only operands: {tf32_value:.1f} frames/s")
+
+    cudnn = None
+    if not args.no_cudnn:
         try:
-            cpu = cpu_reference_run(args, args.cpu_budget, 8, log=log)
+            cudnn = {dt: cudnn_dense_fps(specd, weights, clip, S, max(3, K // 4), dt, barrier, red_dev, ws)
+                     for dt in ("tf32", "fp16")}
+            log(f"[gpu] cuDNN dense (torch conv2d, channels_last): {cudnn}")
+        except Exception as e:  # a cross-check only; never sinks the measured line
+            cudnn = {"error": repr(e)}
+
+    clocks_all = shard.gather_objects(clk)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            cpu = cpu_reference_run(args, args.cpu_budget, S, log=log)
         except Exception as e:  # the CPU column is informative; never sink the GPU number
             cpu = {"value": None, "unit": "frames/s", "cores": 0, "kind": "unavailable", "sample": repr(e)}
 
     roof["frame"]["t_step_ms"] = ms / K
     roof["frame"]["frac_vs_step"] = roof["frame"]["t_roof_ms"] / (ms / K) if ms else None
-    ops = [(k, net.layer_operands(k)) for k in spec.cb_layers()]
-    dtype_str = ("tensor cores, fp32 accumulate: " + ", ".join(f"layer {k} {o}" for k, o in ops)
-                 if args.precision == "tf32" else "f32 (exact)")
+    ops = [(k, net.layer_operands(k)) for k, l in enumerate(spec.layers) if l.is_conv()]
+    operands = {f"layer {k + 1} ({spec.layers[k].kind})": o for k, o in ops}
+    dtype_str = ("fp32 accumulate; operands " + ", ".join(f"L{k + 1} {o}" for k, o in ops)
+                 if args.precision != "exact" else "f32 (exact)")
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
@@ -548,17 +650,27 @@ def run_gpu_arm(args):
             "config": {"workload": f"paper_like {args.width}x{args.height} x {S} streams/GPU, sprite recipe "
                                    f"{args.recipe}% (resident clips, inputs > L2: {S}x2 frames of "
                                    f"{3 * args.height * args.width * 4 / 1e6:.1f} MB per step)",
-                       "streams_per_gpu": S, "taus": list(BASE_TAUS), "precision": args.precision,
+                       "streams_per_gpu": S, "taus": list(BASE_TAUS),
+                       "precision": {"mode": args.precision, "operands": operands,
+                                     "tf32_only_value": tf32_value,
+                                     "note": "f16 = fp16 operands (10 mantissa bits, RN) for the MAXPOOL-fed "
+                                             "304-channel layer 3, kind::tf32 for layer 2, exact fp32 for layer 1 "
+                                             "and the 1x1 head; tf32_only_value = the same step with layer 3 on "
+                                             "kind::tf32 too"},
+                       "cudnn_dense_fps": cudnn,
+                       "l2_flush": "inputs larger than L2: every step reads S x 2 fresh frames "
+                                   f"({S * 2 * 3 * args.height * args.width * 4 / 1e6:.0f} MB > 126 MB L2)",
                        "l1_input_changed": frac_in, "layer_output_changed": frac_out,
                        "dense_fps": dense_fps, "speedup_vs_dense": value / dense_fps, "parallelism": f"streams x{ws}",
                        "single_stream_latency_ms": lat_ms, "lanes": net.num_lanes()},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * K,
-            "clocks": clk,
+            "clocks": clk, "clocks_per_rank": clocks_all,
         }
         if sweep:
             line["sweep"] = sweep
         print(json.dumps(line), flush=True)
     if ws > 1:
+        barrier()  # rank 0 may still have been timing the CPU baseline
         torch.distributed.destroy_process_group()
 
 

@@ -62,7 +62,7 @@ struct ConvGeometry {
 
 enum class LayerKind { CBCONV = CBX_CBCONV, CONV = CBX_CONV, RELU = CBX_RELU, MAXPOOL = CBX_MAXPOOL, CLASSIFY = CBX_CLASSIFY };
 enum class Engine { Baseline = CBX_ENGINE_BASELINE, CBInfer = CBX_ENGINE_CBINFER };
-enum class Precision { Exact = CBX_PREC_EXACT, TF32 = CBX_PREC_TF32 };
+enum class Precision { Exact = CBX_PREC_EXACT, TF32 = CBX_PREC_TF32, F16 = CBX_PREC_F16 };
 
 inline LayerKind layer_kind_from_string(const std::string& s) {
     if (s == "CBCONV") return LayerKind::CBCONV;

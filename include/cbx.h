@@ -60,11 +60,22 @@ typedef enum { CBX_CBCONV = 0, CBX_CONV = 1, CBX_RELU = 2, CBX_MAXPOOL = 3, CBX_
 /* Engine, network.hpp:70 */
 typedef enum { CBX_ENGINE_BASELINE = 0, CBX_ENGINE_CBINFER = 1 } cbx_engine;
 
-/* Arithmetic of the convolution contraction. EXACT reproduces the reference
- * fp32 accumulation order bit for bit (bias first, ascending (c,kj,ki), one
- * rounding per multiply and per add). TF32 runs layers with channels-last
- * inputs on tcgen05 tensor cores (tf32 operands, fp32 accumulate). */
-typedef enum { CBX_PREC_EXACT = 0, CBX_PREC_TF32 = 1 } cbx_precision;
+/* Arithmetic of the convolution contraction.
+ *   EXACT: the reference fp32 accumulation order bit for bit (bias first,
+ *     ascending (c,kj,ki), one rounding per multiply and per add), CUDA cores.
+ *   TF32: convolutions with channels-last inputs and >= 32 outputs run on
+ *     tcgen05 tensor cores, kind::tf32 (operands rounded to 10 mantissa bits,
+ *     fp32 accumulate). The planar first layer and narrow 1x1 heads stay EXACT.
+ *   F16: as TF32, but a layer with > 128 outputs fed by a MAXPOOL runs
+ *     kind::f16 with fp16 operands (the same 10 mantissa bits, round to
+ *     nearest, a 5-bit exponent: |x| <= 65504, subnormal below 6.1e-5; fp32
+ *     accumulate). Twice the tensor rate and half the operand bytes of tf32.
+ *     The MAXPOOL writes an fp16 shadow of its output and flags any value out
+ *     of range; that frame and every later one until the next full evaluation
+ *     then fail with CBX_E_ARG when their stats are read (cbx_forward,
+ *     cbx_wait, cbx_read_stats), and the next frame is evaluated in full.
+ *     Weights out of the fp16 range are rejected by cbx_load_layer. */
+typedef enum { CBX_PREC_EXACT = 0, CBX_PREC_TF32 = 1, CBX_PREC_F16 = 2 } cbx_precision;
 
 /* ConvGeometry, geometry.hpp:12-49 */
 typedef struct {
@@ -119,8 +130,8 @@ CBX_API int cbx_create_ex(const cbx_net_desc* net, int device, int num_streams, 
 CBX_API int cbx_num_lanes(const cbx_ctx* ctx);
 /* Operand format of layer `layer`'s convolution: 0 = fp32 on CUDA cores
  * (exact reference order), 1 = tcgen05 kind::tf32, 2 = tcgen05 kind::f16
- * (fp16 operands rounded to nearest, fp32 accumulation; wide layers fed by a
- * MAXPOOL in tensor-core mode unless CBX_TC_F16=0 at creation), -1 = not a conv. */
+ * (fp16 operands rounded to nearest, fp32 accumulation; CBX_PREC_F16 only),
+ * -1 = not a conv. */
 CBX_API int cbx_layer_operands(const cbx_ctx* ctx, int layer);
 CBX_API void cbx_destroy(cbx_ctx* ctx);
 
@@ -160,10 +171,13 @@ CBX_API int cbx_forward(cbx_ctx* ctx, int engine, const float* frames, uint16_t*
                         cbx_layer_stats* stats, uint64_t* macs);
 
 /* Device-resident variant for clips already in HBM: frames_dev[s] points to
- * stream s's planar frame on the context's device. The previous call's frame
- * buffers must stay valid until this call returns (they are the detection
- * reference, i.e. prevInput of the first CBCONV). Asynchronous on the context
- * stream; use cbx_sync / cbx_read_* afterwards. */
+ * stream s's planar frame on the context's device. Asynchronous on the
+ * context stream; use cbx_sync / cbx_read_* afterwards. The frame buffers are
+ * read by kernels that run after this call returns, and each frame is also
+ * the detection reference (prevInput of the first CBCONV) of the NEXT call:
+ * a frame buffer must stay valid and unmodified until the work of the call
+ * after the one that passed it has completed (cbx_sync, or an event recorded
+ * on cbx_stream after that call). */
 CBX_API int cbx_forward_device(cbx_ctx* ctx, int engine, const float* const* frames_dev);
 /* Pipelined host-frame serving (forward_frame, network.hpp:93-94, split in
  * two): cbx_submit enqueues one frame of every stream -- host -> device copy

@@ -41,7 +41,7 @@ __all__ = [
 
 KINDS = ("CBCONV", "CONV", "RELU", "MAXPOOL", "CLASSIFY")
 ENGINES = {"baseline": 0, "cbinfer": 1}
-PRECISIONS = {"exact": 0, "tf32": 1}
+PRECISIONS = {"exact": 0, "tf32": 1, "f16": 2}
 
 
 @dataclass

@@ -30,6 +30,7 @@
 //   a time, + bias, fused ReLU, compare with the value being overwritten
 //   (next CBCONV's change detection, cbconv.cpp:66-67), in-place scatter into
 //   the persistent output tensor (update_output without the full copy).
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -935,6 +936,12 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
         // fp16 image (round to nearest even): chunk J = tap * C4 + c4 holds
         // channels 8*c4 .. 8*c4+7 of that tap; half (n, kb*64 + j*8 + e) at
         // kb*Npad*64 + n*64 + (j ^ (n & 7))*8 + e
+        // fp16 range: a weight beyond 65504 would become inf (the activations
+        // are range-checked per frame by the shadow writer, engine.cu)
+        for (size_t i = 0; i < (size_t)g.outChannels * Kref; ++i)
+            if (std::fabs(K[i]) > 65504.0f)
+                throw Error(CBX_E_ARG, "a filter weight of a kind::f16 layer exceeds the fp16 range (|w| > 65504); "
+                                       "create the context with CBX_PREC_TF32");
         std::vector<__half> img((size_t)t.NKB * t.Brows * 64, __float2half_rn(0.0f));
         for (int n = 0; n < g.outChannels; ++n)
             for (int J = 0; J < t.NKB * kChunksPerKB; ++J) {

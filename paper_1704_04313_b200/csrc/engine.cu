@@ -150,6 +150,7 @@ struct Engine::Plan {
     bool dirty = true;
     int fused_from = -1;            // conv layer whose epilogue runs the per-pixel tail (-1: none)
     uint32_t* work = nullptr;       // touched-pixel list shared by the MAXPOOL/RELU layers
+    int* ovf = nullptr;             // fp16 shadow overflow flag (sticky until a full frame)
     // Frame scratch zeroed by ONE memset at the start of a steady frame:
     // stats counters, each compaction's look-back status words, each
     // MAXPOOL/RELU's work-list counter (no per-kernel memset nodes).
@@ -180,7 +181,8 @@ struct Engine::Plan {
 Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
     : device_(device), S_(S), precision_(precision) {
     if (S < 1) throw Error(CBX_E_ARG, "num_streams must be >= 1");
-    if (precision != CBX_PREC_EXACT && precision != CBX_PREC_TF32) throw Error(CBX_E_ARG, "bad precision");
+    if (precision != CBX_PREC_EXACT && precision != CBX_PREC_TF32 && precision != CBX_PREC_F16)
+        throw Error(CBX_E_ARG, "bad precision (CBX_PREC_EXACT, CBX_PREC_TF32 or CBX_PREC_F16)");
     dims_ = chain_dims(net, layers_);
     net_ = net;
     net_.layers = layers_.data();
@@ -205,21 +207,17 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
             // first layer reading the planar frame).
             // (N >= 32 output channels: narrower 1x1 heads stay exact on CUDA cores,
             //  usually fused into the epilogue of the preceding tcgen05 layer)
-            if (precision_ == CBX_PREC_TF32 && k > 0 && g.outChannels >= 32 && tc_supported(g)) {
+            if (precision_ != CBX_PREC_EXACT && k > 0 && g.outChannels >= 32 && tc_supported(g)) {
                 const int te = tail_end(k);
                 const int c1 = te > 0 ? layers_[k + 1].geom.outChannels : 0;
                 const int tail_floats = te > 0 ? (c1 <= 8 ? 8 : 16) * g.outChannels : 0;
-                // fp16 operands (kind::f16: 10 explicit mantissa bits like tf32,
-                // twice the rate, half the bytes) for a wide layer fed by a
-                // MAXPOOL, which also writes an fp16 (round-to-nearest) shadow of
-                // its output. Read at construction; CBX_TC_F16=0 keeps tf32.
-                const char* f16_env = std::getenv("CBX_TC_F16");
-                const bool f16 = !(f16_env && std::atoi(f16_env) == 0) && g.outChannels > 128 &&
+                // CBX_PREC_F16: fp16 operands (kind::f16: 10 explicit mantissa
+                // bits like tf32, twice the rate, half the bytes) for a wide
+                // layer fed by a MAXPOOL, which also writes an fp16
+                // (round-to-nearest) shadow of its output.
+                const bool f16 = precision_ == CBX_PREC_F16 && g.outChannels > 128 &&
                                  layers_[k - 1].kind == CBX_MAXPOOL;
-                if (f16) {
-                    f16_layers_.push_back(k);
-                    if (!d_f16_ovf_) d_f16_ovf_ = dmalloc<int>(1);
-                }
+                if (f16) f16_layers_.push_back(k);
                 tc_[k] = make_tc_layer(g, tail_floats, -1, f16);
             }
         }
@@ -233,7 +231,7 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
     d_prev_ = tbl + S;
     const size_t frame = (size_t)net.inputChannels * net.inputHeight * net.inputWidth * S;
     for (auto& s : slots_) s = dmalloc<float>(frame);
-    CBX_CUDA(cudaMallocHost(&h_stats_, sizeof(unsigned long long) * 4 * S * nl + 16));
+    CBX_CUDA(cudaMallocHost(&h_stats_, sizeof(unsigned long long) * 2 * stats_words()));
     last_cb_frames_.assign(S, nullptr);
     for (int e = 0; e < 2; ++e) {
         last_stats_[e].assign((size_t)S * nl, cbx_layer_stats{0, 0, 0});
@@ -251,7 +249,6 @@ Engine::~Engine() {
     tc_.clear();
     for (float* p : dK_) cudaFree(p);
     for (float* p : dBias_) cudaFree(p);
-    if (d_f16_ovf_) cudaFree(d_f16_ovf_);
     cudaFree(d_cur_);
     for (auto& s : slots_) cudaFree(s);
     cudaFreeHost(h_stats_);
@@ -353,7 +350,8 @@ void Engine::build_plan(Plan& p, bool baseline) {
         p.T[0] = TensorView{nullptr, c, h, w, c, h, w, 0, 0, (int64_t)c * h * w};
     }
     p.labels = p.alloc<uint16_t>((size_t)S * lh_ * lw_);
-    p.stats = p.alloc<unsigned long long>((size_t)2 * S * nl);
+    p.stats = p.alloc<unsigned long long>(stats_words());
+    if (!f16_layers_.empty()) p.ovf = p.alloc<int>(1);
     if (baseline) return;  // full mode only: no masks, no lists
 
     // change masks (inputs of CBCONV layers) and updated masks
@@ -435,7 +433,7 @@ void Engine::build_plan(Plan& p, bool baseline) {
         p.work = p.alloc<uint32_t>((size_t)wk);
     }
     // frame scratch: [stats][look-back status per conv][work counter per pool/relu]
-    size_t off = round_up(sizeof(unsigned long long) * 2 * S * nl, 256);
+    size_t off = round_up(sizeof(unsigned long long) * stats_words(), 256);
     std::vector<size_t> ws_off(nl, 0), wc_off(nl, 0);
     for (int k = 0; k < nl; ++k) {
         if (ws_bytes[k]) {
@@ -462,12 +460,14 @@ void Engine::record(Plan& p, bool full) {
     const int nl = (int)layers_.size(), S = S_;
     cudaStream_t st = stream_;
     auto stats_of = [&](int layer, int field) { return p.stats + (size_t)layer * S * 2 + field; };
+    if (full && p.ovf) CBX_CUDA(cudaMemsetAsync(p.ovf, 0, sizeof(int), st));  // full evaluation clears it
     if (!full) {
         CBX_CUDA(cudaMemsetAsync(p.scratch, 0, p.scratch_bytes, st));
         for (int t = 0; t <= nl; ++t)
             if (p.chg_by_conv[t] && p.chg[t].d)
                 CBX_CUDA(cudaMemsetAsync(p.chg[t].d, 0, sizeof(uint32_t) * (size_t)(p.chg[t].stride * S), st));
     }
+    mark("memset", -1);  // (profile pass: the scratch memsets get their own interval)
     // K1: detection on the raw frames
     if (!full) {
         const auto& in = p.T[0];
@@ -613,7 +613,7 @@ void Engine::record(Plan& p, bool full) {
                 a.work_count = p.wcount_k.empty() ? nullptr : p.wcount_k[k];  // (sparse frames only)
                 a.count_zeroed = 1;
                 a.out16 = p.T16[k + 1];
-                a.f16_overflow = p.T16[k + 1].d ? d_f16_ovf_ : nullptr;
+                a.f16_overflow = p.T16[k + 1].d ? p.ovf : nullptr;
                 launch_point_bits(a, st);
                 mark(a.relu ? "relu" : "pool", k);
                 break;
@@ -629,6 +629,9 @@ void Engine::record(Plan& p, bool full) {
         launch_classify_bits(p.T[nl], full ? BitMask{nullptr, 0, 0, 0, 0} : p.upd[nl], p.labels, S, st);
         mark("classify", nl);
     }
+    // this frame's view of the (sticky) fp16 overflow flag, read back with its counters
+    if (p.ovf)
+        CBX_CUDA(cudaMemcpyAsync(p.stats + stats_words() - 1, p.ovf, sizeof(int), cudaMemcpyDeviceToDevice, st));
     CBX_CUDA(cudaGetLastError());
 }
 
@@ -726,7 +729,7 @@ bool Engine::enqueue(int engine, const float* const* frames_dev, unsigned long l
     launch(p, full);
     const int nl = (int)layers_.size();
     if (stats_dst)
-        CBX_CUDA(cudaMemcpyAsync(stats_dst, p.stats, sizeof(unsigned long long) * 2 * S_ * nl, cudaMemcpyDeviceToHost,
+        CBX_CUDA(cudaMemcpyAsync(stats_dst, p.stats, sizeof(unsigned long long) * stats_words(), cudaMemcpyDeviceToHost,
                                  stream_));
     last_full_[engine] = full;
     if (engine == CBX_ENGINE_CBINFER) {
@@ -755,7 +758,7 @@ int64_t Engine::submit(int engine, const float* frames, uint16_t* labels) {
             CBX_CUDA(cudaEventCreateWithFlags(&copied_[q], cudaEventDisableTiming));
             CBX_CUDA(cudaEventCreateWithFlags(&done_[q], cudaEventDisableTiming));
         }
-        CBX_CUDA(cudaMallocHost(&h_ring_stats_, sizeof(unsigned long long) * kRing * 2 * S_ * nl));
+        CBX_CUDA(cudaMallocHost(&h_ring_stats_, sizeof(unsigned long long) * kRing * stats_words()));
     }
     const int64_t j = submitted_;
     const int q = (int)(j % kRing);
@@ -765,7 +768,7 @@ int64_t Engine::submit(int engine, const float* frames, uint16_t* labels) {
     CBX_CUDA(cudaStreamWaitEvent(stream_, copied_[q], 0));
     std::vector<const float*> cur(S_);
     for (int s = 0; s < S_; ++s) cur[s] = ring_[q] + per * s;
-    ring_full_[q] = enqueue(engine, cur.data(), h_ring_stats_ + (size_t)q * 2 * S_ * nl);
+    ring_full_[q] = enqueue(engine, cur.data(), h_ring_stats_ + (size_t)q * stats_words());
     CBX_CUDA(cudaMemcpyAsync(labels, plan(engine).labels, sizeof(uint16_t) * S_ * lh_ * lw_, cudaMemcpyDeviceToHost,
                              stream_));
     CBX_CUDA(cudaEventRecord(done_[q], stream_));
@@ -780,11 +783,12 @@ void Engine::wait(int64_t ticket, cbx_layer_stats* stats, uint64_t* macs) {
         throw Error(CBX_E_ARG, "cbx_wait: unknown or expired ticket (at most the last 3 submissions can be waited on)");
     CBX_CUDA(cudaSetDevice(device_));
     CBX_CUDA(cudaEventSynchronize(done_[q]));
-    check_f16_overflow();
     const int nl = (int)layers_.size();
+    const unsigned long long* hs = h_ring_stats_ + (size_t)q * stats_words();
+    check_f16_overflow(hs, CBX_ENGINE_CBINFER);
     std::vector<cbx_layer_stats> st((size_t)S_ * nl);
     std::vector<uint64_t> mc(S_);
-    stats_from(h_ring_stats_ + (size_t)q * 2 * S_ * nl, ring_full_[q], CBX_ENGINE_CBINFER, st.data(), mc.data());
+    stats_from(hs, ring_full_[q], CBX_ENGINE_CBINFER, st.data(), mc.data());
     if (stats) std::memcpy(stats, st.data(), sizeof(cbx_layer_stats) * st.size());
     if (macs) std::memcpy(macs, mc.data(), sizeof(uint64_t) * S_);
 }
@@ -794,7 +798,8 @@ void Engine::sync() { CBX_CUDA(cudaStreamSynchronize(stream_)); }
 void Engine::finish_stats(Plan& p, bool full, int engine) {
     (void)p;
     const int nl = (int)layers_.size();
-    stats_from(h_stats_ + (size_t)engine * 2 * S_ * nl, full, engine, last_stats_[engine].data(), last_macs_[engine].data());
+    stats_from(h_stats_ + (size_t)engine * stats_words(), full, engine, last_stats_[engine].data(), last_macs_[engine].data());
+    last_ovf_[engine] = h_stats_[(size_t)engine * stats_words() + stats_words() - 1] != 0;
 }
 
 // Per-stream LayerStats from the device counters (cbconv.cpp:170-192,
@@ -831,31 +836,33 @@ void Engine::stats_from(const unsigned long long* hs, bool full, int engine, cbx
     }
 }
 
-void Engine::check_f16_overflow() {
-    if (!d_f16_ovf_) return;
-    int h = 0;
-    CBX_CUDA(cudaMemcpy(&h, d_f16_ovf_, sizeof(int), cudaMemcpyDeviceToHost));
-    if (h) {
-        CBX_CUDA(cudaMemset(d_f16_ovf_, 0, sizeof(int)));
-        throw Error(CBX_E_ARG,
-                    "fp16 operand overflow: an input of a kind::f16 layer exceeded 65504 in magnitude "
-                    "(create the context with CBX_TC_F16=0 to keep tf32 operands)");
-    }
+// fp16 operand range: the MAXPOOL that writes a kind::f16 layer's fp16 shadow
+// raises the plan's overflow flag when a value exceeds 65504. The flag is
+// sticky until the next full evaluation (a change-based frame only rewrites
+// changed pixels, so outputs computed from an inf operand persist), and every
+// frame copies it into its stats block: each frame whose outputs may carry
+// the overflow reports it, and the next frame is evaluated in full.
+void Engine::check_f16_overflow(const unsigned long long* hs, int engine) {
+    if (f16_layers_.empty() || !hs[stats_words() - 1]) return;
+    if (engine == CBX_ENGINE_CBINFER) has_history_ = false;
+    throw Error(CBX_E_ARG,
+                "fp16 operand overflow: an input of a kind::f16 layer exceeded 65504 in magnitude "
+                "(create the context with CBX_PREC_TF32 to keep tf32 operands); the next frame is a full evaluation");
 }
 
 void Engine::read_stats(int engine, cbx_layer_stats* stats, uint64_t* macs) {
     if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
     if (stats_pending_[engine]) {
         const int nl = (int)layers_.size();
-        CBX_CUDA(cudaMemcpyAsync(h_stats_ + (size_t)engine * 2 * S_ * nl, plan(engine).stats,
-                                 sizeof(unsigned long long) * 2 * S_ * nl, cudaMemcpyDeviceToHost, stream_));
+        CBX_CUDA(cudaMemcpyAsync(h_stats_ + (size_t)engine * stats_words(), plan(engine).stats,
+                                 sizeof(unsigned long long) * stats_words(), cudaMemcpyDeviceToHost, stream_));
         sync();
         finish_stats(plan(engine), last_full_[engine], engine);
         stats_pending_[engine] = false;
     } else {
         sync();
     }
-    check_f16_overflow();
+    if (last_ovf_[engine]) check_f16_overflow(h_stats_ + (size_t)engine * stats_words(), engine);
     const int nl = (int)layers_.size();
     if (stats) std::memcpy(stats, last_stats_[engine].data(), sizeof(cbx_layer_stats) * S_ * nl);
     if (macs) std::memcpy(macs, last_macs_[engine].data(), sizeof(uint64_t) * S_);
@@ -995,7 +1002,7 @@ void Engine::profile(int engine, const float* const* frames_dev, std::vector<cbx
     }
     prof_ = nullptr;
     const int nl = (int)layers_.size();
-    CBX_CUDA(cudaMemcpyAsync(h_stats_ + (size_t)engine * 2 * S_ * nl, p.stats, sizeof(unsigned long long) * 2 * S_ * nl,
+    CBX_CUDA(cudaMemcpyAsync(h_stats_ + (size_t)engine * stats_words(), p.stats, sizeof(unsigned long long) * stats_words(),
                              cudaMemcpyDeviceToHost, stream_));
     sync();
     out.clear();

@@ -108,8 +108,10 @@ private:
     std::vector<std::vector<float>> hK_, hB_;  // host copies (kernel-parameter filters)
     std::vector<std::unique_ptr<TcLayer, TcLayerDeleter>> tc_;
     std::vector<int> f16_layers_;  // tcgen05 layers with fp16 operands (their input has an fp16 shadow)
-    int* d_f16_ovf_ = nullptr;     // set by the shadow writers on an fp16 range overflow
-    void check_f16_overflow();
+    void check_f16_overflow(const unsigned long long* hs, int engine);
+    bool last_ovf_[2] = {false, false};
+    // device counters of one frame: [nl][S][2] + the fp16 overflow flag
+    size_t stats_words() const { return (size_t)2 * S_ * layers_.size() + 1; }
 
 public:
     // 0 = exact fp32 (CUDA cores), 1 = tcgen05 tf32, 2 = tcgen05 f16, -1 = not a conv

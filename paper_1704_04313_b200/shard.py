@@ -47,3 +47,14 @@ def barrier() -> None:
 def aggregate_rate(world: int, units_per_rank: int, ms_max: float) -> float:
     """Whole-job throughput: the units all ranks processed / the slowest rank's time."""
     return world * units_per_rank / (ms_max / 1000.0)
+
+
+def gather_objects(obj):
+    """Per-rank values (e.g. each rank's sampled clocks) collected on every
+    rank, rank order; [obj] when torch.distributed is not initialised."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [obj]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out

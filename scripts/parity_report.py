@@ -10,7 +10,8 @@ clips -- the numbers north_star asks to report (SURVEY.md 8c parity plan):
   * final activations (max-abs error) and segmentation maps (label
     disagreement) against the reference,
 
-for precision=tf32 (the serving mode) and precision=exact (bitwise expected),
+for precision=f16 (the bench's serving mode: layer 3 fp16 operands), tf32 and
+exact (bitwise expected); each run records the per-layer operand formats,
 at configs[1] (320x240) and configs[2] (1920x1080), base taus (0.04, 0.05,
 0.05). Test/report infrastructure: runs the reference on the host as checker.
 
@@ -84,8 +85,10 @@ def run(h, w, recipe, frames, precision, nthreads):
                         f"upd {l['updated_symdiff']}/{l['updated_ref']}" for l in layers) +
               f"  max|dy| {rows[-1]['final_max_abs_err']:.2e}  labels {100 * rows[-1]['label_disagreement']:.4f}%",
               flush=True)
+    operands = {str(k): net.layer_operands(k) for k, l in enumerate(net.spec.layers) if l.is_conv()}
     net.close()
-    return dict(height=h, width=w, recipe=recipe, precision=precision, checker=kind, frames=rows)
+    return dict(height=h, width=w, recipe=recipe, precision=precision, operands=operands, checker=kind,
+                frames=rows)
 
 
 def main():
@@ -96,9 +99,10 @@ def main():
     args = ap.parse_args()
     nthreads = os.cpu_count() or 1
     res = dict(when=time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()), taus=list(bench.BASE_TAUS), runs=[])
-    for precision in ("tf32", "exact"):
+    for precision in ("f16", "tf32", "exact"):
         res["runs"].append(run(240, 320, "2.2", args.frames, precision, nthreads))
-    res["runs"].append(run(1080, 1920, "2.2", args.frames_1080, "tf32", nthreads))
+    for precision in ("f16", "tf32"):
+        res["runs"].append(run(1080, 1920, "2.2", args.frames_1080, precision, nthreads))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(res, open(args.out, "w"), indent=1)
     print("wrote", args.out)

@@ -40,7 +40,7 @@ RECIPES_320 = [(2, 24, 3), (4, 24, 3), (4, 32, 4), (8, 32, 5), (10, 40, 6), (12,
 RECIPES_1080 = [(8, 96, 8), (12, 128, 12), (16, 160, 16), (16, 192, 20), (20, 192, 20)]
 
 
-def make_net(h, w, S, taus=bench.BASE_TAUS, precision="tf32"):
+def make_net(h, w, S, taus=bench.BASE_TAUS, precision="f16"):
     specd = bench.paper_spec_dict(h, w, taus)
     spec = cbx.network_spec_from_json(json.dumps(specd))
     return cbx.Network(spec, cbx.generate_weights(spec, None, 1), streams=S, precision=precision)
@@ -167,7 +167,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.json"))
     args = ap.parse_args()
     res = dict(gpu=torch.cuda.get_device_name(0), when=time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
-               precision="tf32", base_taus=list(bench.BASE_TAUS))
+               precision="f16", base_taus=list(bench.BASE_TAUS))
     which = args.which.split(",")
     if "rate" in which:
         print("rate sweep 320x240", flush=True)

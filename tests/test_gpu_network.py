@@ -143,18 +143,17 @@ def test_multistream_independent(gpu, orc):
                 assert np.array_equal(net.trace(cb, s)[1], onets[s].trace(cb)[1])
 
 
-@pytest.mark.parametrize("f16", ["1", "0"])
-def test_tf32_tolerance(gpu, orc, monkeypatch, f16):
-    """Tensor-core mode at tau=0: layer-1 masks/indices/outputs bit-exact,
+@pytest.mark.parametrize("prec", ["f16", "tf32"])
+def test_tf32_tolerance(gpu, orc, prec):
+    """Tensor-core modes at tau=0: layer-1 masks/indices/outputs bit-exact,
     final activations within 1e-3 max-abs, labels within 0.1% (tau > 0:
-    test_tf32_mask_mismatch_counts). f16: layer 3 with fp16 operands (the
-    default) or tf32 (CBX_TC_F16=0)."""
-    monkeypatch.setenv("CBX_TC_F16", f16)
+    test_tf32_mask_mismatch_counts). f16: layer 3 with fp16 operands; tf32:
+    tf32 operands everywhere."""
     spec = paper_spec(64, 96, (0.0, 0.0, 0.0))
     w = orc.generate_weights(spec, 1)
     cfg = dict(channels=3, height=64, width=96, sprites=[(12, 2, 0.9)], noise=0.01, seed=3)
     onet = orc.load_network(spec, w)
-    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32")
+    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision=prec)
     for f in range(4):
         fr = orc.synth_frame(cfg, f)
         want = onet.forward_frame(fr)
@@ -168,8 +167,8 @@ def test_tf32_tolerance(gpu, orc, monkeypatch, f16):
         assert (got.labels != want["labels"]).mean() <= 1e-3
 
 
-@pytest.mark.parametrize("h,w,f16", [(96, 128, "1"), (54, 74, "1"), (96, 128, "0")])
-def test_tf32_mask_mismatch_counts(gpu, orc, monkeypatch, h, w, f16):
+@pytest.mark.parametrize("h,w,prec", [(96, 128, "f16"), (54, 74, "f16"), (96, 128, "tf32")])
+def test_tf32_mask_mismatch_counts(gpu, orc, h, w, prec):
     """TF32 mode at the base taus (0.04, 0.05, 0.05) on a sprite clip: the
     per-CBCONV-layer changed-pixel mismatch counts against the oracle --
     popcount(detected_gpu XOR detected_ref) and |updated_gpu symdiff
@@ -177,12 +176,11 @@ def test_tf32_mask_mismatch_counts(gpu, orc, monkeypatch, h, w, f16):
     count) for layers 2-3, where a tf32 activation can cross tau; labels within
     0.1% (at least one pixel). scripts/parity_report.py writes the same counts at 320x240 and 1080p
     against the compiled reference (profiles/r1_parity.json)."""
-    monkeypatch.setenv("CBX_TC_F16", f16)
     spec = paper_spec(h, w, (0.04, 0.05, 0.05))
     wts = orc.generate_weights(spec, 1)
     cfg = dict(channels=3, height=h, width=w, sprites=[(16, 3, 0.9), (10, 2, 0.9)], noise=0.0, seed=3)
     onet = orc.load_network(spec, wts)
-    net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="tf32")
+    net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision=prec)
     counts = []
     for f in range(5):
         fr = orc.synth_frame(cfg, f)
@@ -206,37 +204,69 @@ def test_tf32_mask_mismatch_counts(gpu, orc, monkeypatch, h, w, f16):
     assert any(c[3] > 0 for c in counts if c[1] == 2)  # the clip reaches layer 3
 
 
-def test_layer_operands(gpu, orc, monkeypatch):
+def test_layer_operands(gpu, orc):
     """Operand formats reported per conv layer: layer 1 exact fp32 (planar
-    first layer), layer 2 tf32, layer 3 fp16 (fed by a MAXPOOL, default) or
-    tf32 with CBX_TC_F16=0; the head's 1x1 convs exact; exact mode fp32 only."""
+    first layer), layer 2 tf32, layer 3 fp16 (fed by a MAXPOOL) under
+    precision f16 and tf32 under precision tf32; the head's 1x1 convs exact;
+    exact mode fp32 only."""
     spec = paper_spec(32, 48)
     w = orc.generate_weights(spec, 1)
-    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32")
+    net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="f16")
     assert [net.layer_operands(k) for k in (0, 2, 4, 5)] == ["fp32", "tf32", "f16", "fp32"]
     assert net.layer_operands(1) == "none"  # MAXPOOL
-    monkeypatch.setenv("CBX_TC_F16", "0")
     net2 = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32")
-    assert net2.layer_operands(4) == "tf32"
+    assert [net2.layer_operands(k) for k in (0, 2, 4, 5)] == ["fp32", "tf32", "tf32", "fp32"]
     ex = gpu.Network(to_pkg_spec(gpu, spec), w, precision="exact")
     assert all(ex.layer_operands(k) == "fp32" for k in (0, 2, 4))
 
 
-def test_f16_overflow_reported(gpu, orc, monkeypatch):
-    """Layer 3's fp16 operands only cover |x| <= 65504: when its input exceeds
-    that (filters scaled so pool-2 outputs reach ~1e6) the frame reports an
-    error instead of silently computing with inf; tf32 operands
-    (CBX_TC_F16=0) take the same frame."""
-    spec = paper_spec(32, 48, (0.0, 0.0, 0.0))
-    w = orc.generate_weights(spec, 1)
-    big = {k: ((K * 1000.0).astype(K.dtype) if k in (0, 2) else K, b) for k, (K, b) in w.items()}
-    fr = orc.synth_frame(dict(channels=3, height=32, width=48, sprites=[(6, 2, 0.9)], noise=0.0, seed=1), 0)
-    net = gpu.Network(to_pkg_spec(gpu, spec), big, precision="tf32")
+def test_f16_overflow_reported(gpu, orc):
+    """Layer 3's fp16 operands only cover |x| <= 65504. The pool-2 shadow
+    writer flags a larger value; the flag is sticky until a full evaluation,
+    so the frame that overflowed AND every later change-based frame (whose
+    outputs may still hold results computed from inf) fail when their stats
+    are read, after which the next frame is evaluated in full and succeeds
+    (tf32 operands take every frame). Weights are scaled so that pool-2
+    peaks near 2e4 on frame A; frame B multiplies a patch of A by 4."""
+    h, w = 32, 48
+    spec = paper_spec(h, w, (0.0, 0.0, 0.0))
+    wts = orc.generate_weights(spec, 1)
+    A = orc.synth_frame(dict(channels=3, height=h, width=w, sprites=[(6, 2, 0.9)], noise=0.0, seed=1), 0)
+    probe = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="tf32")
+    probe.forward_frame(A)
+    c = 2.0e4 / float(np.abs(probe.layer_output(3)).max())
+    big = {k: ((K * c).astype(np.float32), (b * c).astype(np.float32)) if k == 0 else (K, b)
+           for k, (K, b) in wts.items()}
+    B = A.copy()
+    B[:, 8:24, 12:36] *= 4.0
+    tf = gpu.Network(to_pkg_spec(gpu, spec), big, precision="tf32")
+    tf.forward_frame(A)
+    assert np.abs(tf.layer_output(3)).max() < 6.0e4
+    tf.forward_frame(B)
+    assert np.abs(tf.layer_output(3)).max() > 7.0e4  # B's pool-2 values leave the fp16 range
+    net = gpu.Network(to_pkg_spec(gpu, spec), big, precision="f16")
+    net.forward_frame(A)
     with pytest.raises(gpu.CbxError, match="fp16 operand overflow"):
-        net.forward_frame(fr)
-    monkeypatch.setenv("CBX_TC_F16", "0")
-    net2 = gpu.Network(to_pkg_spec(gpu, spec), big, precision="tf32")
-    net2.forward_frame(fr)
+        net.forward_frame(B)
+    ok = net.forward_frame(A)  # evaluated in full after the error
+    assert ok.stats[0]["changedInputPixels"] == h * w
+    # pipelined: the overflowing frame and the incremental frame after it both report
+    S = 1
+    lab = [np.zeros((S,) + tuple(net.label_hw), np.uint16) for _ in range(4)]
+    fr = [np.ascontiguousarray(x[None]) for x in (A, B, B, A)]
+    t = [net.submit(fr[0], lab[0]), net.submit(fr[1], lab[1]), net.submit(fr[2], lab[2])]
+    net.wait(t[0])
+    with pytest.raises(gpu.CbxError, match="fp16 operand overflow"):
+        net.wait(t[1])
+    with pytest.raises(gpu.CbxError, match="fp16 operand overflow"):
+        net.wait(t[2])
+    t3 = net.submit(fr[3], lab[3])
+    stats, _ = net.wait(t3)
+    assert stats[0][0]["changedInputPixels"] == h * w  # full evaluation, no error
+    fresh = gpu.Network(to_pkg_spec(gpu, spec), big, precision="f16")
+    assert np.array_equal(fresh.forward_frame(A).labels, lab[3][0])
+    with pytest.raises(gpu.CbxError, match="fp16 range"):
+        gpu.Network(to_pkg_spec(gpu, spec), {k: (K * 1e7, b) for k, (K, b) in wts.items()}, precision="f16")
 
 
 def test_errors(gpu, orc):

@@ -1,10 +1,17 @@
-"""GPU: the tcgen05 (tf32) gathered convolution against the exact oracle,
-with an error bound derived from the operands: tf32 keeps 10 mantissa bits,
-so |y_tc - y_exact| <= 2^-9 * sum_r |w_r x_r| (+ fp32 accumulation slack).
-Shapes cover N split (304 = 128 + 176 with the split accumulator),
-N padding (52 -> 64, 8 -> 16),
-channel padding (Cin % 4 != 0), stride, asymmetric kernels and K-blocks
-straddling taps."""
+"""GPU: the tcgen05 gathered convolution against the exact oracle, one layer
+at a time, with error bounds derived from the operand formats:
+
+* kind::tf32: 10 mantissa bits, so |y_tc - y_exact| <= 2^-9 * sum_r |w_r x_r|
+  (+ fp32 accumulation slack);
+* kind::f16 (precision "f16": layers with > 128 outputs fed by a MAXPOOL):
+  fp16 keeps the same 10 mantissa bits but a 5-bit exponent; operands below
+  6.1e-5 are subnormal with an absolute rounding error <= 2^-25, so
+  |y_tc - y_exact| <= 2^-9 * sum_r |w_r x_r| + 2^-24 * sum_r (|w_r| + |x_r|).
+
+Shapes cover N split (304 = 128 + 176 with the split accumulator), N padding
+(52 -> 64, 40 -> 48, 37 -> 48), channel padding (Cin % 4 != 0, and % 8 != 0
+for fp16), stride, asymmetric kernels and K-blocks straddling taps; the fp16
+cases also run on small-magnitude (subnormal) activations."""
 import numpy as np
 import pytest
 
@@ -20,20 +27,77 @@ def two_layer(cin, h, w, layer):
         dict(kind="CONV", kernelH=1, kernelW=1, outChannels=cin, weightsFile="a"), layer])
 
 
+def pooled_layer(cin, h, w, layer):
+    # as two_layer, with a 2x2/2 MAXPOOL in front of the tested layer: the
+    # pooling kernel writes the fp16 shadow a kind::f16 layer gathers from
+    return dict(inputChannels=3, inputHeight=h, inputWidth=w, numClasses=layer["outChannels"], layers=[
+        dict(kind="CONV", kernelH=1, kernelW=1, outChannels=cin, weightsFile="a"),
+        dict(kind="MAXPOOL", window=2, stride=2), layer])
+
+
 CASES = [
     (52, 30, 40, dict(kind="CBCONV", kernelH=7, kernelW=7, padH=3, padW=3, outChannels=304, threshold=0.0, fuseRelu=True, weightsFile="b")),
     (4, 60, 80, dict(kind="CBCONV", kernelH=7, kernelW=7, padH=3, padW=3, outChannels=52, threshold=0.0, fuseRelu=True, weightsFile="b")),
-    (304, 20, 24, dict(kind="CONV", kernelH=1, kernelW=1, outChannels=8, weightsFile="b")),
+    (304, 20, 24, dict(kind="CONV", kernelH=1, kernelW=1, outChannels=40, weightsFile="b")),
     (6, 33, 47, dict(kind="CBCONV", kernelH=5, kernelW=3, strideH=2, strideW=1, padH=2, padW=1, outChannels=37, threshold=0.0, fuseRelu=False, weightsFile="b")),
     (13, 17, 19, dict(kind="CBCONV", kernelH=3, kernelW=3, padH=1, padW=1, outChannels=300, threshold=0.0, fuseRelu=True, weightsFile="b")),
 ]
+
+# kind::f16 candidates (> 128 outputs); the input is the pooled tensor
+F16_CASES = [
+    (52, 60, 80, dict(kind="CBCONV", kernelH=7, kernelW=7, padH=3, padW=3, outChannels=304, threshold=0.0, fuseRelu=True, weightsFile="b")),
+    (13, 34, 38, dict(kind="CBCONV", kernelH=3, kernelW=3, padH=1, padW=1, outChannels=300, threshold=0.0, fuseRelu=True, weightsFile="b")),
+    (20, 40, 50, dict(kind="CBCONV", kernelH=5, kernelW=3, strideH=2, strideW=1, padH=2, padW=1, outChannels=160, threshold=0.0, fuseRelu=False, weightsFile="b")),
+    (6, 26, 30, dict(kind="CONV", kernelH=1, kernelW=1, outChannels=136, weightsFile="b")),
+]
+
+
+def _geom(l, cin):
+    return dict(kernelH=l["kernelH"], kernelW=l["kernelW"], strideH=l.get("strideH", 1),
+                strideW=l.get("strideW", 1), padH=l.get("padH", 0), padW=l.get("padW", 0),
+                inChannels=cin, outChannels=l["outChannels"])
+
+
+def _check_layer(gpu, orc, net, onet, spec, wts, cfg, tested, cin, f16, frames=3, scale_in=None):
+    """Runs `frames` frames; the tested layer's input must match the oracle
+    bitwise (exact layers before it), its output within the operand bound."""
+    l = spec["layers"][tested]
+    g = _geom(l, cin)
+    K, b = wts[tested]
+    for f in range(frames):
+        fr = orc.synth_frame(cfg, f)
+        onet.forward_frame(fr)
+        net.forward_frame(fr)
+        x = onet.layer_output(tested - 1)
+        assert np.array_equal(net.layer_output(tested - 1).view(np.uint32), x.view(np.uint32))
+        want = onet.layer_output(tested)
+        got = net.layer_output(tested)
+        ho, wo = want.shape[1:]
+        X = orc.gen_x_reduced(np.abs(x), np.arange(ho * wo, dtype=np.int32), g)
+        scale = orc.gemm(np.abs(K), np.abs(b), X).reshape(want.shape).astype(np.float64)
+        bound = 2.0 ** -9 * scale + 1e-6
+        if f16:
+            ones = np.ones_like(X)
+            sum_w = orc.gemm(np.abs(K), np.zeros_like(b), ones).reshape(want.shape).astype(np.float64)
+            sum_x = X.astype(np.float64).sum(axis=1).reshape(want.shape[1:])[None]
+            bound = bound + 2.0 ** -24 * (sum_w + sum_x)
+        err = np.abs(got.astype(np.float64) - want)
+        assert np.all(err <= bound), (float((err / bound).max()), float(err.max()))
 
 
 @pytest.mark.parametrize("pair", [-1, 0, 1])
 @pytest.mark.parametrize("cin,h,w,layer", CASES)
 def test_tc_layer_vs_exact(gpu, orc, cin, h, w, layer, pair):
-    """pair: CBX_OPT_TC_PAIR (-1 auto = CTA pairs for N > 128, 0 single CTA, 1 pairs)."""
+    """pair: CBX_OPT_TC_PAIR (-1 auto = single CTA, 0 single CTA, 1 CTA pairs)."""
     check_tc_layer(gpu, orc, cin, h, w, layer, pair)
+
+
+def test_all_cases_run_on_tcgen05(gpu, orc):
+    """Every tf32 case above actually runs on the tensor cores (>= 32 outputs)."""
+    for cin, h, w, layer in CASES:
+        spec = two_layer(cin, h, w, layer)
+        net = gpu.Network(to_pkg_spec(gpu, spec), orc.generate_weights(spec, 11), precision="tf32")
+        assert net.layer_operands(1) == "tf32", layer
 
 
 @pytest.mark.parametrize("pair", [0, 1])
@@ -54,29 +118,40 @@ def check_tc_layer(gpu, orc, cin, h, w, layer, pair):
     net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="tf32")
     net.set_tc_pair(pair)
     cfg = dict(channels=3, height=h, width=w, sprites=[(5, 2, 0.9)], noise=0.02, seed=5)
-    for f in range(3):
-        fr = orc.synth_frame(cfg, f)
+    _check_layer(gpu, orc, net, onet, spec, wts, cfg, 1, cin, False)
+
+
+@pytest.mark.parametrize("magnitude", ["unit", "subnormal"])
+@pytest.mark.parametrize("maxctas", [None, "2"])
+@pytest.mark.parametrize("cin,h,w,layer", F16_CASES)
+def test_f16_layer_vs_exact(gpu, orc, monkeypatch, cin, h, w, layer, maxctas, magnitude):
+    """kind::f16 per-layer bound: a MAXPOOL-fed layer with > 128 outputs under
+    precision "f16" (the headline operand format of the paper's layer 3),
+    against the exact oracle on the same pooled input; 'subnormal' scales the
+    first layer so the pooled activations are ~1e-5 (fp16 subnormal range);
+    maxctas=2 makes every CTA walk several tiles."""
+    if maxctas:
+        monkeypatch.setenv("CBX_TC_MAXCTAS", maxctas)
+    spec = pooled_layer(cin, h, w, layer)
+    wts = orc.generate_weights(spec, 13)
+    if magnitude == "subnormal":
+        K0, b0 = wts[0]
+        wts[0] = ((K0 * 4e-5).astype(np.float32), (b0 * 4e-5).astype(np.float32))
+    onet = orc.load_network(spec, wts)
+    net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="f16")
+    assert net.layer_operands(2) == "f16"
+    cfg = dict(channels=3, height=h, width=w, sprites=[(5, 2, 0.9)], noise=0.02, seed=5)
+    if magnitude == "subnormal":
+        fr = orc.synth_frame(cfg, 0)
         onet.forward_frame(fr)
-        net.forward_frame(fr)
-        x = onet.layer_output(0)
-        assert np.array_equal(net.layer_output(0).view(np.uint32), x.view(np.uint32))
-        want = onet.layer_output(1)
-        got = net.layer_output(1)
-        l = spec["layers"][1]
-        g = dict(kernelH=l["kernelH"], kernelW=l["kernelW"], strideH=l.get("strideH", 1),
-                 strideW=l.get("strideW", 1), padH=l.get("padH", 0), padW=l.get("padW", 0),
-                 inChannels=cin, outChannels=l["outChannels"])
-        K, b = wts[1]
-        ho, wo = want.shape[1:]
-        X = orc.gen_x_reduced(np.abs(x), np.arange(ho * wo, dtype=np.int32), g)
-        scale = orc.gemm(np.abs(K), np.abs(b), X).reshape(want.shape)
-        err = np.abs(got.astype(np.float64) - want)
-        bound = 2.0 ** -9 * scale + 1e-6
-        assert np.all(err <= bound), (float((err / bound).max()), float(err.max()))
+        x = onet.layer_output(1)
+        assert 0 < np.abs(x).max() < 6.1e-5 * 4  # mostly below the fp16 normal range
+        onet.reset_state()
+    _check_layer(gpu, orc, net, onet, spec, wts, cfg, 2, cin, True)
 
 
-@pytest.mark.parametrize("maxctas,f16", [(None, "1"), ("3", "1"), (None, "0")])
-def test_fused_tail_equals_unfused(gpu, orc, monkeypatch, maxctas, f16):
+@pytest.mark.parametrize("maxctas,prec", [(None, "f16"), ("3", "f16"), (None, "tf32")])
+def test_fused_tail_equals_unfused(gpu, orc, monkeypatch, maxctas, prec):
     """The per-pixel head (1x1 CONV, RELU, 1x1 CONV, CLASSIFY) run inside the
     last tcgen05 conv's epilogue gives bitwise the same labels, final
     activation and stats as running every layer separately (maxctas: grid
@@ -84,11 +159,10 @@ def test_fused_tail_equals_unfused(gpu, orc, monkeypatch, maxctas, f16):
     from netutil import paper_spec, stats_arr
     if maxctas:
         monkeypatch.setenv("CBX_TC_MAXCTAS", maxctas)
-    monkeypatch.setenv("CBX_TC_F16", f16)
     spec = paper_spec(72, 112)
     w = orc.generate_weights(spec, 1)
-    fused = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32", fuse_tail=True)
-    plain = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32", fuse_tail=False)
+    fused = gpu.Network(to_pkg_spec(gpu, spec), w, precision=prec, fuse_tail=True)
+    plain = gpu.Network(to_pkg_spec(gpu, spec), w, precision=prec, fuse_tail=False)
     cfg = dict(channels=3, height=72, width=112, sprites=[(14, 3, 0.9)], noise=0.01, seed=4)
     for f in range(4):
         fr = orc.synth_frame(cfg, f)
