@@ -152,7 +152,11 @@ CBX_API int cbx_get_thresholds(const cbx_ctx* ctx, float* taus, int n);
  * tcgen05 convs. 1 pairs the two SMs of a TPC (cta_group::2, M = 256 tiles,
  * each SM holds half the filter bank); 0 forces one CTA per tile. Same tf32
  * error bound either way. */
-typedef enum { CBX_OPT_FUSE_TAIL = 0, CBX_OPT_TC_PAIR = 1 } cbx_option;
+/* CBX_OPT_STEP_TIMES (default 0): record CUDA event nodes at the kernel
+ * boundaries of the frame graph so cbx_read_step_times can return the
+ * reference's per-layer StepTimes (cbconv.hpp:44-52) -- the collectTimings
+ * switch of CBConvState (cbconv.hpp:70). Off: no timing nodes in the graph. */
+typedef enum { CBX_OPT_FUSE_TAIL = 0, CBX_OPT_TC_PAIR = 1, CBX_OPT_STEP_TIMES = 2 } cbx_option;
 CBX_API int cbx_set_option(cbx_ctx* ctx, int option, int value);
 
 /* Drops all change-based state of every stream: the next frame is a full
@@ -192,6 +196,15 @@ CBX_API int cbx_forward_device(cbx_ctx* ctx, int engine, const float* const* fra
  * last 3 tickets can be waited on. Change-based engine only. */
 CBX_API int cbx_submit(cbx_ctx* ctx, int engine, const float* frames, uint16_t* labels, int64_t* ticket);
 CBX_API int cbx_wait(cbx_ctx* ctx, int64_t ticket, cbx_layer_stats* stats, uint64_t* macs);
+/* 8-bit camera frames (read_ppm, io.cpp:60-104): `frames` holds S frames back
+ * to back, each H x W pixels of inputChannels interleaved bytes (the binary
+ * PPM raster). Only the bytes cross PCIe (4x fewer than fp32 planar frames);
+ * the device decodes them into the planar fp32 frame px / 255.0f exactly as
+ * read_ppm does, so results equal cbx_forward / cbx_submit on read_ppm's
+ * tensors bit for bit. Same semantics and ticket ring otherwise. */
+CBX_API int cbx_forward_u8(cbx_ctx* ctx, int engine, const uint8_t* frames, uint16_t* labels,
+                           cbx_layer_stats* stats, uint64_t* macs);
+CBX_API int cbx_submit_u8(cbx_ctx* ctx, int engine, const uint8_t* frames, uint16_t* labels, int64_t* ticket);
 /* cbench analyze-prop (tools/cbench.cpp:242-302) for the last change-based
  * frame (not a full one): for every CBCONV k >= 1 (0-based among CBCONVs), the
  * worst-case updated count of layer k -- the updated set of CBCONV k-1 pushed
@@ -230,6 +243,26 @@ CBX_API int cbx_profile_forward(cbx_ctx* ctx, int engine, const float* const* fr
 CBX_API int cbx_get_activation(cbx_ctx* ctx, int engine, int layer, int s, float* out);
 CBX_API int cbx_get_trace(cbx_ctx* ctx, int cb, int s, uint8_t* detected, int32_t* updated,
                           int64_t* n, int* first);
+/* Input tensor of layer `layer` for stream s after the last frame, planar CHW
+ * host floats: the reference's CBConvState::prevInput (cbconv.hpp:71) when the
+ * layer is a CBCONV. Layer 0 returns the last frame the change-based engine
+ * consumed (CBX_E_SPEC before the first frame / after a reset). */
+CBX_API int cbx_get_input(cbx_ctx* ctx, int engine, int layer, int s, float* out);
+/* 1 when the change-based state holds a previous frame (CBConvState::
+ * has_history, cbconv.hpp:73): the next frame is evaluated incrementally;
+ * 0 after creation, cbx_reset or an fp16 range error; -1 on a null context. */
+CBX_API int cbx_has_history(const cbx_ctx* ctx);
+/* StepTimes of the last frame launched with CBX_OPT_STEP_TIMES on:
+ * nanos[(s * numLayers + k) * 5 + {0..4}] = detect, extract, generate,
+ * multiply, update of layer k (stepNanos, cbconv.hpp:44-52; 0 for non-CBCONV
+ * work that has no step). The B200 kernels fuse steps: detect = the frame
+ * detection kernel (first CBCONV; later CBCONVs detect inside their
+ * producer's compare-before-write), extract = dilation + compaction,
+ * multiply = the gathered convolution including the patch gather (generate)
+ * and the in-place scatter (update), which therefore read 0. Streams that
+ * share a lane share the lane's kernels and report the same times. Timed
+ * with CUDA events on the device; all zero when the option is off. */
+CBX_API int cbx_read_step_times(cbx_ctx* ctx, int64_t* nanos);
 
 /* ---- op level, device pointers, asynchronous on `stream` (cudaStream_t) ---- */
 CBX_API int cbx_op_detect(const float* cur, const float* prev, int C, int H, int W, float tau,
@@ -243,6 +276,27 @@ CBX_API int cbx_op_extract(const uint8_t* mask, int64_t n, int32_t* idx, int* co
 CBX_API int cbx_op_maxpool(const float* in, int C, int H, int W, int window, int stride,
                            float* out, void* stream);
 CBX_API int cbx_op_argmax(const float* t, int C, int H, int W, uint16_t* labels, void* stream);
+/* Matrix-form reference ops (the network path never materializes X or Y):
+ *   cbx_op_gen_x   <- gen_x_reduced / im2col_full / fill_patch_column
+ *                     (cbconv.cpp:115-133, baseline.cpp:9-45): X column-major
+ *                     [n][C*kh*kw], column j = the (c,kj,ki) receptive field of
+ *                     output pixel idx[j] (idx NULL: pixel j), zero padded.
+ *                     Indices must lie in [0, Ho*Wo) (checked by the caller).
+ *   cbx_op_gemm    <- gemm (baseline.cpp:47-63): Y row-major [rows][n] =
+ *                     bias + K X, ascending r, no FMA (bitwise the reference).
+ *   cbx_op_scatter <- update_output without its copy (cbconv.cpp:135-155):
+ *                     out[c][idx[j]] = Y[c][j] (max(0, .) when relu), in place. */
+CBX_API int cbx_op_gen_x(const float* in, int C, int H, int W, const cbx_geom* geom, const int32_t* idx,
+                         int64_t n, float* X, void* stream);
+CBX_API int cbx_op_gemm(const float* K, const float* bias, int rows, int cols, const float* X, int64_t n,
+                        float* Y, void* stream);
+CBX_API int cbx_op_scatter(float* out, int C, int H, int W, const float* Y, const int32_t* idx, int64_t n,
+                           int relu, void* stream);
+/* The decode of cbx_forward_u8 on device buffers: S interleaved 8-bit frames
+ * (H x W x C) -> S planar fp32 frames px / 255.0f (read_ppm, io.cpp:60-104). */
+CBX_API int cbx_op_decode_u8(const uint8_t* in, int S, int C, int H, int W, float* out, void* stream);
+/* relu (baseline.cpp:113-117): out = max(0, in) element-wise, planar CHW. */
+CBX_API int cbx_op_relu(const float* in, int C, int H, int W, float* out, void* stream);
 /* Reduced conv over an index list (gen_x_reduced + gemm + update_output,
  * cbconv.cpp:115-155), planar CHW in/out, exact fp32 order; out is updated in
  * place at the listed output pixels. */

@@ -253,6 +253,13 @@ def synth_frame_device(cfg: dict, f: int, out_ptr: int, stream: int = 0) -> None
     check(lib.cbx_synth_frame_device(C.byref(c), f, C.c_void_p(out_ptr), C.c_void_p(stream)))
 
 
+def decode_u8_device(in_ptr: int, S: int, channels: int, height: int, width: int, out_ptr: int,
+                     stream: int = 0) -> None:
+    """cbx_op_decode_u8: S interleaved 8-bit frames on the device -> planar fp32 px / 255."""
+    check(lib.cbx_op_decode_u8(C.c_void_p(in_ptr), S, channels, height, width, C.c_void_p(out_ptr),
+                               C.c_void_p(stream)))
+
+
 # ---------------------------------------------------------------- network
 @dataclass
 class ForwardResult:
@@ -343,6 +350,28 @@ class Network:
         tcgen05 conv's epilogue (default) or materialize every layer."""
         self._chk(lib.cbx_set_option(self._h, 0, int(bool(on))))
 
+    def set_step_times(self, on: bool) -> None:
+        """CBX_OPT_STEP_TIMES: event nodes at the kernel boundaries of the frame
+        graph; step_times() then returns the reference's StepTimes per layer."""
+        self._chk(lib.cbx_set_option(self._h, 2, int(bool(on))))
+
+    def step_times(self) -> np.ndarray:
+        """[S, layers, 5] ns (detect, extract, generate, multiply, update) of
+        the last frame (StepTimes, cbconv.hpp:44-52; see cbx_read_step_times)."""
+        out = np.zeros((self.streams, self.nl, 5), np.int64)
+        self._chk(lib.cbx_read_step_times(self._h, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out
+
+    def has_history(self) -> bool:
+        return lib.cbx_has_history(self._h) == 1
+
+    def layer_input(self, layer: int, s: int = 0, engine: str = "cbinfer") -> np.ndarray:
+        """Input tensor of `layer` after the last frame (prevInput of a CBCONV)."""
+        c, h, w = self.shapes[layer][0]
+        out = np.zeros((c, h, w), np.float32)
+        self._chk(lib.cbx_get_input(self._h, ENGINES[engine], layer, s, out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out
+
     def set_tc_pair(self, mode: int) -> None:
         """CBX_OPT_TC_PAIR: -1 auto (single-CTA tiles), 0 single-CTA tiles,
         1 CTA pairs (cta_group::2) everywhere."""
@@ -367,6 +396,37 @@ class Network:
                        gemmMacs=stats[s * self.nl + k].gemmMacs) for k in range(self.nl)]
             out.append(ForwardResult(labels[s], st, macs[s]))
         return out
+
+    def forward_u8(self, frames: np.ndarray, engine: str = "cbinfer") -> List[ForwardResult]:
+        """cbx_forward_u8: 8-bit camera frames [S, H, W, C] (or [H, W, C]),
+        interleaved like the binary PPM raster; decoded on the device as
+        read_ppm does (px / 255, io.cpp:60-104)."""
+        f = np.ascontiguousarray(frames, np.uint8)
+        if f.size != self._frame_elems * self.streams:
+            raise ShapeError("forward_frame: frame does not match network input dimensions")
+        S = self.streams
+        labels = np.zeros((S,) + tuple(self.label_hw), np.uint16)
+        stats = (LayerStats * (S * self.nl))()
+        macs = (C.c_uint64 * S)()
+        self._chk(lib.cbx_forward_u8(self._h, ENGINES[engine], f.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                     labels.ctypes.data_as(C.POINTER(C.c_uint16)), stats, macs))
+        return [ForwardResult(labels[s], [dict(changedInputPixels=stats[s * self.nl + k].changedInputPixels,
+                                               changedOutputPixels=stats[s * self.nl + k].changedOutputPixels,
+                                               gemmMacs=stats[s * self.nl + k].gemmMacs) for k in range(self.nl)],
+                              macs[s]) for s in range(S)]
+
+    def submit_u8(self, frames: np.ndarray, labels: np.ndarray) -> int:
+        """cbx_submit_u8: as submit() with 8-bit interleaved frames [S, H, W, C]
+        (4x fewer bytes over PCIe), decoded on the device."""
+        if frames.dtype != np.uint8 or not frames.flags.c_contiguous or frames.size != self._frame_elems * self.streams:
+            raise ShapeError("submit_u8: frames must be a contiguous uint8 [S, H, W, C] array of the network input")
+        want = (self.streams,) + tuple(self.label_hw)
+        if labels.dtype != np.uint16 or not labels.flags.c_contiguous or labels.shape != want:
+            raise ShapeError(f"submit_u8: labels must be a contiguous uint16 array of shape {want}")
+        t = C.c_int64()
+        self._chk(lib.cbx_submit_u8(self._h, ENGINES["cbinfer"], frames.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                    labels.ctypes.data_as(C.POINTER(C.c_uint16)), C.byref(t)))
+        return t.value
 
     def submit(self, frames: np.ndarray, labels: np.ndarray) -> int:
         """cbx_submit: enqueue the next frame of every stream ([S, C, H, W]

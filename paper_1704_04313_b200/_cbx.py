@@ -96,6 +96,10 @@ lib.cbx_stream.argtypes = [VP]
 lib.cbx_last_launch_count.argtypes = [VP]
 lib.cbx_op_extract_workspace.restype = C.c_size_t
 lib.cbx_op_extract_workspace.argtypes = [C.c_int64]
+lib.cbx_has_history.argtypes = [VP]
+lib.cbx_submit_u8.argtypes = [VP, C.c_int, C.POINTER(C.c_uint8), C.POINTER(C.c_uint16), C.POINTER(C.c_int64)]
+lib.cbx_get_input.argtypes = [VP, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]
+lib.cbx_read_step_times.argtypes = [VP, C.POINTER(C.c_int64)]
 for _name in ("cbx_load_layer", "cbx_set_thresholds", "cbx_get_thresholds", "cbx_set_option", "cbx_reset", "cbx_forward",
               "cbx_forward_device", "cbx_sync", "cbx_read_labels", "cbx_read_stats", "cbx_labels_device",
               "cbx_get_activation", "cbx_get_trace", "cbx_destroy"):
@@ -117,6 +121,8 @@ EXPORTS = [
     "cbx_last_launch_count", "cbx_profile_forward", "cbx_get_activation", "cbx_get_trace", "cbx_op_detect", "cbx_op_dilate",
     "cbx_op_extract_workspace", "cbx_op_extract", "cbx_op_maxpool", "cbx_op_argmax",
     "cbx_op_cbconv_update", "cbx_random_filters", "cbx_synth_frame", "cbx_synth_frame_device",
+    "cbx_get_input", "cbx_has_history", "cbx_read_step_times", "cbx_op_relu", "cbx_op_gen_x", "cbx_op_gemm",
+    "cbx_op_scatter", "cbx_forward_u8", "cbx_submit_u8", "cbx_op_decode_u8",
 ]
 
 

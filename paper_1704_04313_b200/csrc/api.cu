@@ -175,6 +175,18 @@ CBX_API int cbx_submit(cbx_ctx* ctx, int engine, const float* frames, uint16_t* 
     });
 }
 
+CBX_API int cbx_forward_u8(cbx_ctx* ctx, int engine, const uint8_t* frames, uint16_t* labels, cbx_layer_stats* stats,
+                           uint64_t* macs) {
+    return guarded(ctx, [&] { E(ctx).forward_host_u8(engine, frames, labels, stats, macs); });
+}
+
+CBX_API int cbx_submit_u8(cbx_ctx* ctx, int engine, const uint8_t* frames, uint16_t* labels, int64_t* ticket) {
+    return guarded(ctx, [&] {
+        const int64_t t = E(ctx).submit_u8(engine, frames, labels);
+        if (ticket) *ticket = t;
+    });
+}
+
 CBX_API int cbx_wait(cbx_ctx* ctx, int64_t ticket, cbx_layer_stats* stats, uint64_t* macs) {
     return guarded(ctx, [&] { E(ctx).wait(ticket, stats, macs); });
 }
@@ -229,6 +241,21 @@ CBX_API int cbx_profile_forward(cbx_ctx* ctx, int engine, const float* const* fr
         if (out && m > 0) std::memcpy(out, v.data(), sizeof(cbx_kernel_time) * m);
         if (n) *n = (int)v.size();
     });
+}
+
+CBX_API int cbx_get_input(cbx_ctx* ctx, int engine, int layer, int s, float* out) {
+    return guarded(ctx, [&] {
+        if (!out) throw cbx::Error(CBX_E_ARG, "null output");
+        E(ctx).get_input(engine, layer, s, out);
+    });
+}
+
+CBX_API int cbx_has_history(const cbx_ctx* ctx) {
+    return ctx && ctx->eng ? (ctx->eng->has_history() ? 1 : 0) : -1;
+}
+
+CBX_API int cbx_read_step_times(cbx_ctx* ctx, int64_t* nanos) {
+    return guarded(ctx, [&] { E(ctx).read_step_times(nanos); });
 }
 
 // ---- op level ---------------------------------------------------------
@@ -324,6 +351,72 @@ CBX_API int cbx_op_argmax(const float* t, int C, int H, int W, uint16_t* labels,
         a.S = 1;
         cbx::launch_classify(a, st);
         CBX_CUDA(cudaFreeAsync(ti.d, st));
+        CBX_CUDA(cudaGetLastError());
+    });
+}
+
+CBX_API int cbx_op_gen_x(const float* in, int C, int H, int W, const cbx_geom* g, const int32_t* idx,
+                         int64_t n, float* X, void* stream) {
+    return guarded(nullptr, [&] {
+        if (!in || !g || (n > 0 && !X)) throw cbx::Error(CBX_E_ARG, "null pointer");
+        if (C != g->inChannels) throw cbx::Error(CBX_E_SHAPE, "gen_x_reduced: channel count mismatch");
+        if (g->kernelH < 1 || g->kernelW < 1 || g->strideH < 1 || g->strideW < 1 || g->padH < 0 || g->padW < 0 ||
+            H + 2 * g->padH < g->kernelH || W + 2 * g->padW < g->kernelW)
+            throw cbx::Error(CBX_E_GEOMETRY, "invalid convolution geometry or empty output");
+        cbx::launch_gen_x(in, C, H, W, g->kernelH, g->kernelW, g->strideH, g->strideW, g->padH, g->padW, idx, n, X,
+                          (cudaStream_t)stream);
+        CBX_CUDA(cudaGetLastError());
+    });
+}
+
+CBX_API int cbx_op_gemm(const float* K, const float* bias, int rows, int cols, const float* X, int64_t n, float* Y,
+                        void* stream) {
+    return guarded(nullptr, [&] {
+        if (rows < 0 || cols < 0 || n < 0) throw cbx::Error(CBX_E_SHAPE, "gemm: negative dimension");
+        if (rows && n && (!K || !bias || !Y || (cols && !X))) throw cbx::Error(CBX_E_ARG, "null pointer");
+        cbx::launch_gemm_exact(K, bias, rows, cols, X, n, Y, (cudaStream_t)stream);
+        CBX_CUDA(cudaGetLastError());
+    });
+}
+
+CBX_API int cbx_op_scatter(float* out, int C, int H, int W, const float* Y, const int32_t* idx, int64_t n, int relu,
+                           void* stream) {
+    return guarded(nullptr, [&] {
+        if (n > 0 && (!out || !Y || !idx)) throw cbx::Error(CBX_E_ARG, "null pointer");
+        cbx::launch_scatter(out, C, (int64_t)H * W, Y, idx, n, relu, (cudaStream_t)stream);
+        CBX_CUDA(cudaGetLastError());
+    });
+}
+
+CBX_API int cbx_op_decode_u8(const uint8_t* in, int S, int C, int H, int W, float* out, void* stream) {
+    return guarded(nullptr, [&] {
+        if (!in || !out) throw cbx::Error(CBX_E_ARG, "null pointer");
+        if (S < 1 || C < 1 || H < 1 || W < 1) throw cbx::Error(CBX_E_SHAPE, "decode_u8: empty frame");
+        cbx::launch_decode_u8(in, S, C, H, W, out, (cudaStream_t)stream);
+        CBX_CUDA(cudaGetLastError());
+    });
+}
+
+CBX_API int cbx_op_relu(const float* in, int C, int H, int W, float* out, void* stream) {
+    return guarded(nullptr, [&] {
+        if (!in || !out) throw cbx::Error(CBX_E_ARG, "null pointer");
+        if (C < 1 || H < 1 || W < 1) throw cbx::Error(CBX_E_SHAPE, "relu: empty tensor");
+        cudaStream_t st = (cudaStream_t)stream;
+        const int Cp = (int)cbx::round_up(C, 4);
+        cbx::TensorView ti{nullptr, C, H, W, Cp, H, W, 0, 0, (int64_t)H * W * Cp};
+        cbx::TensorView to = ti;
+        CBX_CUDA(cudaMallocAsync((void**)&ti.d, ti.ss * 4, st));
+        CBX_CUDA(cudaMallocAsync((void**)&to.d, to.ss * 4, st));
+        CBX_CUDA(cudaMemsetAsync(ti.d, 0, ti.ss * 4, st));
+        cbx::launch_chw_to_hwc(in, ti, 0, st);
+        cbx::PointArgs a{};
+        a.in = ti;
+        a.out = to;
+        a.S = 1;
+        cbx::launch_relu(a, st);
+        cbx::launch_hwc_to_chw(to, 0, out, st);
+        CBX_CUDA(cudaFreeAsync(ti.d, st));
+        CBX_CUDA(cudaFreeAsync(to.d, st));
         CBX_CUDA(cudaGetLastError());
     });
 }

@@ -82,6 +82,26 @@ void Context::forward_host(int engine, const float* frames, uint16_t* labels, cb
     read_stats(engine, stats, macs);
 }
 
+void Context::forward_host_u8(int engine, const uint8_t* frames, uint16_t* labels, cbx_layer_stats* stats,
+                              uint64_t* macs) {
+    if (!frames) throw Error(CBX_E_ARG, "frames is null");
+    for (size_t l = 0; l < lanes_.size(); ++l) lanes_[l]->enqueue_host_u8(engine, frames + frame_elems_ * off_[l]);
+    join();
+    if (labels) read_labels(engine, labels);
+    read_stats(engine, stats, macs);
+}
+
+int64_t Context::submit_u8(int engine, const uint8_t* frames, uint16_t* labels) {
+    if (!frames || !labels) throw Error(CBX_E_ARG, "null frames or labels");
+    Sub& sub = subs_[submitted_ % 3];
+    sub.lane_tickets.assign(lanes_.size(), -1);
+    for (size_t l = 0; l < lanes_.size(); ++l)
+        sub.lane_tickets[l] =
+            lanes_[l]->submit_u8(engine, frames + frame_elems_ * off_[l], labels + (size_t)lh_ * lw_ * off_[l]);
+    sub.ticket = submitted_;
+    return submitted_++;
+}
+
 void Context::forward_device(int engine, const float* const* frames_dev) {
     if (!frames_dev) throw Error(CBX_E_ARG, "frames is null");
     for (size_t l = 0; l < lanes_.size(); ++l) lanes_[l]->forward_device(engine, frames_dev + off_[l]);
@@ -140,6 +160,22 @@ void Context::get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int6
     int local;
     const int l = lane_of(s, local);
     lanes_[l]->get_trace(cb, local, detected, updated, n, first);
+}
+
+void Context::get_input(int engine, int layer, int s, float* out) {
+    int local;
+    const int l = lane_of(s, local);
+    lanes_[l]->get_input(engine, layer, local, out);
+}
+
+void Context::read_step_times(int64_t* nanos) {
+    if (!nanos) throw Error(CBX_E_ARG, "null output");
+    std::vector<int64_t> lane((size_t)nl_ * 5);
+    for (size_t l = 0; l < lanes_.size(); ++l) {
+        lanes_[l]->read_step_times(lane.data());
+        for (int s = off_[l]; s < off_[l + 1]; ++s)
+            std::memcpy(nanos + (size_t)s * nl_ * 5, lane.data(), sizeof(int64_t) * lane.size());
+    }
 }
 
 void Context::worst_case_counts(int64_t* worst) {

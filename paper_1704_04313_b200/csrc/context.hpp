@@ -40,6 +40,8 @@ public:
     // frames
     void forward_host(int engine, const float* frames, uint16_t* labels, cbx_layer_stats* stats, uint64_t* macs);
     void forward_device(int engine, const float* const* frames_dev);
+    void forward_host_u8(int engine, const uint8_t* frames, uint16_t* labels, cbx_layer_stats* stats, uint64_t* macs);
+    int64_t submit_u8(int engine, const uint8_t* frames, uint16_t* labels);
     int64_t submit(int engine, const float* frames, uint16_t* labels);
     void wait(int64_t ticket, cbx_layer_stats* stats, uint64_t* macs);
     void sync();
@@ -50,6 +52,9 @@ public:
     const uint16_t* labels_device(int engine);
     void get_activation(int engine, int layer, int s, float* out);
     void get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64_t* n, int* first);
+    void get_input(int engine, int layer, int s, float* out);
+    bool has_history() const { return lanes_[0]->has_history(); }
+    void read_step_times(int64_t* nanos);  // [S][nl][5]
     void worst_case_counts(int64_t* worst);
     void profile(int engine, const float* const* frames_dev, std::vector<cbx_kernel_time>& out);
     int last_launch_count() const;

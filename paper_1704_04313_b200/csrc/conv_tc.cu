@@ -164,6 +164,13 @@ __device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint6
         "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
 // arrive (when the issued MMAs complete) on the barrier at this smem offset in both CTAs of the pair
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
     asm volatile(
@@ -437,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], PAIR ? 2 * (kEpiThreads / 32) : kEpiThreads);
         }
-        mbar_init(tshared, kEpiThreads);
+        mbar_init(tshared, PAIR ? 2 * (kEpiThreads / 32) : kEpiThreads);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 8) {
@@ -631,7 +638,9 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             for (int64_t tile = tile_first; tile < ntiles; tile += tile_step, ++acc_it) {
                 const uint32_t as = acc_it % a.acc_stages, aph = (acc_it / a.acc_stages) & 1u;
                 if constexpr (PAIR) mbar_wait_cluster(&tempty[as], aph ^ 1u); else mbar_wait(&tempty[as], aph ^ 1u);
-                if (a.ovl && acc_it > 0) mbar_wait(tshared, (acc_it - 1) & 1u);
+                if (a.ovl && acc_it > 0) {
+                    if constexpr (PAIR) mbar_wait_cluster(tshared, (acc_it - 1) & 1u); else mbar_wait(tshared, (acc_it - 1) & 1u);
+                }
                 tc_fence_after();
                 const uint32_t d = tmem_base + (a.ovl ? (uint32_t)a.ovl_s : as * a.acc_cols);
                 const uint32_t d1 = a.ovl ? tmem_base + (uint32_t)(as ? a.ovl_b1 : a.ovl_b0) : d + a.N0;
@@ -650,8 +659,13 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                         for (int k = 0; k < kKBlock / 8; ++k) {
                             const uint32_t accum = (kb | k) ? 1u : 0u;
                             if constexpr (PAIR) {
-                                mma_tf32_pair(d, ad + 2 * k, bd + 2 * k, id0, accum);
-                                if (two) mma_tf32_pair(d + a.N0, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
+                                if (f16) {
+                                    mma_f16_pair(d, ad + 2 * k, bd + 2 * k, id0, accum);
+                                    if (two) mma_f16_pair(d1, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
+                                } else {
+                                    mma_tf32_pair(d, ad + 2 * k, bd + 2 * k, id0, accum);
+                                    if (two) mma_tf32_pair(d1, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
+                                }
                             } else if (f16) {
                                 mma_f16(d, ad + 2 * k, bd + 2 * k, id0, accum);
                                 if (two) mma_f16(d1, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
@@ -717,7 +731,12 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 if (a.ovl && c0 + 32 == a.N0) {
                     // shared columns drained: the next tile's MMAs may start
                     tc_fence_before();
-                    mbar_arrive(tshared);
+                    if constexpr (PAIR) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(mapa(tshared, 0));
+                    } else {
+                        mbar_arrive(tshared);
+                    }
                 }
                 if (!valid) continue;
                 if (c0 + 32 <= a.O)
@@ -820,7 +839,6 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     // fp16 operands: 8 channels per 16-byte chunk; Cp stays in 4-byte units so
     // the gather's address arithmetic is the same for both operand types
     t->f16 = f16;
-    if (f16) pair_mode = 0;
     t->Cp = f16 ? (int)round_up(g.inChannels, 8) / 2 : (int)round_up(g.inChannels, 4);
     const int nchunks = g.kernelH * g.kernelW * (t->Cp / 4);
     t->NKB = (nchunks + kChunksPerKB - 1) / kChunksPerKB;
@@ -847,7 +865,7 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     // then waits only for tile t's first four 32-channel chunks.
     // CBX_TC_OVL=0 keeps the single accumulator (tuning).
     const char* ovl_env = std::getenv("CBX_TC_OVL");
-    if (pair_mode <= 0 && t->Npad > 256 && !(ovl_env && std::atoi(ovl_env) == 0)) {
+    if (t->Npad > 256 && !(ovl_env && std::atoi(ovl_env) == 0)) {
         const int n0 = 128, n1 = t->Npad - n0;
         const int s0 = (int)round_up(n1, 32);
         if (n1 <= 256 && s0 + t->Npad <= 512) {
@@ -932,18 +950,36 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
     const int C4 = t.Cp / 4, khw = g.kernelH * g.kernelW;
     const int Kref = g.inChannels * khw;
     const int ranks = t.pair ? 2 : 1;
+    // filter row of output channel n: single CTA -> row n of the one image; CTA
+    // pair -> each rank holds its half of every instruction's N columns
+    auto place = [&](int n, int& rank, int& row) {
+        rank = 0;
+        row = n;
+        if (!t.pair) return;
+        if (n < t.N0) {
+            rank = n / (t.N0 / 2);
+            row = n % (t.N0 / 2);
+        } else {
+            const int m = n - t.N0;
+            rank = m / (t.N1 / 2);
+            row = t.N0 / 2 + m % (t.N1 / 2);
+        }
+    };
     if (t.f16) {
         // fp16 image (round to nearest even): chunk J = tap * C4 + c4 holds
-        // channels 8*c4 .. 8*c4+7 of that tap; half (n, kb*64 + j*8 + e) at
-        // kb*Npad*64 + n*64 + (j ^ (n & 7))*8 + e
+        // channels 8*c4 .. 8*c4+7 of that tap; half (row, kb*64 + j*8 + e) at
+        // kb*Brows*64 + row*64 + (j ^ (row & 7))*8 + e of its rank's image
         // fp16 range: a weight beyond 65504 would become inf (the activations
         // are range-checked per frame by the shadow writer, engine.cu)
         for (size_t i = 0; i < (size_t)g.outChannels * Kref; ++i)
             if (std::fabs(K[i]) > 65504.0f)
                 throw Error(CBX_E_ARG, "a filter weight of a kind::f16 layer exceeds the fp16 range (|w| > 65504); "
                                        "create the context with CBX_PREC_TF32");
-        std::vector<__half> img((size_t)t.NKB * t.Brows * 64, __float2half_rn(0.0f));
-        for (int n = 0; n < g.outChannels; ++n)
+        std::vector<__half> img((size_t)ranks * t.NKB * t.Brows * 64, __float2half_rn(0.0f));
+        for (int n = 0; n < g.outChannels; ++n) {
+            int rank, row;
+            place(n, rank, row);
+            __half* base = img.data() + (size_t)rank * t.NKB * t.Brows * 64;
             for (int J = 0; J < t.NKB * kChunksPerKB; ++J) {
                 const int tap = J / C4, c4 = J - tap * C4;
                 if (tap >= khw) continue;
@@ -951,27 +987,19 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
                 for (int e = 0; e < 8; ++e) {
                     const int c = c4 * 8 + e;
                     if (c >= g.inChannels) continue;
-                    img[(size_t)kb * t.Brows * 64 + (size_t)n * 64 + ((j ^ (n & 7)) * 8) + e] =
+                    base[(size_t)kb * t.Brows * 64 + (size_t)row * 64 + ((j ^ (row & 7)) * 8) + e] =
                         __float2half_rn(K[(size_t)n * Kref + (size_t)c * khw + tap]);
                 }
             }
+        }
         CBX_CUDA(cudaMemcpyAsync(t.Bw, img.data(), img.size() * sizeof(__half), cudaMemcpyHostToDevice, st));
         CBX_CUDA(cudaStreamSynchronize(st));
         return;
     }
     std::vector<float> img((size_t)ranks * t.NKB * t.Brows * kKBlock, 0.0f);
     for (int n = 0; n < g.outChannels; ++n) {
-        int rank = 0, row = n;
-        if (t.pair) {
-            if (n < t.N0) {
-                rank = n / (t.N0 / 2);
-                row = n % (t.N0 / 2);
-            } else {
-                const int m = n - t.N0;
-                rank = m / (t.N1 / 2);
-                row = t.N0 / 2 + m % (t.N1 / 2);
-            }
-        }
+        int rank, row;
+        place(n, rank, row);
         float* base = img.data() + (size_t)rank * t.NKB * t.Brows * kKBlock;
         for (int J = 0; J < t.NKB * kChunksPerKB; ++J) {
             const int tap = J / C4, c4 = J - tap * C4;

@@ -34,8 +34,10 @@
 namespace cbx {
 
 void cuda_check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess)
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();  // a non-sticky error must not leak into the caller's next CUDA call
         throw Error(CBX_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
 }
 
 namespace {
@@ -147,6 +149,12 @@ struct Engine::Plan {
     unsigned long long* stats = nullptr;  // [nl][S][2]
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int launches[2] = {0, 0};
+    // CBX_OPT_STEP_TIMES: event-record nodes at the kernel boundaries of each graph
+    std::vector<Engine::ProfMark> tm[2];
+    void drop_marks(int m) {
+        for (auto& x : tm[m]) cudaEventDestroy(x.ev);
+        tm[m].clear();
+    }
     bool dirty = true;
     int fused_from = -1;            // conv layer whose epilogue runs the per-pixel tail (-1: none)
     uint32_t* work = nullptr;       // touched-pixel list shared by the MAXPOOL/RELU layers
@@ -162,6 +170,8 @@ struct Engine::Plan {
     ~Plan() {
         for (auto& g : gexec)
             if (g) cudaGraphExecDestroy(g);
+        drop_marks(0);
+        drop_marks(1);
         for (void* p : allocs) cudaFree(p);
     }
     template <class T>
@@ -253,7 +263,9 @@ Engine::~Engine() {
     for (auto& s : slots_) cudaFree(s);
     cudaFreeHost(h_stats_);
     if (copy_st_) cudaStreamSynchronize(copy_st_);
+    if (u8_stage_) cudaFree(u8_stage_);
     for (int q = 0; q < kRing; ++q) {
+        if (ring_u8_[q]) cudaFree(ring_u8_[q]);
         if (ring_[q]) cudaFree(ring_[q]);
         if (copied_[q]) cudaEventDestroy(copied_[q]);
         if (done_[q]) cudaEventDestroy(done_[q]);
@@ -647,13 +659,32 @@ void Engine::launch(Plan& p, bool full) {
     }
     if (!p.gexec[m]) {
         cudaGraph_t graph = nullptr;
+        p.drop_marks(m);
+        if (step_times_) {  // events exist before the capture records them
+            for (int i = 0; i < 64; ++i) {
+                cudaEvent_t e;
+                CBX_CUDA(cudaEventCreate(&e));
+                p.tm[m].push_back(ProfMark{"", -1, e});
+            }
+        }
         CBX_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
         try {
+            if (step_times_) {
+                tmarks_ = &p.tm[m];
+                tmarks_used_ = 0;
+                mark("start", -1);
+            }
             record(p, full);
+            tmarks_ = nullptr;
         } catch (...) {
+            tmarks_ = nullptr;
             cudaStreamEndCapture(stream_, &graph);
             if (graph) cudaGraphDestroy(graph);
             throw;
+        }
+        if (step_times_) {
+            for (size_t i = tmarks_used_; i < p.tm[m].size(); ++i) cudaEventDestroy(p.tm[m][i].ev);
+            p.tm[m].resize(tmarks_used_);
         }
         CBX_CUDA(cudaStreamEndCapture(stream_, &graph));
         size_t n = 0;
@@ -672,6 +703,7 @@ void Engine::launch(Plan& p, bool full) {
     }
     CBX_CUDA(cudaGraphLaunch(p.gexec[m], stream_));
     last_launches_ = p.launches[m];
+    last_tm_ = step_times_ ? &p.tm[m] : nullptr;
 }
 
 void Engine::stage_frame_pointers(int engine, const float* const* cur, const float* const* prev) {
@@ -691,6 +723,31 @@ void Engine::stage_frame_pointers(int engine, const float* const* cur, const flo
 void Engine::forward_host(int engine, const float* frames, uint16_t* labels, cbx_layer_stats* stats,
                           uint64_t* macs) {
     enqueue_host(engine, frames);
+    if (labels) read_labels(engine, labels);
+    read_stats(engine, stats, macs);
+}
+
+// 8-bit host frames (S x H x W x C interleaved, the PPM raster): H2D of the
+// bytes into a staging buffer, decoded on the device into the frame slot
+// (px / 255, read_ppm io.cpp:60-104), then the frame as enqueue_host.
+void Engine::enqueue_host_u8(int engine, const uint8_t* frames) {
+    if (!frames) throw Error(CBX_E_ARG, "frames is null");
+    if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
+    CBX_CUDA(cudaSetDevice(device_));
+    const size_t per = (size_t)net_.inputChannels * net_.inputHeight * net_.inputWidth;
+    if (!u8_stage_) u8_stage_ = dmalloc<uint8_t>(per * S_);
+    float* slot = engine == CBX_ENGINE_CBINFER ? slots_[parity_] : slots_[2];
+    CBX_CUDA(cudaMemcpyAsync(u8_stage_, frames, per * S_, cudaMemcpyHostToDevice, stream_));
+    launch_decode_u8(u8_stage_, S_, net_.inputChannels, net_.inputHeight, net_.inputWidth, slot, stream_);
+    std::vector<const float*> cur(S_);
+    for (int s = 0; s < S_; ++s) cur[s] = slot + per * s;
+    forward_device(engine, cur.data());
+    if (engine == CBX_ENGINE_CBINFER) parity_ ^= 1;
+}
+
+void Engine::forward_host_u8(int engine, const uint8_t* frames, uint16_t* labels, cbx_layer_stats* stats,
+                             uint64_t* macs) {
+    enqueue_host_u8(engine, frames);
     if (labels) read_labels(engine, labels);
     read_stats(engine, stats, macs);
 }
@@ -745,9 +802,20 @@ bool Engine::enqueue(int engine, const float* const* frames_dev, unsigned long l
 // frame j. Slot j % 3 was last read by frame j-2 (as its detection
 // reference), hence the copy of frame j waits for frame j-2 only.
 int64_t Engine::submit(int engine, const float* frames, uint16_t* labels) {
+    return submit_any(engine, frames, nullptr, labels);
+}
+
+int64_t Engine::submit_u8(int engine, const uint8_t* frames, uint16_t* labels) {
+    return submit_any(engine, nullptr, frames, labels);
+}
+
+// f32: planar fp32 host frames copied into the ring slot; u8: 8-bit
+// interleaved host frames copied into a byte ring and decoded into the slot
+// on the context stream (4x fewer PCIe bytes).
+int64_t Engine::submit_any(int engine, const float* frames, const uint8_t* frames_u8, uint16_t* labels) {
     if (engine != CBX_ENGINE_CBINFER)
         throw Error(CBX_E_ARG, "cbx_submit runs the change-based engine (use cbx_forward for the dense comparator)");
-    if (!frames || !labels) throw Error(CBX_E_ARG, "null frames or labels");
+    if ((!frames && !frames_u8) || !labels) throw Error(CBX_E_ARG, "null frames or labels");
     CBX_CUDA(cudaSetDevice(device_));
     const int nl = (int)layers_.size();
     const size_t per = (size_t)net_.inputChannels * net_.inputHeight * net_.inputWidth;
@@ -763,9 +831,18 @@ int64_t Engine::submit(int engine, const float* frames, uint16_t* labels) {
     const int64_t j = submitted_;
     const int q = (int)(j % kRing);
     if (j >= 2) CBX_CUDA(cudaStreamWaitEvent(copy_st_, done_[(j - 2) % kRing], 0));
-    CBX_CUDA(cudaMemcpyAsync(ring_[q], frames, per * S_ * sizeof(float), cudaMemcpyHostToDevice, copy_st_));
+    if (frames_u8) {
+        if (!ring_u8_[q]) ring_u8_[q] = dmalloc<uint8_t>(per * S_);
+        CBX_CUDA(cudaMemcpyAsync(ring_u8_[q], frames_u8, per * S_, cudaMemcpyHostToDevice, copy_st_));
+    } else {
+        CBX_CUDA(cudaMemcpyAsync(ring_[q], frames, per * S_ * sizeof(float), cudaMemcpyHostToDevice, copy_st_));
+    }
     CBX_CUDA(cudaEventRecord(copied_[q], copy_st_));
     CBX_CUDA(cudaStreamWaitEvent(stream_, copied_[q], 0));
+    // ring_[q] was last read by frame j-2 (as its detection reference): the
+    // context stream has finished it before this decode runs
+    if (frames_u8)
+        launch_decode_u8(ring_u8_[q], S_, net_.inputChannels, net_.inputHeight, net_.inputWidth, ring_[q], stream_);
     std::vector<const float*> cur(S_);
     for (int s = 0; s < S_; ++s) cur[s] = ring_[q] + per * s;
     ring_full_[q] = enqueue(engine, cur.data(), h_ring_stats_ + (size_t)q * stats_words());
@@ -930,6 +1007,18 @@ void Engine::get_activation(int engine, int layer, int s, float* out) {
     sync();
 }
 
+// Input tensor of `layer` (planar CHW) after the last frame: prevInput of a
+// CBCONV (cbconv.hpp:71). Layer 0 reads the frame the engine last consumed.
+void Engine::get_input(int engine, int layer, int s, float* out) {
+    if (layer < 0 || layer >= (int)layers_.size() || s < 0 || s >= S_) throw Error(CBX_E_BOUNDS, "layer/stream out of range");
+    if (layer > 0) return get_activation(engine, layer - 1, s, out);
+    if (engine != CBX_ENGINE_CBINFER) throw Error(CBX_E_ARG, "the dense engine keeps no frame history");
+    if (!has_history_) throw Error(CBX_E_SPEC, "no frame has been evaluated since the last reset");
+    const size_t n = (size_t)net_.inputChannels * net_.inputHeight * net_.inputWidth;
+    CBX_CUDA(cudaMemcpyAsync(out, last_cb_frames_[s], n * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+    sync();
+}
+
 void Engine::get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64_t* n, int* first) {
     if (cb < 0 || cb >= (int)cb_layers_.size() || s < 0 || s >= S_) throw Error(CBX_E_BOUNDS, "trace index out of range");
     const int k = cb_layers_[cb];
@@ -975,6 +1064,16 @@ void Engine::get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64
 namespace cbx {
 
 void Engine::mark(const char* name, int layer) {
+    if (tmarks_) {  // graph capture with CBX_OPT_STEP_TIMES: an event-record node
+        if (tmarks_used_ >= tmarks_->size()) throw Error(CBX_E_ARG, "too many step-time marks");
+        ProfMark& pm = (*tmarks_)[tmarks_used_++];
+        pm.name = name;
+        pm.layer = layer;
+        // an event-record node (a plain cudaEventRecord under capture only
+        // becomes a graph edge and is never timestamped)
+        CBX_CUDA(cudaEventRecordWithFlags(pm.ev, stream_, cudaEventRecordExternal));
+        return;
+    }
     if (!prof_) return;
     cudaEvent_t e;
     CBX_CUDA(cudaEventCreate(&e));
@@ -1123,7 +1222,44 @@ void Engine::worst_case_counts(int64_t* worst) {
     for (void* q : tmp) cudaFree(q);
 }
 
+// StepTimes (cbconv.hpp:44-52) of the last frame launched as a graph, per
+// layer: [nl][5] = detect, extract, generate, multiply, update (ns). Mapping
+// of the fused B200 kernels onto the reference's five steps: detect = the
+// frame detection kernel (first CBCONV; a later CBCONV's detection is fused
+// into its producer's compare-before-write), extract = dilation + index
+// compaction (one kernel), multiply = the gathered convolution, which also
+// generates the patches (producer warps) and updates the output (epilogue
+// scatter), so generate and update are 0. Every stream of the engine shares
+// the same kernels, hence the same times.
+void Engine::read_step_times(int64_t* out) {
+    const int nl = (int)layers_.size();
+    std::memset(out, 0, sizeof(int64_t) * 5 * nl);
+    if (!last_tm_ || last_tm_->size() < 2) return;
+    sync();
+    const auto& v = *last_tm_;
+    for (size_t i = 1; i < v.size(); ++i) {
+        float ms = 0;
+        CBX_CUDA(cudaEventElapsedTime(&ms, v[i - 1].ev, v[i].ev));
+        const int64_t ns = (int64_t)((double)ms * 1e6);
+        const std::string& n = v[i].name;
+        const int k = v[i].layer;
+        if (k < 0 || k >= nl) continue;
+        int slot = -1;
+        if (n == "detect") slot = 0;
+        else if (n == "dilate_compact" || n == "compact" || n == "dilate") slot = 1;
+        else if (n.rfind("conv", 0) == 0) slot = 3;
+        if (slot >= 0) out[5 * k + slot] += ns;
+    }
+}
+
 void Engine::set_option(int option, int value) {
+    if (option == CBX_OPT_STEP_TIMES) {
+        step_times_ = value != 0;
+        cb_->dirty = true;
+        if (base_) base_->dirty = true;
+        last_tm_ = nullptr;
+        return;
+    }
     if (option == CBX_OPT_TC_PAIR) {
         if (value < -1 || value > 1) throw Error(CBX_E_ARG, "CBX_OPT_TC_PAIR takes -1, 0 or 1");
         // rebuild every tcgen05 layer with the requested CTA grouping; the

@@ -51,6 +51,10 @@ public:
     void forward_host(int engine, const float* frames, uint16_t* labels, cbx_layer_stats* stats,
                       uint64_t* macs);
     void enqueue_host(int engine, const float* frames);  // forward_host without the read-back
+    // 8-bit interleaved host frames (PPM raster), decoded on the device
+    void forward_host_u8(int engine, const uint8_t* frames, uint16_t* labels, cbx_layer_stats* stats, uint64_t* macs);
+    void enqueue_host_u8(int engine, const uint8_t* frames);
+    int64_t submit_u8(int engine, const uint8_t* frames, uint16_t* labels);
     int num_streams() const { return S_; }
     void forward_device(int engine, const float* const* frames_dev);
     // pipelined host-frame path (cbx_submit / cbx_wait)
@@ -65,6 +69,9 @@ public:
     void worst_case_counts(int64_t* worst);
 
     void profile(int engine, const float* const* frames_dev, std::vector<cbx_kernel_time>& out);
+    void read_step_times(int64_t* out);  // [nl][5] of the last graph launch (CBX_OPT_STEP_TIMES)
+    bool has_history() const { return has_history_; }
+    void get_input(int engine, int layer, int s, float* out);
     void set_option(int option, int value);
 
     cudaStream_t stream() const { return stream_; }
@@ -88,12 +95,19 @@ private:
     int final_tensor() const;
     bool fuse_tail_ = true;
 
+public:
     struct ProfMark {
         std::string name;
         int layer;
         cudaEvent_t ev;
     };
+
+private:
     std::vector<ProfMark>* prof_ = nullptr;
+    std::vector<ProfMark>* tmarks_ = nullptr;        // capture in progress with step times
+    size_t tmarks_used_ = 0;
+    const std::vector<ProfMark>* last_tm_ = nullptr;  // marks of the last launched graph
+    bool step_times_ = false;
 
     int device_, S_, precision_;
     cbx_net_desc net_{};
@@ -132,6 +146,9 @@ private:
     // submit/wait ring: staging slots, copy stream, per-slot events and counters
     static constexpr int kRing = 3;
     float* ring_[kRing] = {nullptr, nullptr, nullptr};
+    uint8_t* ring_u8_[kRing] = {nullptr, nullptr, nullptr};  // 8-bit submissions
+    uint8_t* u8_stage_ = nullptr;                             // 8-bit synchronous forwards
+    int64_t submit_any(int engine, const float* frames, const uint8_t* frames_u8, uint16_t* labels);
     cudaStream_t copy_st_ = nullptr;
     cudaEvent_t copied_[kRing] = {nullptr, nullptr, nullptr}, done_[kRing] = {nullptr, nullptr, nullptr};
     unsigned long long* h_ring_stats_ = nullptr;  // pinned, [kRing][nl][S][2]

@@ -120,6 +120,17 @@ void launch_chw_to_hwc(const float* in, TensorView t, int s, cudaStream_t st);
 // planar frames (device pointer table) -> channels-last tensor, all streams
 void launch_ingest(const float* const* frames, TensorView t, int S, cudaStream_t st);
 
+// 8-bit interleaved camera frames -> planar fp32 px / 255 (read_ppm, io.cpp:60-104)
+void launch_decode_u8(const uint8_t* in, int S, int C, int H, int W, float* out, cudaStream_t st);
+
+// ---- matrix-form reference ops (op-level API only; k_ops.cu) ----
+void launch_gen_x(const float* in, int C, int H, int W, int kh, int kw, int sh, int sw, int ph, int pw,
+                  const int32_t* idx, int64_t n, float* X, cudaStream_t st);
+void launch_gemm_exact(const float* K, const float* bias, int rows, int cols, const float* X, int64_t n, float* Y,
+                       cudaStream_t st);
+void launch_scatter(float* out, int C, int64_t HW, const float* Y, const int32_t* idx, int64_t n, int relu,
+                    cudaStream_t st);
+
 // ---- synthetic frames ----
 struct SpriteRect {
     int y0, x0, y1, x1;

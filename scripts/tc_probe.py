@@ -23,6 +23,7 @@ ap.add_argument("--streams", type=int, default=4)
 ap.add_argument("--recipe", default="2.2")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--only", default="", help="engine filter: cbinfer or baseline")
+ap.add_argument("--precision", default="f16", choices=["f16", "tf32"])
 ap.add_argument("--stages", default="", help="comma list of CBX_TC_STAGES values to sweep")
 ap.add_argument("--nofuse", action="store_true", help="run the per-pixel head unfused (no tail in the L3 epilogue)")
 ap.add_argument("--nsplit", default="", help="comma list of CBX_TC_NSPLIT values (1 even split, 0 256+rest)")
@@ -32,7 +33,7 @@ S, F, H, W = args.streams, 6, 1080, 1920
 specd = bench.paper_spec_dict(H, W)
 spec = cbx.network_spec_from_json(json.dumps(specd))
 wts = cbx.generate_weights(spec, None, 1)
-net = cbx.Network(spec, wts, streams=S, precision="tf32", fuse_tail=not args.nofuse)
+net = cbx.Network(spec, wts, streams=S, precision=args.precision, fuse_tail=not args.nofuse, lanes=1)
 clip = torch.empty((F, S, 3, H, W), dtype=torch.float32, device="cuda")
 ns = argparse.Namespace(recipe=args.recipe, height=H, width=W)
 for s in range(S):

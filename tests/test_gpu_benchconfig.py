@@ -64,12 +64,12 @@ def test_bench_configuration_vs_reference(gpu):
                 t.start()
             for t in ts:
                 t.join()
+        if want is None:  # warm(): the reference's full frame 0 keeps no trace
+            continue
         for s in range(S):
             fa_gpu, fa_ref = net.final_activation(s), rnets[s].final_activation()
             err = float(np.abs(fa_gpu.astype(np.float64) - fa_ref).max())
             assert err <= 1e-3, (f, s, err)
-            if want is None:
-                continue
             lab = got[s].labels
             dis = int(np.count_nonzero(lab != want[s]["labels"]))
             assert dis <= max(1, 1e-3 * lab.size), (f, s, dis)

@@ -227,18 +227,17 @@ def test_f16_overflow_reported(gpu, orc):
     outputs may still hold results computed from inf) fail when their stats
     are read, after which the next frame is evaluated in full and succeeds
     (tf32 operands take every frame). Weights are scaled so that pool-2
-    peaks near 2e4 on frame A; frame B multiplies a patch of A by 4."""
+    peaks near 3e4 on frame A; frame B is A times 6."""
     h, w = 32, 48
     spec = paper_spec(h, w, (0.0, 0.0, 0.0))
     wts = orc.generate_weights(spec, 1)
     A = orc.synth_frame(dict(channels=3, height=h, width=w, sprites=[(6, 2, 0.9)], noise=0.0, seed=1), 0)
     probe = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="tf32")
     probe.forward_frame(A)
-    c = 2.0e4 / float(np.abs(probe.layer_output(3)).max())
+    c = 3.0e4 / float(np.abs(probe.layer_output(3)).max())
     big = {k: ((K * c).astype(np.float32), (b * c).astype(np.float32)) if k == 0 else (K, b)
            for k, (K, b) in wts.items()}
-    B = A.copy()
-    B[:, 8:24, 12:36] *= 4.0
+    B = (A * 6.0).astype(np.float32)
     tf = gpu.Network(to_pkg_spec(gpu, spec), big, precision="tf32")
     tf.forward_frame(A)
     assert np.abs(tf.layer_output(3)).max() < 6.0e4
@@ -404,3 +403,82 @@ def test_lanes_equivalent(gpu, orc):
         w1 = nets[0].worst_case_counts()
         for n in nets[1:]:
             assert np.array_equal(n.worst_case_counts(), w1)
+
+
+def test_step_times(gpu, orc):
+    """CBX_OPT_STEP_TIMES: per-layer StepTimes from event nodes inside the
+    frame graph (cbconv.hpp:44-52): first CBCONV has a detection interval,
+    every CBCONV an extract (dilate + compact) and a multiply interval (the
+    fused gather-conv-scatter); generate / update are fused (0); non-CB layers
+    have none; results are unchanged by the timing nodes; off -> zeros."""
+    spec = paper_spec(48, 64)
+    w = orc.generate_weights(spec, 1)
+    cfg = dict(channels=3, height=48, width=64, sprites=[(10, 2, 0.9)], noise=0.01, seed=3)
+    timed = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32", streams=2)
+    plain = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32", streams=2)
+    timed.set_step_times(True)
+    cb = timed.spec.cb_layers()
+    for f in range(3):
+        fr = np.stack([orc.synth_frame(dict(cfg, seed=3 + s), f) for s in range(2)])
+        a, b = timed.forward(fr), plain.forward(fr)
+        for s in range(2):
+            assert np.array_equal(a[s].labels, b[s].labels)
+        t = timed.step_times()
+        assert t.shape == (2, len(spec["layers"]), 5)
+        for k in range(len(spec["layers"])):
+            if k not in cb:
+                assert not t[:, k].any(), k
+        for k in cb:
+            assert (t[:, k, 3] > 0).all(), (f, k)                # multiply
+            assert not t[:, k, 2].any() and not t[:, k, 4].any()  # generate / update fused
+            if f > 0:
+                assert (t[:, k, 1] > 0).all(), (f, k)            # extract
+        assert (t[:, cb[0], 0] > 0).all() == (f > 0)             # detection only on steady frames
+        assert not t[:, cb[1:], 0].any()
+        assert not plain.step_times().any()
+    assert timed.has_history()
+    x = timed.layer_input(0, 1)
+    assert np.array_equal(x.view(np.uint32), fr[1].view(np.uint32))
+    assert np.array_equal(timed.layer_input(2, 0).view(np.uint32), timed.layer_output(1, 0).view(np.uint32))
+    timed.reset_state()
+    assert not timed.has_history()
+
+
+@pytest.mark.parametrize("precision", ["exact", "f16"])
+def test_u8_ingest_equals_decoded_frames(gpu, orc, precision):
+    """8-bit camera frames (the PPM raster, io.cpp:60-104) through
+    cbx_forward_u8 / cbx_submit_u8 give bitwise the labels, stats, traces and
+    activations of cbx_forward on the planar px / 255.0f frames read_ppm would
+    produce (numpy float32 division is the same IEEE-rounded division)."""
+    spec = paper_spec(48, 64)
+    w = orc.generate_weights(spec, 1)
+    S = 2
+    rng = np.random.default_rng(5)
+    clips = []
+    for s in range(S):
+        cfg = dict(channels=3, height=48, width=64, sprites=[(10, 2 + s, 0.9)], noise=0.01, seed=3 + s)
+        clips.append([np.clip(np.rint(orc.synth_frame(cfg, f).transpose(1, 2, 0) * 255.0), 0, 255).astype(np.uint8)
+                      for f in range(5)])
+    u8 = [np.ascontiguousarray(np.stack([clips[s][f] for s in range(S)])) for f in range(5)]
+    dec = [np.ascontiguousarray((x.astype(np.float32) / np.float32(255.0)).transpose(0, 3, 1, 2)) for x in u8]
+    a = gpu.Network(to_pkg_spec(gpu, spec), w, streams=S, precision=precision)
+    b = gpu.Network(to_pkg_spec(gpu, spec), w, streams=S, precision=precision)
+    p = gpu.Network(to_pkg_spec(gpu, spec), w, streams=S, precision=precision)
+    labs = [np.zeros((S,) + tuple(p.label_hw), np.uint16) for _ in range(5)]
+    tickets = [p.submit_u8(u8[f], labs[f]) for f in range(3)]
+    waited = {t: p.wait(t) for t in tickets}
+    for f in range(3, 5):
+        tickets.append(p.submit_u8(u8[f], labs[f]))
+        waited[tickets[-1]] = p.wait(tickets[-1])
+    for f in range(5):
+        ra, rb = a.forward_u8(u8[f]), b.forward(dec[f])
+        for s in range(S):
+            assert np.array_equal(ra[s].labels, rb[s].labels), (f, s)
+            assert np.array_equal(labs[f][s], rb[s].labels), (f, s)
+            assert [x["changedOutputPixels"] for x in ra[s].stats] == [x["changedOutputPixels"] for x in rb[s].stats]
+            assert [x["changedOutputPixels"] for x in waited[tickets[f]][0][s]] == \
+                [x["changedOutputPixels"] for x in rb[s].stats]
+            assert np.array_equal(a.layer_input(0, s).view(np.uint32), dec[f][s].view(np.uint32))
+            assert np.array_equal(a.final_activation(s).view(np.uint32), b.final_activation(s).view(np.uint32))
+            assert np.array_equal(a.trace(0, s)[1], b.trace(0, s)[1])
+    _ = rng
