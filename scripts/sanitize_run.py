@@ -1,0 +1,45 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck): the paper net at 96x128 through every kernel family -- detect,
+dilate+compact, the exact planar layer-1 conv, the tcgen05 convs (tf32, f16,
+single CTA and CTA pairs, split accumulator, fused tail, persistent grid
+capped so CTAs walk several tiles), pooling, argmax, u8 ingest, the op-level
+API -- a few frames each. Test infrastructure (the oracle is not used).
+
+  compute-sanitizer --tool memcheck python scripts/sanitize_run.py
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1704_04313_b200 as cbx  # noqa: E402
+
+H, W = 96, 128
+spec = json.load(open(os.path.join(ROOT, "paper_1704_04313_b200", "netspecs", "paper_like.json")))
+spec["inputHeight"], spec["inputWidth"] = H, W
+for l, t in zip([l for l in spec["layers"] if l["kind"] == "CBCONV"], (0.04, 0.05, 0.05)):
+    l["threshold"] = t
+sp = cbx.network_spec_from_json(json.dumps(spec))
+w = cbx.generate_weights(sp, None, 1)
+frames = [np.stack([cbx.synth_frame(dict(channels=3, height=H, width=W, sprites=[(14, 3, 0.9)], noise=0.01,
+                                         seed=3 + s), f) for s in range(2)]) for f in range(4)]
+for prec, pair, maxctas in [("f16", -1, None), ("f16", 1, None), ("tf32", 0, "2"), ("tf32", 1, "2"), ("exact", -1, None)]:
+    if maxctas:
+        os.environ["CBX_TC_MAXCTAS"] = maxctas
+    else:
+        os.environ.pop("CBX_TC_MAXCTAS", None)
+    net = cbx.Network(sp, w, streams=2, precision=prec)
+    net.set_tc_pair(pair)
+    net.set_step_times(True)
+    for f in range(4):
+        net.forward(frames[f])
+        net.forward(frames[f], "baseline")
+    u8 = np.ascontiguousarray(np.clip(np.rint(frames[0] * 255), 0, 255).astype(np.uint8).transpose(0, 2, 3, 1))
+    net.forward_u8(u8)
+    net.step_times()
+    net.close()
+    print("ok", prec, pair, maxctas, flush=True)
+print("sanitize workload done")

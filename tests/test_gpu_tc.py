@@ -122,14 +122,15 @@ def check_tc_layer(gpu, orc, cin, h, w, layer, pair):
 
 
 @pytest.mark.parametrize("magnitude", ["unit", "subnormal"])
-@pytest.mark.parametrize("maxctas", [None, "2"])
+@pytest.mark.parametrize("maxctas,pair", [(None, -1), ("2", -1), (None, 1), ("4", 1)])
 @pytest.mark.parametrize("cin,h,w,layer", F16_CASES)
-def test_f16_layer_vs_exact(gpu, orc, monkeypatch, cin, h, w, layer, maxctas, magnitude):
+def test_f16_layer_vs_exact(gpu, orc, monkeypatch, cin, h, w, layer, maxctas, pair, magnitude):
     """kind::f16 per-layer bound: a MAXPOOL-fed layer with > 128 outputs under
     precision "f16" (the headline operand format of the paper's layer 3),
     against the exact oracle on the same pooled input; 'subnormal' scales the
     first layer so the pooled activations are ~1e-5 (fp16 subnormal range);
-    maxctas=2 makes every CTA walk several tiles."""
+    maxctas caps the persistent grid so every CTA walks several tiles; pair=1
+    runs CTA pairs (cta_group::2, M = 256, each SM holding half the filters)."""
     if maxctas:
         monkeypatch.setenv("CBX_TC_MAXCTAS", maxctas)
     spec = pooled_layer(cin, h, w, layer)
@@ -139,6 +140,7 @@ def test_f16_layer_vs_exact(gpu, orc, monkeypatch, cin, h, w, layer, maxctas, ma
         wts[0] = ((K0 * 4e-5).astype(np.float32), (b0 * 4e-5).astype(np.float32))
     onet = orc.load_network(spec, wts)
     net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="f16")
+    net.set_tc_pair(pair)
     assert net.layer_operands(2) == "f16"
     cfg = dict(channels=3, height=h, width=w, sprites=[(5, 2, 0.9)], noise=0.02, seed=5)
     if magnitude == "subnormal":
