@@ -248,12 +248,14 @@ def run_reference_arm(args):
 
 
 # --------------------------------------------------------------------------- GPU arm
-def algorithmic_work(kernel, layer, st, S, dims, spec):
+def algorithmic_work(kernel, layer, st, S, dims, spec, u8=False):
     """Algorithmic bytes or flops of one launch, from the
     frame's counters. Returns (amount, 'hbm'|'tensor'|'fp32')."""
     inC, inH, inW = dims[layer][0] if layer >= 0 and layer < len(dims) else (0, 0, 0)
     if kernel == "detect":  # read both frames, write the change mask as bits
         c, h, w = dims[0][0]
+        if u8:  # 8-bit frames: both read as bytes, the RGBX copy written for the i8 layer 1
+            return S * (2 * c * h * w + 4 * h * w + h * w // 8), "hbm"
         return S * (2 * c * h * w * 4 + h * w // 8), "hbm"
     if kernel == "dilate":  # mask bits in, mask bits out
         (_, h, w), (_, ho, wo) = dims[layer]
@@ -395,17 +397,28 @@ def run_gpu_arm(args):
         cbx.decode_u8_device(clip_u8.data_ptr(), F * S, 3, args.height, args.width, clip.data_ptr(),
                              torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
-    ptrs = lambda i: [clip[pingpong(i, F), s].data_ptr() for s in range(S)]
+    ptrs_f32 = lambda i: [clip[pingpong(i, F), s].data_ptr() for s in range(S)]
+    # value: the camera frames as they arrive -- 8-bit RGB resident in HBM,
+    # run natively (byte detection + kind::i8 layer 1); fp32 planar frames
+    # (the decoded clip, layer 1 on the exact fp32 path) are timed beside it
+    U8 = clip_u8 is not None
+    ptrs8 = (lambda i: [clip_u8[pingpong(i, F), s].data_ptr() for s in range(S)]) if U8 else None
+
+    def fwd(n, i, engine="cbinfer", u8=U8):
+        if u8:
+            n.forward_device_u8(ptrs8(i), engine)
+        else:
+            n.forward_device(ptrs_f32(i), engine)
 
     barrier = shard.barrier
 
-    def timed(engine, i0, K):
+    def timed(engine, i0, K, u8=U8):
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(i0, i0 + K):
-            net.forward_device(ptrs(i), engine)
+            fwd(net, i, engine, u8)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -415,9 +428,9 @@ def run_gpu_arm(args):
     clocks.start()
     time.sleep(0.3)  # nvidia-smi needs a moment before its first sample
     # warm-up: frame 0 is the full evaluation, then W steady steps
-    net.forward_device(ptrs(0))
+    fwd(net, 0, "cbinfer")
     for i in range(1, args.warmup + 1):
-        net.forward_device(ptrs(i))
+        fwd(net, i, "cbinfer")
     net.sync()
     i0 = args.warmup + 1
     K = args.steps
@@ -429,7 +442,7 @@ def run_gpu_arm(args):
     j = i0 + K
     while time.perf_counter() < t_end:
         for _ in range(10):
-            net.forward_device(ptrs(j))
+            fwd(net, j, "cbinfer")
             j += 1
         net.sync()
     clk = clocks.stop()
@@ -442,7 +455,7 @@ def run_gpu_arm(args):
     st_all = []
     net.reset_state()
     for i in range(0, i0 + K):
-        net.forward_device(ptrs(i))
+        fwd(net, i, "cbinfer")
         if i >= i0:
             stats, _ = net.read_stats()
             st_all.append(stats)
@@ -454,7 +467,7 @@ def run_gpu_arm(args):
     # per-kernel device times (graph-free pass with CUDA events on the launch stream)
     prof_runs = []
     for i in range(i0 + K, i0 + K + 3):
-        prof_runs.append((net.profile(ptrs(i)), net.read_stats()[0]))
+        prof_runs.append((net.profile(ptrs8(i) if U8 else ptrs_f32(i), u8=U8), net.read_stats()[0]))
     per = {}
     for prof, st in prof_runs:
         for kt in prof:
@@ -463,14 +476,17 @@ def run_gpu_arm(args):
     tot = {k: sum(m for m, _ in v) / len(v) for k, v in per.items()}
     step_ms = sum(tot.values())
     (kname, klayer), kms = max(tot.items(), key=lambda kv: kv[1])
-    amounts = [algorithmic_work(kname, klayer, st, S, dims, specd)[0] for _, st in per[(kname, klayer)]]
-    bound = algorithmic_work(kname, klayer, per[(kname, klayer)][0][1], S, dims, specd)[1]
+    amounts = [algorithmic_work(kname, klayer, st, S, dims, specd, U8)[0] for _, st in per[(kname, klayer)]]
+    bound = algorithmic_work(kname, klayer, per[(kname, klayer)][0][1], S, dims, specd, U8)[1]
     amount = float(np.mean(amounts))
     peaks, peak_src = load_peaks()
     # tensor peak per operand format: f16 = the measured dense bf16 rate, tf32 = half of it
     def tensor_peak(layer):
         bf16 = peaks.get("bf16_tflops", 1590.0)
-        return bf16 if net.layer_operands(layer) == "f16" else bf16 / 2.0
+        op = net.layer_operands(layer)
+        if op == "i8" and not U8:
+            return 75.0  # fp32 frames: layer 1 on the exact fp32 path
+        return {"f16": bf16, "i8": 2.0 * bf16}.get(op, bf16 / 2.0)
     if bound == "hbm":
         achieved = amount / (kms / 1000.0) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
@@ -506,8 +522,8 @@ def run_gpu_arm(args):
     # algorithmic counts, against the serial kernel sum (graph-free pass) and the graph-timed step
     t_roof = 0.0
     for (n, l), v in per.items():
-        amt = float(np.mean([algorithmic_work(n, l, st_, S, dims, specd)[0] for _, st_ in v]))
-        bnd = algorithmic_work(n, l, v[0][1], S, dims, specd)[1]
+        amt = float(np.mean([algorithmic_work(n, l, st_, S, dims, specd, U8)[0] for _, st_ in v]))
+        bnd = algorithmic_work(n, l, v[0][1], S, dims, specd, U8)[1]
         pk = (peaks["hbm_gbs"] * 1e9 if bnd == "hbm" else
               tensor_peak(l) * 1e12 if bnd == "tensor" else 75.0e12)
         t_roof += amt / pk * 1000.0
@@ -520,7 +536,7 @@ def run_gpu_arm(args):
 
     # dense per-frame B200 conv (same kernels, every pixel, Baseline engine)
     Kd = max(3, K // 4)
-    net.forward_device(ptrs(0), "baseline")
+    fwd(net, 0, "baseline")
     ms_d = timed("baseline", 1, Kd)
     dense_fps = shard.aggregate_rate(ws, S * Kd, ms_d)
     log(f"[gpu] dense: {ms_d / Kd:.3f} ms/step, {dense_fps:.1f} frames/s")
@@ -531,15 +547,19 @@ def run_gpu_arm(args):
     if S > 1:
         net1 = cbx.Network(spec, weights, device=local, streams=1, precision=args.precision)
         st1 = torch.cuda.ExternalStream(net1.stream_handle(), device=torch.device("cuda", local))
-        p1 = lambda i: [clip[pingpong(i, F), 0].data_ptr()]
+        def f1(i):
+            if U8:
+                net1.forward_device_u8([clip_u8[pingpong(i, F), 0].data_ptr()])
+            else:
+                net1.forward_device([clip[pingpong(i, F), 0].data_ptr()])
         for i in range(0, args.warmup + 1):
-            net1.forward_device(p1(i))
+            f1(i)
         net1.sync()
         per = []
         for i in range(args.warmup + 1, args.warmup + 1 + K):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st1)
-            net1.forward_device(p1(i))
+            f1(i)
             e1.record(st1)
             e1.synchronize()
             per.append(e0.elapsed_time(e1))
@@ -559,18 +579,22 @@ def run_gpu_arm(args):
                 for f in range(F):
                     cbx.synth_frame_device(cfg, f, c2[f, s].data_ptr(), torch.cuda.current_stream().cuda_stream)
             torch.cuda.synchronize()
-            p2 = lambda i: [c2[pingpong(i, F), s].data_ptr() for s in range(S)]
+            if U8:
+                c2u = (c2 * 255.0).round().clamp(0, 255).to(torch.uint8).permute(0, 1, 3, 4, 2).contiguous()
+                p2 = lambda i: net.forward_device_u8([c2u[pingpong(i, F), s].data_ptr() for s in range(S)])
+            else:
+                p2 = lambda i: net.forward_device([c2[pingpong(i, F), s].data_ptr() for s in range(S)])
             net.reset_state()
             for i in range(0, 3):
-                net.forward_device(p2(i))
-            net.forward_device(p2(3))
+                p2(i)
+            p2(3)
             stt, _ = net.read_stats()
             barrier()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for i in range(4, 4 + K):
-                net.forward_device(p2(i))
+                p2(i)
             e1.record(stream)
             torch.cuda.synchronize()
             m2 = shard.max_over_ranks(e0.elapsed_time(e1), device=red_dev)
@@ -645,20 +669,31 @@ def run_gpu_arm(args):
         log(f"[gpu] e2e: {e2e['value']:.1f} frames/s; fp32 upload {f32['value']:.1f}, "
             f"synchronous cbx_forward {sync:.1f}")
 
+    # the same step on fp32 planar frames resident in HBM (the decoded clip:
+    # 4x the detection bytes, layer 1 on the exact fp32 path)
+    f32_value = None
+    if U8:
+        net.reset_state()
+        for i in range(0, args.warmup + 1):
+            fwd(net, i, "cbinfer", False)
+        net.sync()
+        f32_value = shard.aggregate_rate(ws, S * K, timed("cbinfer", i0, K, False))
+        log(f"[gpu] fp32 resident frames: {f32_value:.1f} frames/s")
+
     # tf32-only operands (layer 3 on kind::tf32 too), same workload and timing
     tf32_value = None
     if args.precision == "f16":
         net_t = cbx.Network(spec, weights, device=local, streams=S, precision="tf32", lanes=args.lanes)
         st_t = torch.cuda.ExternalStream(net_t.stream_handle(), device=torch.device("cuda", local))
         for i in range(0, args.warmup + 1):
-            net_t.forward_device(ptrs(i))
+            fwd(net_t, i)
         net_t.sync()
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st_t)
         for i in range(i0, i0 + K):
-            net_t.forward_device(ptrs(i))
+            fwd(net_t, i)
         e1.record(st_t)
         torch.cuda.synchronize()
         barrier()
@@ -699,20 +734,26 @@ def run_gpu_arm(args):
             "data": "synthetic",
             "config": {"workload": f"paper_like {args.width}x{args.height} x {S} streams/GPU, sprite recipe "
                                    f"{args.recipe}% (resident clips, inputs > L2: {S}x2 frames of "
-                                   f"{3 * args.height * args.width * 4 / 1e6:.1f} MB per step)",
+                                   f"{3 * args.height * args.width * (1 if U8 else 4) / 1e6:.1f} MB per step)",
                        "streams_per_gpu": S, "taus": list(BASE_TAUS),
                        "precision": {"mode": args.precision, "operands": operands,
                                      "tf32_only_value": tf32_value,
                                      "note": "f16 = fp16 operands (10 mantissa bits, RN) for the MAXPOOL-fed "
-                                             "304-channel layer 3, kind::tf32 for layer 2, exact fp32 for layer 1 "
-                                             "and the 1x1 head; tf32_only_value = the same step with layer 3 on "
-                                             "kind::tf32 too"},
+                                             "304-channel layer 3, kind::tf32 for layer 2, layer 1 kind::i8 on the "
+                                             "8-bit frame bytes (filters as three 8-bit digits of a 22-bit "
+                                             "fixed-point weight, exact integer accumulation; exact fp32 for fp32 "
+                                             "frames), exact fp32 for the 1x1 head; tf32_only_value = the same step "
+                                             "with layer 3 on kind::tf32 too"},
                        "cudnn_dense_fps": cudnn,
-                       "input": ("8-bit RGB camera frames (synthetic clip quantized to the PPM raster), decoded "
-                                 "px/255 as read_ppm; value: decoded frames resident in HBM; e2e: 8-bit host frames"
-                                 if args.input == "u8" else "fp32 planar synthetic frames"),
+                       "input": ("8-bit RGB camera frames (synthetic clip quantized to the PPM raster; the reference "
+                                 "arm reads them as read_ppm does, px/255). value: the 8-bit frames resident in HBM "
+                                 "(cbx_forward_device_u8: detection on the bytes, layer 1 tcgen05 kind::i8); "
+                                 "f32_frames_value: the same step on the decoded fp32 planar frames resident in HBM; "
+                                 "e2e: 8-bit host frames"
+                                 if U8 else "fp32 planar synthetic frames"),
+                       "f32_frames_value": f32_value,
                        "l2_flush": "inputs larger than L2: every step reads S x 2 fresh frames "
-                                   f"({S * 2 * 3 * args.height * args.width * 4 / 1e6:.0f} MB > 126 MB L2)",
+                                   f"({S * 2 * 3 * args.height * args.width * (1 if U8 else 4) / 1e6:.0f} MB > 126 MB L2)",
                        "l1_input_changed": frac_in, "layer_output_changed": frac_out,
                        "dense_fps": dense_fps, "speedup_vs_dense": value / dense_fps, "parallelism": f"streams x{ws}",
                        "single_stream_latency_ms": lat_ms, "lanes": net.num_lanes()},

@@ -131,7 +131,8 @@ CBX_API int cbx_num_lanes(const cbx_ctx* ctx);
 /* Operand format of layer `layer`'s convolution: 0 = fp32 on CUDA cores
  * (exact reference order), 1 = tcgen05 kind::tf32, 2 = tcgen05 kind::f16
  * (fp16 operands rounded to nearest, fp32 accumulation; CBX_PREC_F16 only),
- * -1 = not a conv. */
+ * 3 = tcgen05 kind::i8 on 8-bit camera frames (layer 0 only, see
+ * CBX_OPT_U8_NATIVE; fp32 frames still take the exact fp32 path), -1 = not a conv. */
 CBX_API int cbx_layer_operands(const cbx_ctx* ctx, int layer);
 CBX_API void cbx_destroy(cbx_ctx* ctx);
 
@@ -156,7 +157,18 @@ CBX_API int cbx_get_thresholds(const cbx_ctx* ctx, float* taus, int n);
  * boundaries of the frame graph so cbx_read_step_times can return the
  * reference's per-layer StepTimes (cbconv.hpp:44-52) -- the collectTimings
  * switch of CBConvState (cbconv.hpp:70). Off: no timing nodes in the graph. */
-typedef enum { CBX_OPT_FUSE_TAIL = 0, CBX_OPT_TC_PAIR = 1, CBX_OPT_STEP_TIMES = 2 } cbx_option;
+/* CBX_OPT_U8_NATIVE (default 1): 8-bit camera frames (cbx_forward_u8,
+ * cbx_submit_u8, cbx_forward_device_u8) run natively in the tensor-core
+ * precisions when the frame is 3-channel with a width divisible by 16 and the
+ * first layer is a conv: change detection on the bytes (decoded exactly as
+ * read_ppm, so layer-1 masks and index lists stay bit-exact) fused with an
+ * RGBX copy of the frame, and layer 1 as a tcgen05 kind::i8 conv over those
+ * bytes (filters as three 8-bit digits of a 22-bit fixed-point weight, exact
+ * integer accumulation: layer-1 outputs within ~2^-22 relative of the fp32
+ * reference instead of bitwise; cbx_layer_operands(ctx, 0) reports 3). 0 decodes
+ * 8-bit frames into fp32 planar frames first (the fp32 path: layer 1 bitwise).
+ * Changing it makes the next frame a full evaluation. */
+typedef enum { CBX_OPT_FUSE_TAIL = 0, CBX_OPT_TC_PAIR = 1, CBX_OPT_STEP_TIMES = 2, CBX_OPT_U8_NATIVE = 3 } cbx_option;
 CBX_API int cbx_set_option(cbx_ctx* ctx, int option, int value);
 
 /* Drops all change-based state of every stream: the next frame is a full
@@ -205,6 +217,10 @@ CBX_API int cbx_wait(cbx_ctx* ctx, int64_t ticket, cbx_layer_stats* stats, uint6
 CBX_API int cbx_forward_u8(cbx_ctx* ctx, int engine, const uint8_t* frames, uint16_t* labels,
                            cbx_layer_stats* stats, uint64_t* macs);
 CBX_API int cbx_submit_u8(cbx_ctx* ctx, int engine, const uint8_t* frames, uint16_t* labels, int64_t* ticket);
+/* 8-bit frames already on the device: frames_dev[s] = stream s's H x W x C
+ * interleaved bytes (16-byte aligned). Same contract as cbx_forward_device
+ * (asynchronous; each frame is the next call's detection reference). */
+CBX_API int cbx_forward_device_u8(cbx_ctx* ctx, int engine, const uint8_t* const* frames_dev);
 /* cbench analyze-prop (tools/cbench.cpp:242-302) for the last change-based
  * frame (not a full one): for every CBCONV k >= 1 (0-based among CBCONVs), the
  * worst-case updated count of layer k -- the updated set of CBCONV k-1 pushed
@@ -233,6 +249,8 @@ typedef struct {
 } cbx_kernel_time;
 CBX_API int cbx_profile_forward(cbx_ctx* ctx, int engine, const float* const* frames_dev,
                                 cbx_kernel_time* out, int cap, int* n);
+CBX_API int cbx_profile_forward_u8(cbx_ctx* ctx, int engine, const uint8_t* const* frames_dev,
+                                   cbx_kernel_time* out, int cap, int* n);
 
 /* Trace access for parity checks (CBConvTrace / ForwardTrace):
  *   cbx_get_activation: output of layer `layer` for stream s, planar CHW, host

@@ -476,6 +476,16 @@ class Network:
         arr = (C.c_void_p * self.streams)(*frame_ptrs)
         self._chk(lib.cbx_forward_device(self._h, ENGINES[engine], arr))
 
+    def forward_device_u8(self, frame_ptrs: Sequence[int], engine: str = "cbinfer") -> None:
+        """cbx_forward_device_u8: 8-bit interleaved frames (H x W x C bytes) on the device."""
+        arr = (C.c_void_p * self.streams)(*frame_ptrs)
+        self._chk(lib.cbx_forward_device_u8(self._h, ENGINES[engine], arr))
+
+    def set_u8_native(self, on: bool) -> None:
+        """CBX_OPT_U8_NATIVE: 8-bit frames run natively (byte detection + kind::i8
+        layer 1) or are decoded to fp32 planar frames first."""
+        self._chk(lib.cbx_set_option(self._h, 3, int(bool(on))))
+
     def sync(self):
         self._chk(lib.cbx_sync(self._h))
 
@@ -494,22 +504,25 @@ class Network:
                       gemmMacs=stats[s * self.nl + k].gemmMacs) for k in range(self.nl)]
                 for s in range(S)], list(macs)
 
-    def profile(self, frame_ptrs: Sequence[int], engine: str = "cbinfer") -> List[dict]:
+    def profile(self, frame_ptrs: Sequence[int], engine: str = "cbinfer", u8: bool = False) -> List[dict]:
         """One forward outside the CUDA graph with CUDA events around every
-        kernel (cbx_profile_forward). Returns [{name, layer, ms}]."""
+        kernel (cbx_profile_forward / cbx_profile_forward_u8 for 8-bit device
+        frames). Returns [{name, layer, ms}]."""
         arr = (C.c_void_p * self.streams)(*frame_ptrs)
         cap = 256
         out = (KernelTime * cap)()
         n = C.c_int()
-        self._chk(lib.cbx_profile_forward(self._h, ENGINES[engine], arr, out, cap, C.byref(n)))
+        fn = lib.cbx_profile_forward_u8 if u8 else lib.cbx_profile_forward
+        self._chk(fn(self._h, ENGINES[engine], arr, out, cap, C.byref(n)))
         return [dict(name=out[i].name.decode(), layer=out[i].layer, ms=out[i].ms) for i in range(min(n.value, cap))]
 
     def num_lanes(self) -> int:
         return lib.cbx_num_lanes(self._h)
 
     def layer_operands(self, layer: int) -> str:
-        """Operand format of a conv layer: 'fp32' (exact, CUDA cores), 'tf32' or 'f16' (tcgen05)."""
-        return {0: "fp32", 1: "tf32", 2: "f16"}.get(lib.cbx_layer_operands(self._h, layer), "none")
+        """Operand format of a conv layer: 'fp32' (exact, CUDA cores), 'tf32' or 'f16' (tcgen05),
+        'i8' (tcgen05 kind::i8 on 8-bit camera frames; fp32 frames take the exact path)."""
+        return {0: "fp32", 1: "tf32", 2: "f16", 3: "i8"}.get(lib.cbx_layer_operands(self._h, layer), "none")
 
     def stream_handle(self) -> int:
         return lib.cbx_stream(self._h) or 0

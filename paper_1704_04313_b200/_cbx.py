@@ -101,7 +101,7 @@ lib.cbx_submit_u8.argtypes = [VP, C.c_int, C.POINTER(C.c_uint8), C.POINTER(C.c_u
 lib.cbx_get_input.argtypes = [VP, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]
 lib.cbx_read_step_times.argtypes = [VP, C.POINTER(C.c_int64)]
 for _name in ("cbx_load_layer", "cbx_set_thresholds", "cbx_get_thresholds", "cbx_set_option", "cbx_reset", "cbx_forward",
-              "cbx_forward_device", "cbx_sync", "cbx_read_labels", "cbx_read_stats", "cbx_labels_device",
+              "cbx_forward_device", "cbx_forward_device_u8", "cbx_profile_forward_u8", "cbx_sync", "cbx_read_labels", "cbx_read_stats", "cbx_labels_device",
               "cbx_get_activation", "cbx_get_trace", "cbx_destroy"):
     getattr(lib, _name).argtypes = None
 lib.cbx_destroy.argtypes = [VP]
@@ -122,7 +122,8 @@ EXPORTS = [
     "cbx_op_extract_workspace", "cbx_op_extract", "cbx_op_maxpool", "cbx_op_argmax",
     "cbx_op_cbconv_update", "cbx_random_filters", "cbx_synth_frame", "cbx_synth_frame_device",
     "cbx_get_input", "cbx_has_history", "cbx_read_step_times", "cbx_op_relu", "cbx_op_gen_x", "cbx_op_gemm",
-    "cbx_op_scatter", "cbx_forward_u8", "cbx_submit_u8", "cbx_op_decode_u8",
+    "cbx_op_scatter", "cbx_forward_u8", "cbx_submit_u8", "cbx_op_decode_u8", "cbx_forward_device_u8",
+    "cbx_profile_forward_u8",
 ]
 
 

@@ -168,6 +168,10 @@ CBX_API int cbx_forward_device(cbx_ctx* ctx, int engine, const float* const* fra
     return guarded(ctx, [&] { E(ctx).forward_device(engine, frames_dev); });
 }
 
+CBX_API int cbx_forward_device_u8(cbx_ctx* ctx, int engine, const uint8_t* const* frames_dev) {
+    return guarded(ctx, [&] { E(ctx).forward_device_u8(engine, frames_dev); });
+}
+
 CBX_API int cbx_submit(cbx_ctx* ctx, int engine, const float* frames, uint16_t* labels, int64_t* ticket) {
     return guarded(ctx, [&] {
         if (!ticket) throw cbx::Error(CBX_E_ARG, "null ticket");
@@ -235,8 +239,21 @@ CBX_API int cbx_get_trace(cbx_ctx* ctx, int cb, int s, uint8_t* detected, int32_
 CBX_API int cbx_profile_forward(cbx_ctx* ctx, int engine, const float* const* frames_dev, cbx_kernel_time* out,
                                 int cap, int* n) {
     return guarded(ctx, [&] {
+        if (!frames_dev) throw cbx::Error(CBX_E_ARG, "frames is null");
         std::vector<cbx_kernel_time> v;
-        E(ctx).profile(engine, frames_dev, v);
+        E(ctx).profile(engine, frames_dev, nullptr, v);
+        const int m = std::min<int>((int)v.size(), cap);
+        if (out && m > 0) std::memcpy(out, v.data(), sizeof(cbx_kernel_time) * m);
+        if (n) *n = (int)v.size();
+    });
+}
+
+CBX_API int cbx_profile_forward_u8(cbx_ctx* ctx, int engine, const uint8_t* const* frames_dev, cbx_kernel_time* out,
+                                   int cap, int* n) {
+    return guarded(ctx, [&] {
+        if (!frames_dev) throw cbx::Error(CBX_E_ARG, "frames is null");
+        std::vector<cbx_kernel_time> v;
+        E(ctx).profile(engine, nullptr, frames_dev, v);
         const int m = std::min<int>((int)v.size(), cap);
         if (out && m > 0) std::memcpy(out, v.data(), sizeof(cbx_kernel_time) * m);
         if (n) *n = (int)v.size();

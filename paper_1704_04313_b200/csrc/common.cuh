@@ -22,6 +22,17 @@ struct TensorView {
     int64_t ss;      // floats per stream
 };
 
+// The layer-1 input of the 8-bit camera path: RGBX pixels (4 bytes, channel
+// 3 zero) in rows of Wp pixels with a zero halo of hh rows / hw pixels (hw a
+// multiple of 4 so every row's interior starts 16-byte aligned); streams ss
+// pixels apart. The tcgen05 conv reads it as a TensorView with Cp = 1
+// (one 4-byte unit per pixel).
+struct Rgbx8View {
+    uint32_t* d;
+    int64_t ss;
+    int Wp, hh, hw;
+};
+
 // Byte mask on a pixel grid: [S][stride], pixel p = y*W + x.
 struct MaskView {
     uint8_t* d;
@@ -40,6 +51,26 @@ struct BitMask {
 };
 
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// Division by a runtime-constant divisor as a multiply-high and a shift, for
+// numerators below 2^31 (the per-pixel index arithmetic of the hot kernels:
+// a 64-bit division is a ~100-instruction subroutine call per pixel):
+// m = ceil(2^(31 + l) / d), l = ceil(log2 d), q = umulhi(n, m) >> (l - 1).
+struct FastDiv {
+    uint32_t d = 1, m = 0, sh = 0;
+    static FastDiv make(uint32_t d) {
+        FastDiv f;
+        f.d = d;
+        if (d > 1) {
+            int l = 0;
+            while ((1ull << l) < d) ++l;
+            f.m = (uint32_t)(((1ull << (31 + l)) + d - 1) / d);
+            f.sh = (uint32_t)(l - 1);
+        }
+        return f;
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const { return d == 1 ? n : (__umulhi(n, m) >> sh); }
+};
 
 __device__ __forceinline__ bool bit_test(const BitMask& m, int s, int y, int x) {
     return (m.d[(int64_t)s * m.stride + (int64_t)y * m.wpr + (x >> 5)] >> (x & 31)) & 1u;

@@ -108,6 +108,12 @@ void Context::forward_device(int engine, const float* const* frames_dev) {
     join();
 }
 
+void Context::forward_device_u8(int engine, const uint8_t* const* frames_dev) {
+    if (!frames_dev) throw Error(CBX_E_ARG, "frames is null");
+    for (size_t l = 0; l < lanes_.size(); ++l) lanes_[l]->forward_device_u8(engine, frames_dev + off_[l]);
+    join();
+}
+
 int64_t Context::submit(int engine, const float* frames, uint16_t* labels) {
     if (!frames || !labels) throw Error(CBX_E_ARG, "null frames or labels");
     Sub& sub = subs_[submitted_ % 3];
@@ -186,12 +192,13 @@ void Context::worst_case_counts(int64_t* worst) {
 
 // Lanes one after the other (no overlap), the times of the same kernel in
 // different lanes summed: per-kernel device time over all streams.
-void Context::profile(int engine, const float* const* frames_dev, std::vector<cbx_kernel_time>& out) {
+void Context::profile(int engine, const float* const* frames_dev, const uint8_t* const* frames_u8,
+                      std::vector<cbx_kernel_time>& out) {
     out.clear();
     std::map<std::pair<std::string, int>, size_t> pos;
     for (size_t l = 0; l < lanes_.size(); ++l) {
         std::vector<cbx_kernel_time> v;
-        lanes_[l]->profile(engine, frames_dev + off_[l], v);
+        lanes_[l]->profile(engine, frames_dev ? frames_dev + off_[l] : nullptr, frames_u8 ? frames_u8 + off_[l] : nullptr, v);
         for (const auto& t : v) {
             const auto key = std::make_pair(std::string(t.name), t.layer);
             auto it = pos.find(key);

@@ -40,6 +40,7 @@ public:
     // frames
     void forward_host(int engine, const float* frames, uint16_t* labels, cbx_layer_stats* stats, uint64_t* macs);
     void forward_device(int engine, const float* const* frames_dev);
+    void forward_device_u8(int engine, const uint8_t* const* frames_dev);
     void forward_host_u8(int engine, const uint8_t* frames, uint16_t* labels, cbx_layer_stats* stats, uint64_t* macs);
     int64_t submit_u8(int engine, const uint8_t* frames, uint16_t* labels);
     int64_t submit(int engine, const float* frames, uint16_t* labels);
@@ -56,7 +57,8 @@ public:
     bool has_history() const { return lanes_[0]->has_history(); }
     void read_step_times(int64_t* nanos);  // [S][nl][5]
     void worst_case_counts(int64_t* worst);
-    void profile(int engine, const float* const* frames_dev, std::vector<cbx_kernel_time>& out);
+    void profile(int engine, const float* const* frames_dev, const uint8_t* const* frames_u8,
+                 std::vector<cbx_kernel_time>& out);
     int last_launch_count() const;
 
 private:

@@ -39,185 +39,40 @@
 
 #include "conv_tc.hpp"
 #include "engine.hpp"
+#include "tc_ptx.cuh"
 
 namespace cbx {
 
 namespace {
 
-constexpr int kTileM = 128;
+using namespace tc;
+
 constexpr int kKBlock = 32;        // tf32 elements per K-block (128 B per row)
 constexpr int kChunksPerKB = 8;    // 16-byte chunks per K-block row
-constexpr int kABytes = kTileM * 128;
+constexpr int kABytes = tc::kTileM * 128;
 constexpr int kEpiThreads = 128, kProdThreads = 128;
 constexpr int kThreads = kEpiThreads + kProdThreads + 32;
 constexpr int kMaxSmem = 232448;   // 227 KB opt-in
 
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-// 16-byte async copy; src_bytes == 0 zero-fills the destination.
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-
-// K-major, SWIZZLE_128B shared-memory matrix descriptor: rows of 128 B, 8-row
-// core groups 1024 B apart (SBO), version 1 (Blackwell).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
-    return (uint64_t)((addr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
-}
-// Instruction descriptor: D=f32, A=B=tf32, both K-major, M=128, N.
-__host__ __device__ constexpr uint32_t idesc_tf32(int N, int M = kTileM) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-// Instruction descriptor: D=f32, A=B=f16, both K-major, M=128, N (kind::f16).
-__host__ __device__ constexpr uint32_t idesc_f16(int N, int M = kTileM) {
-    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-// ---- CTA-pair (cta_group::2) helpers
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t cluster_id_x() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t nclusters_x() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-    return r;
-}
-// shared::cluster address of the same smem object in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-// arrive (when the issued MMAs complete) on the barrier at this smem offset in both CTAs of the pair
-__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
-    asm volatile(
-        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
-            smem_u32(bar))
-        : "memory");
-}
-
-// position in the ring of NS shared-memory stages (stage, barrier parity),
-// advanced without a division per K-block
-struct Ring {
-    uint32_t st = 0, ph = 0;
-    __device__ __forceinline__ void next(int n) {
-        if (++st == (uint32_t)n) {
-            st = 0;
-            ph ^= 1u;
-        }
+// Output pixel of list entry g: stream s, linear pixel p = y*Wo + x.
+struct TcArgs;
+template <class A>
+__device__ __forceinline__ void pixel_of(const A& a, int64_t g, int64_t HoWo, int& s, int& p, int& y, int& x) {
+    if (a.fast) {
+        const uint32_t gg = (uint32_t)g;
+        const uint32_t ss = a.fd_howo.div(gg);
+        const uint32_t pp = gg - ss * (uint32_t)HoWo;
+        const uint32_t yy = a.fd_wo.div(pp);
+        s = (int)ss;
+        p = (int)pp;
+        y = (int)yy;
+        x = (int)(pp - yy * (uint32_t)a.Wo);
+    } else {
+        s = (int)(g / HoWo);
+        p = (int)(g - (int64_t)s * HoWo);
+        y = p / a.Wo;
+        x = p - y * a.Wo;
     }
-};
-
-// one lane of a converged warp (elect.sync): the warp runs the MMA issue loop
-// together, so descriptors and loop state stay warp-uniform (uniform
-// registers) and only the tcgen05 instructions themselves are predicated
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred;
-    asm volatile(
-        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
-    return pred != 0;
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // Remaining per-pixel ops of a fused tail (after the first 1x1 CONV, whose
@@ -287,6 +142,15 @@ struct TcArgs {
     // next tile's MMAs wait only for the shared columns to be drained
     int ovl, ovl_s, ovl_b0, ovl_b1;
     int tap4x7;  // row-lane gather specialised for Cp = 4, 7x7 (NKB = 7)
+    // kind::i8 (8-bit camera path, layer 1): A = RGBX bytes of the frame, one
+    // 4-byte chunk per tap (32 taps per K-block); B = the filters as three
+    // signed base-256 digits per weight, digit q of channel j in accumulator
+    // column q * i8_opad + j; y_j = bias_j + qsc[j] * (A2 * 65536 + A1 * 256 + A0)
+    int i8_opad;
+    const float* qsc;
+    // pixel index -> (stream, y, x) by multiply-shift when S*Ho*Wo < 2^31
+    int fast;
+    FastDiv fd_howo, fd_wo;
     int f16;     // operands are fp16 (kind::f16): the input is an fp16 shadow tensor
                  // addressed in 4-byte units (in_Cp = fp16 channels / 2)
     int relu;
@@ -382,7 +246,7 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, float (&v)[32], int c
 // arrive on a CTA-local mbarrier), and the leader's commits are multicast to
 // both CTAs' empty / accumulator-full barriers. Each CTA's TMEM holds the
 // accumulator rows of its own 128 pixels, so the epilogue is unchanged.
-template <bool ROWLANE, int TC, bool PAIR>
+template <bool ROWLANE, int TC, bool PAIR, bool I8 = false>
 __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // align by offsetting the shared array itself (not via an integer round
@@ -392,11 +256,14 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
     const uint32_t b_bytes = (uint32_t)a.Brows * 128u;
     uint8_t* sA = smem;                                  // NS x 16 KB
     uint8_t* sB = sA + (size_t)NS * kABytes;             // NS x b_bytes
-    int* sTab = reinterpret_cast<int*>(sB + (size_t)NS * b_bytes);   // NKB*8 chunk offsets (floats)
-    float* sBias = reinterpret_cast<float*>(sTab + a.NKB * kChunksPerKB);
+    // NKB*8 chunk offsets (floats); I8: NKB*32 tap offsets (4-byte units)
+    const int tab_n = I8 ? 0 : a.NKB * kChunksPerKB;
+    int* sTab = reinterpret_cast<int*>(sB + (size_t)NS * b_bytes);
+    float* sBias = reinterpret_cast<float*>(sTab + tab_n);
     float* sTailW = sBias + ((a.O + 3) & ~3);  // first tail conv's filters, transposed [O][TC] (16B aligned)
+    float* sQs = sTailW + a.tail_w_floats;
     uint64_t* bars = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(sTailW + a.tail_w_floats) + 7) & ~uintptr_t(7));
+        (reinterpret_cast<uintptr_t>(sQs + (I8 ? a.O : 0)) + 7) & ~uintptr_t(7));
     uint64_t* full = bars;
     uint64_t* empty = full + NS;
     uint64_t* pfull = empty + NS;  // PAIR, leader only: the peer's stage is full
@@ -412,14 +279,16 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
     const uint32_t crank = PAIR ? cluster_rank() : 0u;
     const int64_t tile_first = PAIR ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
     const int64_t tile_step = PAIR ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
-    constexpr int kRowsPerTile = PAIR ? 2 * kTileM : kTileM;
-    const int64_t row_off = (int64_t)crank * kTileM;  // this CTA's rows within a tile
+    constexpr int kRowsPerTile = PAIR ? 2 * tc::kTileM : tc::kTileM;
+    const int64_t row_off = (int64_t)crank * tc::kTileM;  // this CTA's rows within a tile
     const float* Bw = a.Bw + (size_t)crank * a.NKB * a.Brows * kKBlock;
 
     // ---- setup
-    for (int j = tid; j < a.NKB * kChunksPerKB; j += kThreads) {
+    for (int j = tid; j < tab_n; j += kThreads) {
         int off = -1;
-        if (j < nchunks) {
+        if (I8) {
+            // (unused: the register-staged gather computes its offsets)
+        } else if (j < nchunks) {
             const int tap = j / C4, c4 = j - tap * C4;
             const int kj = tap / a.kw, ki = tap - kj * a.kw;
             off = (kj * a.in_Wp + ki) * a.in_Cp + c4 * 4;
@@ -427,6 +296,8 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         sTab[j] = off;
     }
     for (int o = tid; o < a.O; o += kThreads) sBias[o] = a.bias[o];
+    if (I8)
+        for (int o = tid; o < a.O; o += kThreads) sQs[o] = a.qsc[o];
     if (TC > 0) {
         const int c1 = a.tail.cout[0];
         for (int i = tid; i < a.O * TC; i += kThreads) {
@@ -469,7 +340,59 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
 
     if (warp >= 4 && warp < 8) {
         // ================= producers =================
-        if constexpr (ROWLANE) {
+        if constexpr (I8) {
+            // RGBX bytes, register-staged: thread = tile row. Kernel row kr's
+            // kw taps are kw neighbouring 4-byte pixels (consecutive lanes
+            // read consecutive pixels: coalesced LDG.32), padded with zero
+            // words to kwp = 8 taps (two 16-byte granules, the padding tap has
+            // zero weights), written with STS.128 into the SW128 K-major row
+            // (granule g of row r at g ^ (r & 7): conflict-free), then made
+            // visible to the tensor core (fence.proxy.async) before the
+            // stage's barrier arrive. 4 kernel rows per 128-byte K-block.
+            const int r = tid - kEpiThreads;
+            const uint32_t swz = (uint32_t)(r & 7);
+            Ring rg;
+            auto row_index = [&](int64_t t) -> int64_t {
+                const int64_t n = t * kRowsPerTile + r;
+                return (t < ntiles && n < total) ? (a.idx ? (int64_t)__ldg(a.idx + n) : n) : -1;
+            };
+            int64_t gnext = row_index(tile_first);
+            for (int64_t tile = tile_first; tile < ntiles; tile += tile_step) {
+                const int64_t g = gnext;
+                gnext = row_index(tile + tile_step);
+                const bool valid = g >= 0;
+                const uint32_t* base = reinterpret_cast<const uint32_t*>(a.in);
+                if (valid) {
+                    int s, p, y, x;
+                    pixel_of(a, g, HoWo, s, p, y, x);
+                    base += (int64_t)s * a.in_ss + ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw));
+                }
+                for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
+                    const uint32_t st = rg.st, ph = rg.ph;
+                    uint32_t v[4][8];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int kr = 4 * kb + q;
+#pragma unroll
+                        for (int ki = 0; ki < 8; ++ki)
+                            v[q][ki] = (valid && kr < a.kh && ki < a.kw) ? __ldg(base + (int64_t)kr * a.in_Wp + ki) : 0u;
+                    }
+                    mbar_wait(&empty[st], ph ^ 1u);
+                    if (r == 0) {
+                        mbar_arrive_expect_tx(&full[st], b_bytes);
+                        bulk_g2s(sB + (size_t)st * b_bytes, Bw + (size_t)kb * a.Brows * kKBlock, b_bytes, &full[st]);
+                    }
+                    uint4* row = reinterpret_cast<uint4*>(sA + (size_t)st * kABytes + r * 128);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        row[(2 * q) ^ swz] = make_uint4(v[q][0], v[q][1], v[q][2], v[q][3]);
+                        row[(2 * q + 1) ^ swz] = make_uint4(v[q][4], v[q][5], v[q][6], v[q][7]);
+                    }
+                    fence_proxy_async();
+                    mbar_arrive(&full[st]);
+                }
+            }
+        } else if constexpr (ROWLANE) {
             const int r = tid - kEpiThreads;
             const uint32_t swz = (uint32_t)(r & 7);
             Ring rg;
@@ -486,9 +409,8 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 const bool valid = g >= 0;
                 const float* base = a.in;
                 if (valid) {
-                    const int s = (int)(g / HoWo);
-                    const int p = (int)(g - (int64_t)s * HoWo);
-                    const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
+                    int s, p, y, x;
+                    pixel_of(a, g, HoWo, s, p, y, x);
                     base = a.in + (int64_t)s * a.in_ss +
                            ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
                 }
@@ -553,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         const int pt = tid - kEpiThreads;
         const int j = pt & 7, rsub = pt >> 3;
         const uint32_t swz_off = (uint32_t)((j ^ (rsub & 7)) << 4);
-        constexpr int kRowsPerThread = kTileM / 16;
+        constexpr int kRowsPerThread = tc::kTileM / 16;
         Ring rg;
         // indices of the next tile's rows are loaded during this tile's K-loop
         int32_t gnext[kRowsPerThread];
@@ -578,9 +500,8 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 if (gcur[i] >= 0) {
                     vmask |= 1u << i;
                     const int64_t g = gcur[i];
-                    const int s = (int)(g / HoWo);
-                    const int p = (int)(g - (int64_t)s * HoWo);
-                    const int y = p / a.Wo, x = p - (p / a.Wo) * a.Wo;
+                    int s, p, y, x;
+                    pixel_of(a, g, HoWo, s, p, y, x);
                     base[i] = a.in + (int64_t)s * a.in_ss +
                               ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
                 }
@@ -623,8 +544,8 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             }
         } else {
             // ================= MMA issuer (whole warp, one elected lane issues) =================
-            const int M = PAIR ? 2 * kTileM : kTileM;
-            const uint32_t id0 = a.f16 ? idesc_f16(a.N0, M) : idesc_tf32(a.N0, M);
+            const int M = PAIR ? 2 * tc::kTileM : tc::kTileM;
+            const uint32_t id0 = I8 ? idesc_i8(a.N0, M) : a.f16 ? idesc_f16(a.N0, M) : idesc_tf32(a.N0, M);
             const uint32_t id1 = a.f16 ? idesc_f16(a.N1 > 0 ? a.N1 : 16, M) : idesc_tf32(a.N1 > 0 ? a.N1 : 16, M);
             const bool two = a.N1 > 0;
             const bool f16 = a.f16 != 0;
@@ -658,7 +579,9 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
 #pragma unroll
                         for (int k = 0; k < kKBlock / 8; ++k) {
                             const uint32_t accum = (kb | k) ? 1u : 0u;
-                            if constexpr (PAIR) {
+                            if constexpr (I8) {
+                                mma_i8(d, ad + 2 * k, bd + 2 * k, id0, accum);
+                            } else if constexpr (PAIR) {
                                 if (f16) {
                                     mma_f16_pair(d, ad + 2 * k, bd + 2 * k, id0, accum);
                                     if (two) mma_f16_pair(d1, ad + 2 * k, bd + b1_d + 2 * k, id1, accum);
@@ -689,19 +612,26 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         // ================= epilogue: thread = TMEM lane = tile row =================
         const int r = tid;
         uint32_t acc_it = 0;
+        // the index of this row in the NEXT tile is loaded while this tile is
+        // processed: a tile's epilogue never starts with a dependent global
+        // load (short K-loops, e.g. the 2-K-block layer 1, are otherwise
+        // bound by that latency)
+        auto row_index = [&](int64_t t) -> int64_t {
+            const int64_t n = t * kRowsPerTile + row_off + r;
+            return (t < ntiles && n < total) ? (a.idx ? (int64_t)__ldg(a.idx + n) : n) : -1;
+        };
+        int64_t gnext = row_index(tile_first);
         for (int64_t tile = tile_first; tile < ntiles; tile += tile_step, ++acc_it) {
             const uint32_t as = acc_it % a.acc_stages, aph = (acc_it / a.acc_stages) & 1u;
-            const int64_t n = tile * kRowsPerTile + row_off + r;
-            const bool valid = n < total;
-            // index (and output address) resolved before waiting for the accumulator
-            const int64_t g = valid ? (a.idx ? (int64_t)__ldg(a.idx + n) : n) : 0;
+            const int64_t gi = gnext;
+            gnext = row_index(tile + tile_step);
+            const bool valid = gi >= 0;
+            // output address resolved before waiting for the accumulator
+            const int64_t g = valid ? gi : 0;
             int s = 0, p = 0, y = 0, x = 0;
             float* dst = nullptr;
             if (valid) {
-                s = (int)(g / HoWo);
-                p = (int)(g - (int64_t)s * HoWo);
-                y = p / a.Wo;
-                x = p - y * a.Wo;
+                pixel_of(a, g, HoWo, s, p, y, x);
                 dst = a.out + (int64_t)s * a.out_ss + ((int64_t)(y + a.out_hh) * a.out_Wp + (x + a.out_hw)) * a.out_Cp;
                 // the values this pixel overwrites (compare-before-write) are
                 // pulled into L2 while the MMAs run
@@ -713,6 +643,56 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             tc_fence_after();
             bool changed = false;
             const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16);
+            if constexpr (I8) {
+                // digits -> fp32: the s32 digit sums are exact, recombined in
+                // fp64 (exact below 2^53) and rounded once with the bias
+                const uint32_t tb = trow + as * a.acc_cols;
+                const int Op = a.i8_opad;
+                for (int j0 = 0; j0 < a.O; j0 += 4) {
+                    int32_t q0[4], q1[4], q2[4];
+                    tmem_ld4(tb + j0, q0);
+                    tmem_ld4(tb + Op + j0, q1);
+                    tmem_ld4(tb + 2 * Op + j0, q2);
+                    tmem_wait_ld();
+                    if (j0 + 4 >= a.O) {
+                        tc_fence_before();
+                        mbar_arrive(&tempty[as]);
+                    }
+                    if (!valid) continue;
+                    float v[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        // |digit sums| < 2^23: exact in fp32; the scaled
+                        // recombination rounds at most three times (~2^-23 rel.)
+                        const int j = min(j0 + e, a.O - 1);
+                        const float tot = fmaf((float)q2[e], 65536.0f, fmaf((float)q1[e], 256.0f, (float)q0[e]));
+                        const float t = fmaf(tot, sQs[j], sBias[j]);
+                        v[e] = a.relu ? ref_relu(t) : t;
+                    }
+                    if (j0 + 4 <= a.O) {  // channel stride is a multiple of 4: aligned 16-byte store
+                        float4* q4 = reinterpret_cast<float4*>(dst + j0);
+                        if (a.chg.d) {
+                            const float4 old = *q4;
+                            changed |= ref_changed(v[0], old.x, a.tau) | ref_changed(v[1], old.y, a.tau) |
+                                       ref_changed(v[2], old.z, a.tau) | ref_changed(v[3], old.w, a.tau);
+                        }
+                        *q4 = make_float4(v[0], v[1], v[2], v[3]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            if (j0 + e < a.O) {
+                                if (a.chg.d) changed |= ref_changed(v[e], dst[j0 + e], a.tau);
+                                dst[j0 + e] = v[e];
+                            }
+                        }
+                    }
+                }
+                if (a.chg.d) {
+                    if (valid && changed) bit_set(a.chg, s, y, x);
+                    if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
+                }
+                continue;
+            }
             // TMEM column of channel c0: one accumulator per stage, or (ovl)
             // the shared columns for c0 < N0 and this parity's own after
             const uint32_t col_lo = a.ovl ? (uint32_t)a.ovl_s : as * a.acc_cols;
@@ -801,6 +781,9 @@ struct TcLayer {
     bool pair = false;   // CTA pair (cta_group::2, M = 256)
     bool ovl = false;    // split accumulator (see make_tc_layer)
     bool f16 = false;    // fp16 operands (kind::f16): Cp counts 4-byte units of the fp16 shadow input
+    bool i8 = false;     // kind::i8 over RGBX camera bytes (Cp = 1 unit per pixel), digit filters
+    int Opad = 0;        // i8: output channels padded to 4 (digit column stride)
+    float* qsc = nullptr;   // i8: per-channel scale / 255
     int ovl_s = 0, ovl_b0 = 0, ovl_b1 = 0;
     int max_ctas = 0;    // persistent grid cap (0: one per SM x ctas_per_sm)
     int Brows = 0;       // filter rows per CTA
@@ -811,10 +794,17 @@ struct TcLayer {
 
 void TcLayerDeleter::operator()(TcLayer* p) const {
     if (p && p->Bw) cudaFree(p->Bw);
+    if (p && p->qsc) cudaFree(p->qsc);
     delete p;
 }
 
 bool tc_is_f16(const TcLayer& t) { return t.f16; }
+bool tc_is_i8(const TcLayer& t) { return t.i8; }
+
+bool tc_i8_supported(const cbx_geom& g) {
+    return g.inChannels >= 1 && g.inChannels <= 4 && g.outChannels >= 1 && 3 * round_up(g.outChannels, 4) <= 256 &&
+           g.kernelW <= 8 && g.kernelH <= 64;
+}
 
 bool tc_supported(const cbx_geom& g) {
     const int Npad = (int)round_up(g.outChannels, 16);
@@ -822,9 +812,9 @@ bool tc_supported(const cbx_geom& g) {
 }
 
 namespace {
-template <bool R, int T, bool P>
+template <bool R, int T, bool P, bool I = false>
 void set_smem_attr() {
-    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<R, T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CBX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<R, T, P, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
 }
 template <int T, bool P>
 void set_smem_attrs() {
@@ -833,9 +823,45 @@ void set_smem_attrs() {
 }
 }  // namespace
 
-std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats, int pair_mode, bool f16) {
+std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats, int pair_mode, bool f16,
+                                                       bool i8) {
     std::unique_ptr<TcLayer, TcLayerDeleter> t(new TcLayer);
     t->g = g;
+    if (i8) {
+        // layer 1 of the 8-bit camera path: one 4-byte RGBX chunk per tap,
+        // 32 taps per 128-byte K-block; N = three digit columns per channel
+        if (!tc_i8_supported(g)) throw Error(CBX_E_ARG, "kind::i8 conv: unsupported geometry");
+        t->i8 = true;
+        t->Cp = 1;
+        t->NKB = (g.kernelH + 3) / 4;  // 4 kernel rows (8 tap slots each) per K-block
+        t->Opad = (int)round_up(g.outChannels, 4);
+        t->Npad = (int)round_up(3 * t->Opad, 16);
+        t->N0 = t->Npad;
+        t->N1 = 0;
+        t->acc_cols = (int)round_up(t->Npad, 32);
+        t->acc_stages = 2;
+        int cols = 32;
+        while (cols < 2 * t->acc_cols) cols *= 2;
+        t->tmem_cols = cols;
+        t->Brows = t->Npad;
+        t->ctas_per_sm = 2;
+        const size_t b_bytes = (size_t)t->Brows * 128;
+        const size_t fixed = 1024 + round_up(g.outChannels, 4) * 4 + 16 +
+                             (size_t)g.outChannels * 8 + 8 * (3 * 16 + 5) + 16;
+        const size_t budget = (size_t)kMaxSmem / 2 - 1024;
+        int ns = 6;
+        if (const char* e = std::getenv("CBX_TC_STAGES")) ns = std::max(2, std::min(16, std::atoi(e)));
+        while (ns > 2 && fixed + (size_t)ns * (kABytes + b_bytes) > budget) --ns;
+        t->stages = ns;
+        if (const char* e = std::getenv("CBX_TC_MAXCTAS")) t->max_ctas = std::max(1, std::atoi(e));
+        t->smem = fixed + (size_t)ns * (kABytes + b_bytes);
+        set_smem_attr<true, 0, false, true>();
+        CBX_CUDA(cudaMalloc(&t->Bw, (size_t)t->NKB * b_bytes));
+        CBX_CUDA(cudaMemset(t->Bw, 0, (size_t)t->NKB * b_bytes));
+        CBX_CUDA(cudaMalloc(&t->qsc, sizeof(float) * g.outChannels));
+        CBX_CUDA(cudaMemset(t->qsc, 0, sizeof(float) * g.outChannels));
+        return t;
+    }
     // fp16 operands: 8 channels per 16-byte chunk; Cp stays in 4-byte units so
     // the gather's address arithmetic is the same for both operand types
     t->f16 = f16;
@@ -894,7 +920,7 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     const size_t b_bytes = (size_t)t->Brows * 128;
     t->tail_w_floats = (int)round_up(tail_floats, 4);
     const size_t fixed = 1024 + (size_t)t->NKB * kChunksPerKB * 4 + round_up(g.outChannels, 4) * 4 +
-                         (size_t)t->tail_w_floats * 4 + 16 + 8 * (3 * 16 + 5) + 16;
+                         (size_t)t->tail_w_floats * 4 + 16 + 8 * (3 * 16 + 5) + 16 + 8;
     const size_t budget = t->ctas_per_sm == 2 ? (size_t)kMaxSmem / 2 - 1024 : (size_t)kMaxSmem;
     // stage count: deep enough to cover the gather latency, shallow enough to
     // leave L1 for the gather's tap reuse (neighbouring output pixels share
@@ -965,6 +991,42 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
             row = t.N0 / 2 + m % (t.N1 / 2);
         }
     };
+    if (t.i8) {
+        // Each weight as a 22-bit integer multiple of its channel's scale
+        // s_j = max|w_j| / 2^22, split into three balanced base-256 digits
+        // (d0 + 256 d1 + 65536 d2, each in [-128, 127]); digit q of channel j
+        // is filter row q * Opad + j. Tap (kj, ki) has slot t = kj * 8 + ki
+        // (kernel rows padded to 8 taps, the A gather's order); byte
+        // (row, t * 4 + c) of K-block t / 32 sits at
+        // row * 128 + ((k / 16) ^ (row & 7)) * 16 + k % 16, k = (t % 32) * 4 + c.
+        std::vector<int8_t> img((size_t)t.NKB * t.Brows * 128, 0);
+        std::vector<float> qs(g.outChannels, 0.0f);
+        for (int j = 0; j < g.outChannels; ++j) {
+            double mx = 0.0;
+            for (int i = 0; i < Kref; ++i) mx = std::max(mx, (double)std::fabs(K[(size_t)j * Kref + i]));
+            const double sc = mx > 0.0 ? mx / 4194304.0 : 1.0;
+            qs[j] = (float)(sc / 255.0);
+            for (int c = 0; c < g.inChannels; ++c)
+                for (int tap = 0; tap < khw; ++tap) {
+                    long long wi = std::llround((double)K[(size_t)j * Kref + (size_t)c * khw + tap] / sc);
+                    const int slot = (tap / g.kernelW) * 8 + tap % g.kernelW;
+                    const int kb = slot / 32, k = (slot % 32) * 4 + c, jj = k / 16;
+                    for (int q = 0; q < 3; ++q) {
+                        long long r = ((wi % 256) + 256) % 256;
+                        if (r >= 128) r -= 256;
+                        wi = (wi - r) / 256;
+                        const int row = q * t.Opad + j;
+                        img[(size_t)kb * t.Brows * 128 + (size_t)row * 128 + ((jj ^ (row & 7)) * 16) + (k % 16)] =
+                            (int8_t)r;
+                    }
+                    if (wi != 0) throw Error(CBX_E_ARG, "kind::i8 filter digits overflow");
+                }
+        }
+        CBX_CUDA(cudaMemcpyAsync(t.Bw, img.data(), img.size(), cudaMemcpyHostToDevice, st));
+        CBX_CUDA(cudaMemcpyAsync(t.qsc, qs.data(), sizeof(float) * qs.size(), cudaMemcpyHostToDevice, st));
+        CBX_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
     if (t.f16) {
         // fp16 image (round to nearest even): chunk J = tap * C4 + c4 holds
         // channels 8*c4 .. 8*c4+7 of that tap; half (row, kb*64 + j*8 + e) at
@@ -1060,6 +1122,14 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     a.tmem_cols = t.tmem_cols;
     a.ovl = t.ovl;
     a.f16 = t.f16;
+    a.i8_opad = t.Opad;
+    a.qsc = t.qsc;
+    {
+        const int64_t HoWo = (int64_t)out.H * out.W;
+        a.fast = full_count < ((int64_t)1 << 31);
+        a.fd_howo = FastDiv::make((uint32_t)std::min<int64_t>(HoWo, 0x7fffffff));
+        a.fd_wo = FastDiv::make((uint32_t)out.W);
+    }
     static const bool no_tap4x7 = std::getenv("CBX_TC_NO_TAP4X7") != nullptr;  // (tuning)
     a.tap4x7 = !no_tap4x7 && in.Cp == 4 && t.g.kernelH == 7 && t.g.kernelW == 7 && t.NKB == 7;
     a.ovl_s = t.ovl_s;
@@ -1081,7 +1151,7 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     static const int rowlane_env = std::getenv("CBX_TC_ROWLANE") ? std::atoi(std::getenv("CBX_TC_ROWLANE")) : -1;
     const bool rowlane = rowlane_env >= 0 ? rowlane_env != 0 : in.Cp <= 4;  // (env: tuning)
     if (t.pair) {
-        const int64_t max_tiles = (full_count + 2 * kTileM - 1) / (2 * kTileM);
+        const int64_t max_tiles = (full_count + 2 * tc::kTileM - 1) / (2 * tc::kTileM);
         int64_t ccap = t.max_clusters;
         if (t.max_ctas > 0) ccap = std::min<int64_t>(ccap, std::max(1, t.max_ctas / 2));
         const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, ccap));
@@ -1108,9 +1178,13 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
 #undef CBX_TC_LAUNCH
         return;
     }
-    const int64_t max_tiles = (full_count + kTileM - 1) / kTileM;
+    const int64_t max_tiles = (full_count + tc::kTileM - 1) / tc::kTileM;
     const int64_t cap = t.max_ctas > 0 ? t.max_ctas : (int64_t)kNumSMs * t.ctas_per_sm;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, cap));
+    if (t.i8) {
+        conv_tc_kernel<true, 0, false, true><<<grid, kThreads, t.smem, st>>>(a);
+        return;
+    }
 #define CBX_TC_LAUNCH(R, T) conv_tc_kernel<R, T, false><<<grid, kThreads, t.smem, st>>>(a)
     if (tc == 0) {
         if (rowlane) CBX_TC_LAUNCH(true, 0); else CBX_TC_LAUNCH(false, 0);

@@ -40,9 +40,15 @@ bool tc_supported(const cbx_geom& g);
 // pair_mode: -1 = auto (single-CTA tiles), 0 = never, 1 = CTA pairs (cta_group::2).
 // f16: fp16 operands (kind::f16) read from an fp16 shadow of the input whose
 // TensorView counts channels in 4-byte units (tc_input_cp).
+// i8: layer 1 of the 8-bit camera path -- kind::i8 over the RGBX bytes of the
+// frame (TensorView with Cp = 1: one 4-byte unit per pixel), filters as three
+// signed base-256 digits of a 22-bit fixed-point weight (relative weight
+// error <= 2^-23 of the channel's largest weight, exact integer accumulation).
 std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats = 0, int pair_mode = -1,
-                                                       bool f16 = false);
+                                                       bool f16 = false, bool i8 = false);
 bool tc_is_f16(const TcLayer& t);
+bool tc_is_i8(const TcLayer& t);
+bool tc_i8_supported(const cbx_geom& g);
 // K in the reference layout [O][Cin*kh*kw], columns (c,kj,ki); host memory.
 void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st);
 void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float* bias,

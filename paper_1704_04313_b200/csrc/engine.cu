@@ -147,10 +147,11 @@ struct Engine::Plan {
     std::vector<void*> allocs;
     uint16_t* labels = nullptr;
     unsigned long long* stats = nullptr;  // [nl][S][2]
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
-    int launches[2] = {0, 0};
+    // graphs: [steady, full] x [fp32 frames, 8-bit native frames]
+    cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};
+    int launches[4] = {0, 0, 0, 0};
     // CBX_OPT_STEP_TIMES: event-record nodes at the kernel boundaries of each graph
-    std::vector<Engine::ProfMark> tm[2];
+    std::vector<Engine::ProfMark> tm[4];
     void drop_marks(int m) {
         for (auto& x : tm[m]) cudaEventDestroy(x.ev);
         tm[m].clear();
@@ -170,8 +171,7 @@ struct Engine::Plan {
     ~Plan() {
         for (auto& g : gexec)
             if (g) cudaGraphExecDestroy(g);
-        drop_marks(0);
-        drop_marks(1);
+        for (int m = 0; m < 4; ++m) drop_marks(m);
         for (void* p : allocs) cudaFree(p);
     }
     template <class T>
@@ -206,6 +206,7 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
     hK_.assign(nl, {});
     hB_.assign(nl, {});
     tc_.resize(nl);
+    mpr_.resize(nl);
     for (int k = 0; k < nl; ++k) {
         if (layers_[k].kind == CBX_CBCONV) cb_layers_.push_back(k);
         if (is_conv(layers_[k].kind)) {
@@ -229,9 +230,24 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
                                  layers_[k - 1].kind == CBX_MAXPOOL;
                 if (f16) f16_layers_.push_back(k);
                 tc_[k] = make_tc_layer(g, tail_floats, -1, f16);
+                // narrow layer on a 4-channel input (paper layer 2): groups of
+                // R adjacent output pixels per tensor-core row, fp16 operands
+                // converted while gathering. Opt-in (CBX_MPR_F16=1): on the
+                // paper's layer 2 the fp32 output scatter (52 channels per
+                // pixel) bounds it, and it measured slower than conv_tc's tf32
+                // path (R = 1/2/4: 52/63/87 vs 44 us per 8 x 1080p lane-frame)
+                const char* me = std::getenv("CBX_MPR_F16");
+                if (precision_ == CBX_PREC_F16 && !f16 && te < 0 && g.inChannels <= 4 && me && std::atoi(me) == 1) {
+                    int R = 4;
+                    if (const char* re = std::getenv("CBX_MPR_R")) R = std::atoi(re);  // (tuning)
+                    while (R > 1 && !mpr_supported(g, 1, R)) R /= 2;
+                    if (mpr_supported(g, 1, R)) mpr_[k] = make_mpr_layer(g, 1, R, 0);
+                }
             }
         }
     }
+    any_f16_ = !f16_layers_.empty();
+    for (const auto& m : mpr_) any_f16_ = any_f16_ || (m && mpr_mode(*m) == 1);
     const bool hasClassify = layers_.back().kind == CBX_CLASSIFY;
     const int fl = nl - 1;
     lh_ = hasClassify ? dims_[6 * fl + 1] : dims_[6 * fl + 4];
@@ -239,6 +255,32 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
     const float** tbl = dmalloc<const float*>(2 * (size_t)S);
     d_cur_ = tbl;
     d_prev_ = tbl + S;
+    // 8-bit camera path: layer 1 as kind::i8 over an RGBX copy of the frame
+    // (tensor-core precisions; exact mode decodes to fp32 and stays bitwise)
+    if (precision_ != CBX_PREC_EXACT && is_conv(layers_[0].kind) && rgb8_native_ok(net.inputChannels, net.inputHeight, net.inputWidth) &&
+        tc_i8_supported(layers_[0].geom)) {
+        const cbx_geom& g = layers_[0].geom;
+        tc8_ = make_tc_layer(g, 0, -1, false, true);
+        const char* me = std::getenv("CBX_MPR");
+        if (mpr_supported(g, 0, 4) && !(me && std::atoi(me) == 0))
+            mpr8_ = make_mpr_layer(g, 0, 4, (int)round_up(g.padW, 4));
+        const uint8_t** t8 = dmalloc<const uint8_t*>(2 * (size_t)S);
+        d_cur8_ = t8;
+        d_prev8_ = t8 + S;
+        TensorView v{};
+        v.C = net.inputChannels;
+        v.H = net.inputHeight;
+        v.W = net.inputWidth;
+        v.Cp = 1;
+        v.hh = g.padH;
+        v.hw = (int)round_up(g.padW, 4);
+        v.Hp = v.H + 2 * v.hh;
+        v.Wp = v.W + 2 * v.hw;
+        v.ss = round_up((int64_t)v.Hp * v.Wp, 64);
+        v.d = dmalloc<float>((size_t)(v.ss * S) + 2 * (size_t)v.Wp + 64);  // zero halo, never written (+ window slack)
+        rgbx_tv_ = v;
+        rgbx_ = Rgbx8View{reinterpret_cast<uint32_t*>(v.d), v.ss, v.Wp, v.hh, v.hw};
+    }
     const size_t frame = (size_t)net.inputChannels * net.inputHeight * net.inputWidth * S;
     for (auto& s : slots_) s = dmalloc<float>(frame);
     CBX_CUDA(cudaMallocHost(&h_stats_, sizeof(unsigned long long) * 2 * stats_words()));
@@ -261,9 +303,16 @@ Engine::~Engine() {
     for (float* p : dBias_) cudaFree(p);
     cudaFree(d_cur_);
     for (auto& s : slots_) cudaFree(s);
+    tc8_.reset();
+    mpr8_.reset();
+    mpr_.clear();
+    if (d_cur8_) cudaFree(d_cur8_);
+    if (rgbx_tv_.d) cudaFree(rgbx_tv_.d);
+    if (prev_dec_) cudaFree(prev_dec_);
+    for (auto& s : slots8_)
+        if (s) cudaFree(s);
     cudaFreeHost(h_stats_);
     if (copy_st_) cudaStreamSynchronize(copy_st_);
-    if (u8_stage_) cudaFree(u8_stage_);
     for (int q = 0; q < kRing; ++q) {
         if (ring_u8_[q]) cudaFree(ring_u8_[q]);
         if (ring_[q]) cudaFree(ring_[q]);
@@ -275,8 +324,16 @@ Engine::~Engine() {
     if (stream_) cudaStreamDestroy(stream_);
 }
 
+int Engine::list_group(int k, bool u8) const {
+    if (k == 0 && u8 && mpr8_) return mpr_group_width(*mpr8_);
+    if (mpr_[k]) return mpr_group_width(*mpr_[k]);
+    return 1;
+}
+
 int Engine::layer_operands(int layer) const {
     if (layer < 0 || layer >= (int)layers_.size() || !is_conv(layers_[layer].kind)) return -1;
+    if (layer == 0 && u8_native()) return 3;
+    if (mpr_[layer]) return 2;
     if (!tc_[layer]) return 0;
     return tc_is_f16(*tc_[layer]) ? 2 : 1;
 }
@@ -334,7 +391,9 @@ void Engine::build_plan(Plan& p, bool baseline) {
         v.Hp = h + 2 * v.hh;
         v.Wp = w + 2 * v.hw;
         v.ss = round_up((int64_t)v.Hp * v.Wp * v.Cp, 64);
-        v.d = p.alloc<float>((size_t)(v.ss * S));
+        // (slack: a multi-pixel-row gather window of the last row may run a
+        // few pixels past the last stream's right halo; zero weights there)
+        v.d = p.alloc<float>((size_t)(v.ss * S) + 64 * (size_t)v.Cp);
         p.T[t] = v;
     };
 
@@ -363,7 +422,7 @@ void Engine::build_plan(Plan& p, bool baseline) {
     }
     p.labels = p.alloc<uint16_t>((size_t)S * lh_ * lw_);
     p.stats = p.alloc<unsigned long long>(stats_words());
-    if (!f16_layers_.empty()) p.ovf = p.alloc<int>(1);
+    if (any_f16_) p.ovf = p.alloc<int>(1);
     if (baseline) return;  // full mode only: no masks, no lists
 
     // change masks (inputs of CBCONV layers) and updated masks
@@ -422,7 +481,7 @@ void Engine::build_plan(Plan& p, bool baseline) {
         if (!is_conv(l.kind)) continue;
         const int Ho = dims_[6 * k + 4], Wo = dims_[6 * k + 5];
         if (l.kind == CBX_CONV && identity_geom(l.geom) && p.upd_owner[k] >= 0 &&
-            is_conv(layers_[p.upd_owner[k]].kind)) {
+            is_conv(layers_[p.upd_owner[k]].kind) && !mpr_[p.upd_owner[k]] && !(p.upd_owner[k] == 0 && mpr8_)) {
             const int j = p.upd_owner[k];
             p.idx_src[k] = p.idx_src[j] >= 0 ? p.idx_src[j] : j;
             continue;
@@ -481,7 +540,21 @@ void Engine::record(Plan& p, bool full) {
     }
     mark("memset", -1);  // (profile pass: the scratch memsets get their own interval)
     // K1: detection on the raw frames
-    if (!full) {
+    if (rec_u8_) {
+        // 8-bit frames: detection on the bytes + RGBX copy for the i8 layer 1
+        const auto& in = p.T[0];
+        if (!full && p.chg[0].d) {
+            launch_detect_rgb8(d_cur8_, d_prev8_, S, in.H, in.W, layers_[0].threshold, 0, p.chg[0], stats_of(0, 0), 2,
+                               rgbx_, st);
+            mark("detect", 0);
+        } else if (!full && p.upd[0].d && p.upd_owner[0] == -1) {
+            launch_detect_rgb8(d_cur8_, d_prev8_, S, in.H, in.W, 0.0f, 1, p.upd[0], nullptr, 2, rgbx_, st);
+            mark("detect_bitwise", 0);
+        } else {
+            launch_detect_rgb8(d_cur8_, d_cur8_, S, in.H, in.W, 0.0f, 2, BitMask{nullptr, 0, 0, 0, 0}, nullptr, 2, rgbx_, st);
+            mark("expand", 0);
+        }
+    } else if (!full) {
         const auto& in = p.T[0];
         if (p.chg[0].d) {
             launch_detect_bits(d_cur_, d_prev_, S, in.C, in.H, in.W, layers_[0].threshold, 0, p.chg[0],
@@ -517,14 +590,15 @@ void Engine::record(Plan& p, bool full) {
                         unsigned long long* cnt = l.kind == CBX_CBCONV ? stats_of(k, 1) : nullptr;
                         const bool fused = g.strideH == 1 && g.strideW == 1 && g.padW <= 31 &&
                                            g.kernelW - 1 - g.padW <= 31 && 2 * g.padW <= g.kernelW - 1;
+                        const int R = list_group(k, rec_u8_);
                         if (identity_geom(g)) {
                             const bool own = p.U[k].d != nullptr;  // CBCONV 1x1: U_k is its own mask
                             launch_dilate_compact(src, own ? p.U[k] : src, own, S, 1, 1, 0, 0, p.idx[k], p.cnt[k], p.ws_k[k],
-                                                  cnt, 2, st, true);
+                                                  cnt, 2, st, true, R);
                             mark("compact", k);
                         } else if (fused) {
                             launch_dilate_compact(src, p.U[k], true, S, g.kernelH, g.kernelW, g.padH, g.padW, p.idx[k],
-                                                  p.cnt[k], p.ws_k[k], cnt, 2, st, true);
+                                                  p.cnt[k], p.ws_k[k], cnt, 2, st, true, R);
                             mark("dilate_compact", k);
                         } else {
                             launch_dilate_bits(src, p.U[k], S, g.kernelH, g.kernelW, g.strideH, g.strideW, g.padH, g.padW, st);
@@ -541,6 +615,22 @@ void Engine::record(Plan& p, bool full) {
                 const bool planar_in = (k == 0 && !p.ingest);
                 const bool relu = l.kind == CBX_CBCONV && l.fuseRelu;
                 const int64_t full_count = (int64_t)S * dims_[6 * k + 4] * dims_[6 * k + 5];
+                if (k == 0 && rec_u8_) {
+                    if (mpr8_)
+                        launch_conv_mpr(*mpr8_, rgbx_tv_, p.T[1], dBias_[0], reinterpret_cast<const uint32_t*>(idx), count,
+                                        S, relu, chg_next, tau_next, cnt_next, 2, nullptr, st);
+                    else
+                        launch_conv_tc(*tc8_, rgbx_tv_, p.T[1], dBias_[0], idx, count, full_count, relu, chg_next, tau_next,
+                                       cnt_next, 2, S, st);
+                    mark("conv_tc", 0);
+                    break;
+                }
+                if (mpr_[k] && !planar_in) {
+                    launch_conv_mpr(*mpr_[k], p.T[k], p.T[k + 1], dBias_[k], reinterpret_cast<const uint32_t*>(idx), count,
+                                    S, relu, chg_next, tau_next, cnt_next, 2, p.ovf, st);
+                    mark("conv_tc", k);
+                    break;
+                }
                 const int tail_last = (tc_[k] && !planar_in) ? tail_end(k) : -1;
                 if (tail_last > 0) {
                     // per-pixel layers k+1..tail_last fused into this conv's epilogue
@@ -648,7 +738,7 @@ void Engine::record(Plan& p, bool full) {
 }
 
 void Engine::launch(Plan& p, bool full) {
-    const int m = full ? 1 : 0;
+    const int m = (full ? 1 : 0) + (rec_u8_ ? 2 : 0);
     if (p.dirty) {
         for (auto& g : p.gexec)
             if (g) {
@@ -735,14 +825,15 @@ void Engine::enqueue_host_u8(int engine, const uint8_t* frames) {
     if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
     CBX_CUDA(cudaSetDevice(device_));
     const size_t per = (size_t)net_.inputChannels * net_.inputHeight * net_.inputWidth;
-    if (!u8_stage_) u8_stage_ = dmalloc<uint8_t>(per * S_);
-    float* slot = engine == CBX_ENGINE_CBINFER ? slots_[parity_] : slots_[2];
-    CBX_CUDA(cudaMemcpyAsync(u8_stage_, frames, per * S_, cudaMemcpyHostToDevice, stream_));
-    launch_decode_u8(u8_stage_, S_, net_.inputChannels, net_.inputHeight, net_.inputWidth, slot, stream_);
-    std::vector<const float*> cur(S_);
-    for (int s = 0; s < S_; ++s) cur[s] = slot + per * s;
-    forward_device(engine, cur.data());
-    if (engine == CBX_ENGINE_CBINFER) parity_ ^= 1;
+    // byte staging (CB ping-pong: the previous frame stays the detection
+    // reference; the dense comparator has its own slot)
+    const int q = engine == CBX_ENGINE_CBINFER ? parity8_ : 2;
+    if (!slots8_[q]) slots8_[q] = dmalloc<uint8_t>(per * S_);
+    CBX_CUDA(cudaMemcpyAsync(slots8_[q], frames, per * S_, cudaMemcpyHostToDevice, stream_));
+    std::vector<const uint8_t*> cur(S_);
+    for (int s = 0; s < S_; ++s) cur[s] = slots8_[q] + per * s;
+    forward_device_u8(engine, cur.data());
+    if (engine == CBX_ENGINE_CBINFER) parity8_ ^= 1;
 }
 
 void Engine::forward_host_u8(int engine, const uint8_t* frames, uint16_t* labels, cbx_layer_stats* stats,
@@ -770,29 +861,102 @@ void Engine::enqueue_host(int engine, const float* frames) {
 void Engine::forward_device(int engine, const float* const* frames_dev) {
     // counters stay on the device until cbx_read_stats asks for them (the
     // frame scratch holds the last frame's counters until the next frame)
-    enqueue(engine, frames_dev, nullptr);
+    enqueue(engine, frames_dev, nullptr, nullptr);
     stats_pending_[engine] = true;
+}
+
+void Engine::forward_device_u8(int engine, const uint8_t* const* frames_dev) {
+    enqueue(engine, nullptr, frames_dev, nullptr);
+    stats_pending_[engine] = true;
+}
+
+bool Engine::u8_native() const {
+    return u8_opt_ && tc8_ && rgb8_native_ok(net_.inputChannels, net_.inputHeight, net_.inputWidth);
+}
+
+// Frame path selection. 8-bit frames run natively (detection on the bytes,
+// kind::i8 layer 1) when the engine supports it and the change-based history
+// is 8-bit too (or there is none); otherwise they are decoded (px / 255.0f,
+// read_ppm) into an fp32 slot that then serves as the history. An fp32 frame
+// after 8-bit history gets the previous frames decoded as its detection
+// reference. Either way the change masks are those of the reference on
+// read_ppm's tensors.
+bool Engine::prepare_frame(int engine, const float* const* f32, const uint8_t* const* u8) {
+    if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
+    if (!f32 && !u8) throw Error(CBX_E_ARG, "frames is null");
+    CBX_CUDA(cudaSetDevice(device_));
+    const bool cb = engine == CBX_ENGINE_CBINFER;
+    const bool full = !cb || !has_history_;
+    const size_t per = (size_t)net_.inputChannels * net_.inputHeight * net_.inputWidth;
+    cur_u8_.clear();
+    cur_f32_.clear();
+    if (u8) {
+        for (int s = 0; s < S_; ++s)
+            if (!u8[s] || reinterpret_cast<uintptr_t>(u8[s]) % 16)
+                throw Error(CBX_E_ARG, "frame pointers must be non-null and 16-byte aligned");
+        rec_u8_ = u8_native() && (full || hist_u8_);
+        if (rec_u8_) {
+            cur_u8_.assign(u8, u8 + S_);
+            std::vector<const uint8_t*> tbl(2 * (size_t)S_);
+            for (int s = 0; s < S_; ++s) {
+                tbl[s] = u8[s];
+                tbl[S_ + s] = full ? u8[s] : last_cb_frames8_[s];
+            }
+            CBX_CUDA(cudaMemcpyAsync(d_cur8_, tbl.data(), sizeof(const uint8_t*) * 2 * S_, cudaMemcpyHostToDevice, stream_));
+            return full;
+        }
+        // decode into the fp32 staging slot of this frame
+        float* slot = cb ? slots_[parity_] : slots_[2];
+        if (cb) parity_ ^= 1;
+        for (int s = 0; s < S_; ++s) {
+            launch_decode_u8(u8[s], 1, net_.inputChannels, net_.inputHeight, net_.inputWidth, slot + per * s, stream_);
+            cur_f32_.push_back(slot + per * s);
+        }
+    } else {
+        rec_u8_ = false;
+        cur_f32_.assign(f32, f32 + S_);
+    }
+    const float* const* prev = nullptr;
+    std::vector<const float*> dec;
+    if (cb && !full) {
+        if (hist_u8_) {
+            if (!prev_dec_) prev_dec_ = dmalloc<float>(per * S_);
+            for (int s = 0; s < S_; ++s) {
+                launch_decode_u8(last_cb_frames8_[s], 1, net_.inputChannels, net_.inputHeight, net_.inputWidth,
+                                 prev_dec_ + per * s, stream_);
+                dec.push_back(prev_dec_ + per * s);
+            }
+            prev = dec.data();
+        } else {
+            prev = last_cb_frames_.data();
+        }
+    }
+    stage_frame_pointers(engine, cur_f32_.data(), prev);
+    return full;
+}
+
+void Engine::frame_done(int engine) {
+    if (engine != CBX_ENGINE_CBINFER) return;
+    has_history_ = true;
+    hist_u8_ = rec_u8_;
+    if (rec_u8_)
+        last_cb_frames8_ = cur_u8_;
+    else
+        last_cb_frames_ = cur_f32_;
 }
 
 // Enqueues one frame on the context stream (pointer table, graph, counter
 // readback into stats_dst); returns whether it is a full evaluation.
-bool Engine::enqueue(int engine, const float* const* frames_dev, unsigned long long* stats_dst) {
-    if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
-    if (!frames_dev) throw Error(CBX_E_ARG, "frames is null");
-    CBX_CUDA(cudaSetDevice(device_));
+bool Engine::enqueue(int engine, const float* const* frames_dev, const uint8_t* const* frames_u8,
+                     unsigned long long* stats_dst) {
+    const bool full = prepare_frame(engine, frames_dev, frames_u8);
     Plan& p = plan(engine);
-    const bool full = engine == CBX_ENGINE_BASELINE || !has_history_;
-    stage_frame_pointers(engine, frames_dev, engine == CBX_ENGINE_CBINFER && has_history_ ? last_cb_frames_.data() : nullptr);
     launch(p, full);
-    const int nl = (int)layers_.size();
     if (stats_dst)
         CBX_CUDA(cudaMemcpyAsync(stats_dst, p.stats, sizeof(unsigned long long) * stats_words(), cudaMemcpyDeviceToHost,
                                  stream_));
     last_full_[engine] = full;
-    if (engine == CBX_ENGINE_CBINFER) {
-        has_history_ = true;
-        last_cb_frames_.assign(frames_dev, frames_dev + S_);
-    }
+    frame_done(engine);
     return full;
 }
 
@@ -819,8 +983,7 @@ int64_t Engine::submit_any(int engine, const float* frames, const uint8_t* frame
     CBX_CUDA(cudaSetDevice(device_));
     const int nl = (int)layers_.size();
     const size_t per = (size_t)net_.inputChannels * net_.inputHeight * net_.inputWidth;
-    if (!ring_[0]) {
-        for (auto& r : ring_) r = dmalloc<float>(per * S_);
+    if (!copy_st_) {
         CBX_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
         for (int q = 0; q < kRing; ++q) {
             CBX_CUDA(cudaEventCreateWithFlags(&copied_[q], cudaEventDisableTiming));
@@ -835,17 +998,21 @@ int64_t Engine::submit_any(int engine, const float* frames, const uint8_t* frame
         if (!ring_u8_[q]) ring_u8_[q] = dmalloc<uint8_t>(per * S_);
         CBX_CUDA(cudaMemcpyAsync(ring_u8_[q], frames_u8, per * S_, cudaMemcpyHostToDevice, copy_st_));
     } else {
+        if (!ring_[q]) ring_[q] = dmalloc<float>(per * S_);
         CBX_CUDA(cudaMemcpyAsync(ring_[q], frames, per * S_ * sizeof(float), cudaMemcpyHostToDevice, copy_st_));
     }
     CBX_CUDA(cudaEventRecord(copied_[q], copy_st_));
     CBX_CUDA(cudaStreamWaitEvent(stream_, copied_[q], 0));
-    // ring_[q] was last read by frame j-2 (as its detection reference): the
-    // context stream has finished it before this decode runs
-    if (frames_u8)
-        launch_decode_u8(ring_u8_[q], S_, net_.inputChannels, net_.inputHeight, net_.inputWidth, ring_[q], stream_);
-    std::vector<const float*> cur(S_);
-    for (int s = 0; s < S_; ++s) cur[s] = ring_[q] + per * s;
-    ring_full_[q] = enqueue(engine, cur.data(), h_ring_stats_ + (size_t)q * stats_words());
+    // ring slot q was last read by frame j-2 (as its detection reference)
+    if (frames_u8) {
+        std::vector<const uint8_t*> cur(S_);
+        for (int s = 0; s < S_; ++s) cur[s] = ring_u8_[q] + per * s;
+        ring_full_[q] = enqueue(engine, nullptr, cur.data(), h_ring_stats_ + (size_t)q * stats_words());
+    } else {
+        std::vector<const float*> cur(S_);
+        for (int s = 0; s < S_; ++s) cur[s] = ring_[q] + per * s;
+        ring_full_[q] = enqueue(engine, cur.data(), nullptr, h_ring_stats_ + (size_t)q * stats_words());
+    }
     CBX_CUDA(cudaMemcpyAsync(labels, plan(engine).labels, sizeof(uint16_t) * S_ * lh_ * lw_, cudaMemcpyDeviceToHost,
                              stream_));
     CBX_CUDA(cudaEventRecord(done_[q], stream_));
@@ -920,7 +1087,7 @@ void Engine::stats_from(const unsigned long long* hs, bool full, int engine, cbx
 // frame copies it into its stats block: each frame whose outputs may carry
 // the overflow reports it, and the next frame is evaluated in full.
 void Engine::check_f16_overflow(const unsigned long long* hs, int engine) {
-    if (f16_layers_.empty() || !hs[stats_words() - 1]) return;
+    if (!any_f16_ || !hs[stats_words() - 1]) return;
     if (engine == CBX_ENGINE_CBINFER) has_history_ = false;
     throw Error(CBX_E_ARG,
                 "fp16 operand overflow: an input of a kind::f16 layer exceeded 65504 in magnitude "
@@ -972,6 +1139,9 @@ void Engine::load_layer(int layer, const float* K, const float* bias) {
     if (cb_) cb_->dirty = true;
     if (base_) base_->dirty = true;
     if (tc_[layer]) tc_load_weights(*tc_[layer], K, stream_);
+    if (layer == 0 && tc8_) tc_load_weights(*tc8_, K, stream_);
+    if (layer == 0 && mpr8_) mpr_load_weights(*mpr8_, K, stream_);
+    if (mpr_[layer]) mpr_load_weights(*mpr_[layer], K, stream_);
     CBX_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -1015,7 +1185,15 @@ void Engine::get_input(int engine, int layer, int s, float* out) {
     if (engine != CBX_ENGINE_CBINFER) throw Error(CBX_E_ARG, "the dense engine keeps no frame history");
     if (!has_history_) throw Error(CBX_E_SPEC, "no frame has been evaluated since the last reset");
     const size_t n = (size_t)net_.inputChannels * net_.inputHeight * net_.inputWidth;
-    CBX_CUDA(cudaMemcpyAsync(out, last_cb_frames_[s], n * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+    if (hist_u8_) {  // 8-bit history: the frame the reference would hold, px / 255.0f
+        float* tmp = nullptr;
+        CBX_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), stream_));
+        launch_decode_u8(last_cb_frames8_[s], 1, net_.inputChannels, net_.inputHeight, net_.inputWidth, tmp, stream_);
+        CBX_CUDA(cudaMemcpyAsync(out, tmp, n * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+        CBX_CUDA(cudaFreeAsync(tmp, stream_));
+    } else {
+        CBX_CUDA(cudaMemcpyAsync(out, last_cb_frames_[s], n * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+    }
     sync();
 }
 
@@ -1050,12 +1228,29 @@ void Engine::get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64
     CBX_CUDA(cudaMemcpy(&total, p.cnt[k], sizeof(int), cudaMemcpyDeviceToHost));
     std::vector<int32_t> all(total);
     if (total) CBX_CUDA(cudaMemcpy(all.data(), p.idx[k], sizeof(int32_t) * total, cudaMemcpyDeviceToHost));
+    const int R = list_group(k, hist_u8_);
+    const int Wo = dims_[6 * k + 5], Gw = (Wo + R - 1) / R;
+    const int64_t Ng = (int64_t)dims_[6 * k + 4] * Gw;
     int64_t m = 0;
-    for (int32_t g : all)
-        if (g >= s * N && g < (s + 1) * N) {
-            if (updated) updated[m] = (int32_t)(g - s * N);
-            ++m;
+    for (int32_t g : all) {
+        if (R == 1) {
+            if (g >= s * N && g < (s + 1) * N) {
+                if (updated) updated[m] = (int32_t)(g - s * N);
+                ++m;
+            }
+            continue;
         }
+        // group entry (gid << 4 | mask): its set pixels, ascending
+        const int64_t gid = (uint32_t)g >> 4;
+        if (gid < s * Ng || gid >= (s + 1) * Ng) continue;
+        const int64_t rem = gid - s * Ng;
+        const int64_t y = rem / Gw, x0 = (rem % Gw) * R;
+        for (int j = 0; j < R; ++j)
+            if ((g >> j) & 1) {
+                if (updated) updated[m] = (int32_t)(y * Wo + x0 + j);
+                ++m;
+            }
+    }
     if (n) *n = m;
 }
 
@@ -1084,12 +1279,10 @@ void Engine::mark(const char* name, int layer) {
 // One forward without the graph, each kernel bracketed by CUDA events on the
 // context stream (the stream every kernel is launched on). Advances the state
 // exactly like forward_device.
-void Engine::profile(int engine, const float* const* frames_dev, std::vector<cbx_kernel_time>& out) {
-    if (engine != CBX_ENGINE_CBINFER && engine != CBX_ENGINE_BASELINE) throw Error(CBX_E_ARG, "bad engine");
-    CBX_CUDA(cudaSetDevice(device_));
+void Engine::profile(int engine, const float* const* frames_dev, const uint8_t* const* frames_u8,
+                     std::vector<cbx_kernel_time>& out) {
+    const bool full = prepare_frame(engine, frames_dev, frames_u8);
     Plan& p = plan(engine);
-    const bool full = engine == CBX_ENGINE_BASELINE || !has_history_;
-    stage_frame_pointers(engine, frames_dev, engine == CBX_ENGINE_CBINFER && has_history_ ? last_cb_frames_.data() : nullptr);
     std::vector<ProfMark> marks;
     prof_ = &marks;
     try {
@@ -1118,10 +1311,7 @@ void Engine::profile(int engine, const float* const* frames_dev, std::vector<cbx
     last_full_[engine] = full;
     finish_stats(p, full, engine);  // h_stats_ was filled above
     stats_pending_[engine] = false;
-    if (engine == CBX_ENGINE_CBINFER) {
-        has_history_ = true;
-        last_cb_frames_.assign(frames_dev, frames_dev + S_);
-    }
+    frame_done(engine);
 }
 
 }  // namespace cbx
@@ -1277,6 +1467,12 @@ void Engine::set_option(int option, int value) {
         }
     } else if (option == CBX_OPT_FUSE_TAIL) {
         fuse_tail_ = value != 0;
+    } else if (option == CBX_OPT_U8_NATIVE) {
+        // switching paths keeps results within the tolerance, not bitwise:
+        // the next frame is a full evaluation
+        if (u8_opt_ != (value != 0)) has_history_ = false;
+        u8_opt_ = value != 0;
+        return;
     } else {
         throw Error(CBX_E_ARG, "unknown option");
     }

@@ -20,6 +20,7 @@
 
 #include "../../include/cbx.h"
 #include "common.cuh"
+#include "conv_mpr.hpp"
 #include "conv_tc.hpp"
 
 namespace cbx {
@@ -57,6 +58,10 @@ public:
     int64_t submit_u8(int engine, const uint8_t* frames, uint16_t* labels);
     int num_streams() const { return S_; }
     void forward_device(int engine, const float* const* frames_dev);
+    // 8-bit interleaved frames already on the device (frames_dev[s] = H x W x C bytes)
+    void forward_device_u8(int engine, const uint8_t* const* frames_dev);
+    // the 8-bit camera path runs natively (RGB8 detection + kind::i8 layer 1)
+    bool u8_native() const;
     // pipelined host-frame path (cbx_submit / cbx_wait)
     int64_t submit(int engine, const float* frames, uint16_t* labels);
     void wait(int64_t ticket, cbx_layer_stats* stats, uint64_t* macs);
@@ -68,7 +73,8 @@ public:
     void get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64_t* n, int* first);
     void worst_case_counts(int64_t* worst);
 
-    void profile(int engine, const float* const* frames_dev, std::vector<cbx_kernel_time>& out);
+    void profile(int engine, const float* const* frames_dev, const uint8_t* const* frames_u8,
+                 std::vector<cbx_kernel_time>& out);
     void read_step_times(int64_t* out);  // [nl][5] of the last graph launch (CBX_OPT_STEP_TIMES)
     bool has_history() const { return has_history_; }
     void get_input(int engine, int layer, int s, float* out);
@@ -87,9 +93,14 @@ private:
     void record(Plan& p, bool full);
     void launch(Plan& p, bool full);
     void stage_frame_pointers(int engine, const float* const* cur, const float* const* prev);
+    // picks the frame path (8-bit native or fp32), decodes when needed, stages
+    // the pointer tables; returns whether the frame is a full evaluation
+    bool prepare_frame(int engine, const float* const* f32, const uint8_t* const* u8);
+    void frame_done(int engine);  // history bookkeeping after a frame was enqueued
     void finish_stats(Plan& p, bool full, int engine);
     void stats_from(const unsigned long long* hs, bool full, int engine, cbx_layer_stats* out, uint64_t* macs) const;
-    bool enqueue(int engine, const float* const* frames_dev, unsigned long long* stats_dst);
+    bool enqueue(int engine, const float* const* frames_dev, const uint8_t* const* frames_u8,
+                 unsigned long long* stats_dst);
     void mark(const char* name, int layer);
     int tail_end(int k) const;
     int final_tensor() const;
@@ -122,6 +133,11 @@ private:
     std::vector<std::vector<float>> hK_, hB_;  // host copies (kernel-parameter filters)
     std::vector<std::unique_ptr<TcLayer, TcLayerDeleter>> tc_;
     std::vector<int> f16_layers_;  // tcgen05 layers with fp16 operands (their input has an fp16 shadow)
+    // multi-pixel-row tcgen05 convs (conv_mpr.cu): narrow layers with a
+    // 4-channel input, fp16 operands converted while gathering
+    std::vector<std::unique_ptr<MprLayer, MprLayerDeleter>> mpr_;
+    bool any_f16_ = false;  // some layer has fp16 operands: the plan keeps an overflow flag
+    int list_group(int k, bool u8) const;  // group width of layer k's update list (1 = pixel indices)
     void check_f16_overflow(const unsigned long long* hs, int engine);
     bool last_ovf_[2] = {false, false};
     // device counters of one frame: [nl][S][2] + the fp16 overflow flag
@@ -139,15 +155,32 @@ private:
     const float** d_cur_ = nullptr;
     const float** d_prev_ = nullptr;
     std::vector<const float*> last_cb_frames_;
+
+    // 8-bit camera path (TC precisions, RGB frames with W % 16 == 0, conv
+    // first layer): detection on the bytes fused with the RGBX expansion of
+    // the frame, layer 1 as a kind::i8 tcgen05 conv over the RGBX bytes.
+    std::unique_ptr<TcLayer, TcLayerDeleter> tc8_;
+    std::unique_ptr<MprLayer, MprLayerDeleter> mpr8_;  // the same as a multi-pixel-row conv (preferred)
+    bool u8_opt_ = true;          // CBX_OPT_U8_NATIVE
+    bool rec_u8_ = false;         // the frame being recorded/launched is 8-bit native
+    Rgbx8View rgbx_{};            // RGBX copy of the current frame (zero halo)
+    TensorView rgbx_tv_{};        // the same buffer as the layer-1 conv input (Cp = 1)
+    const uint8_t** d_cur8_ = nullptr;
+    const uint8_t** d_prev8_ = nullptr;
+    std::vector<const uint8_t*> last_cb_frames8_;
+    bool hist_u8_ = false;        // the change-based history holds 8-bit frames
+    float* prev_dec_ = nullptr;   // decoded 8-bit history for an fp32 frame that follows it
+    uint8_t* slots8_[3] = {nullptr, nullptr, nullptr};  // 8-bit host staging (CB ping-pong + baseline)
+    std::vector<const float*> cur_f32_;   // pointers of the frame being enqueued (fp32 path)
+    std::vector<const uint8_t*> cur_u8_;  // (8-bit native path)
     // host-input staging slots: CB ping-pong + baseline
     float* slots_[3] = {nullptr, nullptr, nullptr};
-    int parity_ = 0;
+    int parity_ = 0, parity8_ = 0;
 
     // submit/wait ring: staging slots, copy stream, per-slot events and counters
     static constexpr int kRing = 3;
     float* ring_[kRing] = {nullptr, nullptr, nullptr};
     uint8_t* ring_u8_[kRing] = {nullptr, nullptr, nullptr};  // 8-bit submissions
-    uint8_t* u8_stage_ = nullptr;                             // 8-bit synchronous forwards
     int64_t submit_any(int engine, const float* frames, const uint8_t* frames_u8, uint16_t* labels);
     cudaStream_t copy_st_ = nullptr;
     cudaEvent_t copied_[kRing] = {nullptr, nullptr, nullptr}, done_[kRing] = {nullptr, nullptr, nullptr};

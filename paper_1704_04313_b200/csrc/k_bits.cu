@@ -148,6 +148,172 @@ __global__ void __launch_bounds__(256) detect_c3_kernel(const float* const* cur,
     }
 }
 
+// K1 on 8-bit camera frames (the PPM raster read_ppm decodes, io.cpp:60-104):
+// H x W x 3 interleaved bytes per stream, W a multiple of 16. A thread owns 16
+// pixels (48 bytes = three 128-bit loads per frame). Pixel values are the
+// reference's px / 255.0f (__fdiv_rn, correctly rounded like the host
+// division), so the change test is detect_changes on read_ppm's tensors bit
+// for bit; bytes that are equal in both frames give d = 0 and are skipped
+// without decoding. The same pass writes the current frame as 4-byte RGBX
+// pixels (channel 3 = 0) into the zero-halo tensor the layer-1 tcgen05 conv
+// gathers from, one 4-byte chunk per tap.
+//   MODE 0: threshold test (CBCONV); MODE 1: any byte differs (updated
+//   pixels of a non-CB first layer); MODE 2: full frame, expansion only.
+template <int MODE>
+__global__ void __launch_bounds__(256) detect_rgb8_kernel(const uint8_t* const* cur, const uint8_t* const* prev, int H,
+                                                          int W, float tau, int dlo, int dhi, BitMask m,
+                                                          unsigned long long* cnt, int cstride, Rgbx8View x) {
+    // px / 255.0f of every byte value: the reference's read_ppm decode
+    // (correctly rounded division, like the host's)
+    __shared__ float lut[256];
+    if (MODE == 0) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = __fdiv_rn((float)i, 255.0f);
+        __syncthreads();
+    }
+    const uint32_t lo4 = (uint32_t)dlo * 0x01010101u, hi4 = (uint32_t)min(dhi, 255) * 0x01010101u;
+    const int s = blockIdx.y;
+    const uint4* a = reinterpret_cast<const uint4*>(cur[s]);
+    const uint4* b = MODE == 2 ? nullptr : reinterpret_cast<const uint4*>(prev[s]);
+    const int wpr = (W + 31) >> 5;
+    const int gpr = 2 * wpr;  // 16-pixel groups per row, padded to whole mask words
+    const int ng = H * gpr;
+    const int lane = threadIdx.x & 31;
+    uint32_t* dst = MODE == 2 ? nullptr : m.d + (int64_t)s * m.stride;
+    uint32_t* xs = x.d + (int64_t)s * x.ss;
+    for (int base = blockIdx.x * blockDim.x; base < ng; base += gridDim.x * blockDim.x) {
+        const int g = base + threadIdx.x;
+        const int y = g / gpr, gx = g - y * gpr;
+        const bool act = g < ng && 16 * gx < W;
+        uint32_t flags = 0, amb = 0;
+        uint32_t o[16], op[16];
+        if (act) {
+            const int64_t q = ((int64_t)y * W + 16 * gx) / 16 * 3;  // uint4 index of the 48-byte group
+            uint32_t cw[12], pw[12];
+            {
+                const uint4 c0 = __ldg(a + q), c1 = __ldg(a + q + 1), c2 = __ldg(a + q + 2);
+                cw[0] = c0.x; cw[1] = c0.y; cw[2] = c0.z; cw[3] = c0.w;
+                cw[4] = c1.x; cw[5] = c1.y; cw[6] = c1.z; cw[7] = c1.w;
+                cw[8] = c2.x; cw[9] = c2.y; cw[10] = c2.z; cw[11] = c2.w;
+            }
+            if constexpr (MODE != 2) {
+                const uint4 p0 = __ldcs(b + q), p1 = __ldcs(b + q + 1), p2 = __ldcs(b + q + 2);
+                pw[0] = p0.x; pw[1] = p0.y; pw[2] = p0.z; pw[3] = p0.w;
+                pw[4] = p1.x; pw[5] = p1.y; pw[6] = p1.z; pw[7] = p1.w;
+                pw[8] = p2.x; pw[9] = p2.y; pw[10] = p2.z; pw[11] = p2.w;
+            }
+            // RGBX expansion: pixel p = bytes 3p..3p+2 of the group
+#pragma unroll
+            for (int p = 0; p < 16; ++p) {
+                const int bi = 3 * p, wi = bi >> 2, r = bi & 3;
+                const uint32_t sel = (uint32_t)(r | ((r + 1) << 4) | ((r + 2) << 8));
+                o[p] = __byte_perm(cw[wi], wi + 1 < 12 ? cw[wi + 1] : 0u, sel) & 0x00ffffffu;
+                if constexpr (MODE != 2) {
+                    op[p] = __byte_perm(pw[wi], wi + 1 < 12 ? pw[wi + 1] : 0u, sel) & 0x00ffffffu;
+                    // |a - b| per channel byte: >= dhi is changed for every byte
+                    // pair, < dlo for none; in between decide exactly below
+                    const uint32_t ad = __vabsdiffu4(o[p], op[p]);
+                    if (__vcmpgeu4(ad, hi4) && dhi <= 255) flags |= 1u << p;
+                    else if (__vcmpgeu4(ad, lo4)) amb |= 1u << p;
+                }
+            }
+            uint4* xo = reinterpret_cast<uint4*>(xs + (int64_t)(y + x.hh) * x.Wp + x.hw + 16 * gx);
+            xo[0] = make_uint4(o[0], o[1], o[2], o[3]);
+            xo[1] = make_uint4(o[4], o[5], o[6], o[7]);
+            xo[2] = make_uint4(o[8], o[9], o[10], o[11]);
+            xo[3] = make_uint4(o[12], o[13], o[14], o[15]);
+        }
+        if constexpr (MODE != 2) {
+            // the exact test (decode + reference compare) for pixels whose
+            // channel differences straddle tau's byte-difference boundary --
+            // none for a tau that is not within an ulp of some k / 255
+            if (__any_sync(0xffffffffu, amb != 0u)) {
+#pragma unroll
+                for (int p = 0; p < 16; ++p) {
+                    if ((amb >> p) & 1u) {
+                        bool c = false;
+#pragma unroll
+                        for (int e = 0; e < 3; ++e) {
+                            const uint32_t u = (o[p] >> (8 * e)) & 0xffu, v = (op[p] >> (8 * e)) & 0xffu;
+                            c |= MODE == 1 ? u != v : ref_changed(lut[u], lut[v], tau);
+                        }
+                        if (c) flags |= 1u << p;
+                    }
+                }
+            }
+            uint32_t word = flags << (16 * (gx & 1));
+            word |= __shfl_xor_sync(0xffffffffu, word, 1);
+            if (g < ng && (gx & 1) == 0) dst[(int64_t)y * m.wpr + (gx >> 1)] = word;
+            if (cnt) {
+                const int n = __reduce_add_sync(0xffffffffu, __popc(flags));
+                if (lane == 0 && n) atomicAdd(cnt + (int64_t)s * cstride, (unsigned long long)n);
+            }
+        }
+    }
+}
+
+// Byte-difference bounds of the reference change test on read_ppm values for
+// threshold tau: a channel pair (u, v) of bytes is changed
+// (ref_changed(u / 255.0f, v / 255.0f, tau)) for every pair with
+// |u - v| >= dhi and for no pair with |u - v| < dlo (brute force over all
+// 65536 pairs with the same IEEE division and subtraction as the device).
+// dhi = 256 when some difference class is never entirely changed above dlo.
+static void rgb8_tau_bounds(float tau, int mode, int& dlo, int& dhi) {
+    if (mode == 1) {  // bitwise: any differing byte
+        dlo = dhi = 1;
+        return;
+    }
+    // (one tau per layer-1 threshold setting: remember the last one)
+    thread_local float last_tau = -1.0f;
+    thread_local int last_lo = 0, last_hi = 0;
+    if (tau == last_tau) {
+        dlo = last_lo;
+        dhi = last_hi;
+        return;
+    }
+    bool any[256] = {}, all[256];
+    for (int k = 0; k < 256; ++k) all[k] = true;
+    for (int u = 0; u < 256; ++u)
+        for (int v = 0; v < 256; ++v) {
+            const float fu = (float)u / 255.0f, fv = (float)v / 255.0f;
+            const float d = fu - fv;
+            const bool c = d > tau || -d > tau;
+            const int k = u > v ? u - v : v - u;
+            any[k] = any[k] || c;
+            all[k] = all[k] && c;
+        }
+    dlo = 256;
+    for (int k = 0; k < 256; ++k)
+        if (any[k]) {
+            dlo = k;
+            break;
+        }
+    dhi = 256;
+    for (int k = 255; k >= 0 && all[k]; --k) dhi = k;
+    if (dhi < dlo) dhi = dlo;
+    last_tau = tau;
+    last_lo = dlo;
+    last_hi = dhi;
+}
+
+bool rgb8_native_ok(int C, int H, int W) { return C == 3 && W % 16 == 0 && W > 0 && H > 0 && (int64_t)H * W < (1 << 30); }
+
+void launch_detect_rgb8(const uint8_t* const* cur, const uint8_t* const* prev, int S, int H, int W, float tau, int mode,
+                        BitMask m, unsigned long long* cnt, int cstride, Rgbx8View x, cudaStream_t st) {
+    const int ng = H * 2 * ((W + 31) / 32);
+    int gx = (ng + 255) / 256;
+    const int cap = (kNumSMs * 8 + S - 1) / S;
+    if (gx > cap) gx = cap < 1 ? 1 : cap;
+    const dim3 grid(gx, S);
+    int dlo = 256, dhi = 256;
+    if (mode != 2) rgb8_tau_bounds(tau, mode, dlo, dhi);
+    if (mode == 0)
+        detect_rgb8_kernel<0><<<grid, 256, 0, st>>>(cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
+    else if (mode == 1)
+        detect_rgb8_kernel<1><<<grid, 256, 0, st>>>(cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
+    else
+        detect_rgb8_kernel<2><<<grid, 256, 0, st>>>(cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
+}
+
 void launch_detect_bits(const float* const* cur, const float* const* prev, int S, int C, int H, int W, float tau,
                         int mode, BitMask m, unsigned long long* cnt, int cstride, cudaStream_t st) {
     const int64_t nq = (int64_t)H * m.wpr * 8;
@@ -298,7 +464,15 @@ __device__ __forceinline__ uint32_t hdilate(uint32_t prev, uint32_t cur, uint32_
 // words. It is staged into shared memory with coalesced 16-byte loads,
 // horizontally dilated once per input word, and every output word is then
 // the OR of kh shared-memory words.
-template <int WPT>
+//
+// R = 1: the list holds pixel indices s*Ho*Wo + y*Wo + x (extract_indexes
+// order). R = 2 / 4: it holds GROUP entries (gid << 4 | mask) of R
+// horizontally adjacent pixels, gid = s*Ho*Gw + y*Gw + x / R, mask = the
+// group's set pixels (the multi-pixel-row conv's tiles, conv_mpr.cu); the
+// per-stream counter still counts pixels. The list is written warp-
+// cooperatively: each non-empty word is expanded by the 32 lanes at once, so
+// every store instruction writes consecutive entries (coalesced).
+template <int WPT, int R>
 __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, BitMask out, bool write_out,
                                                                     int kh, int kw, int ph, int pw, bool identity,
                                                                     int32_t* __restrict__ idx, int* total,
@@ -343,11 +517,22 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
         __syncthreads();
     }
     uint32_t words[WPT];
-    int my = 0;
+    int my = 0, mypx = 0;
+    // per-group "non-empty" bit at the group's lowest bit position
+    auto group_bits = [](uint32_t w) -> uint32_t {
+        if (R == 1) return w;
+        if (R == 2) return (w | (w >> 1)) & 0x55555555u;
+        uint32_t t = w | (w >> 1);
+        return (t | (t >> 2)) & 0x11111111u;
+    };
+    const int y0 = (int)(w0 / out.wpr), wr0 = (int)(w0 - (int64_t)y0 * out.wpr);
 #pragma unroll
     for (int i = 0; i < WPT; ++i) {
-        const int64_t wi = w0 + i;
-        const int y = (int)(wi / out.wpr), w = (int)(wi - (int64_t)(wi / out.wpr) * out.wpr);
+        int y = y0, w = wr0 + i;
+        if (w >= out.wpr) {  // (a thread's WPT words may wrap into the next rows)
+            y += w / out.wpr;
+            w -= (w / out.wpr) * out.wpr;
+        }
         uint32_t word = 0;
         if (y < out.H && w < in.wpr) {
             if (identity) {
@@ -364,12 +549,17 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
             word = 0;
         }
         words[i] = word;
-        my += __popc(word);
+        mypx += __popc(word);
+        my += __popc(group_bits(word));
     }
     if (write_out) {
         uint32_t* o = out.d + (int64_t)s * out.stride + w0;
 #pragma unroll
         for (int i = 0; i < WPT; ++i) o[i] = words[i];
+    }
+    if (cnt) {  // changed pixels per stream (a tile never straddles two streams)
+        const int wpx = __reduce_add_sync(0xffffffffu, mypx);
+        if ((threadIdx.x & 31) == 0 && wpx) atomicAdd(cnt + (int64_t)s * cstride, (unsigned long long)wpx);
     }
     int agg;
     const int excl = block_scan(my, s_warp, agg);
@@ -377,25 +567,39 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
         const long long b = lookback(status, tile, agg);
         if (threadIdx.x == 0) {
             s_base = b;
-            if (agg && cnt) atomicAdd(cnt + (int64_t)s * cstride, (unsigned long long)agg);
             if (tile == gridDim.x - 1) *total = (int)(b + agg);  // the last tile holds the inclusive total
         }
     }
     __syncthreads();
-    int64_t o = s_base + excl;
-    const int64_t sbase = (int64_t)s * out.H * out.W;
+    const int lane = threadIdx.x & 31;
+    int64_t o = s_base + excl;  // this thread's first entry
+    const int Gw = (out.W + R - 1) / R;
+    const int64_t sbase = R == 1 ? (int64_t)s * out.H * out.W : (int64_t)s * out.H * Gw;
 #pragma unroll
     for (int i = 0; i < WPT; ++i) {
-        uint32_t word = words[i];
-        if (!word) continue;
-        const int64_t wi = w0 + i;
-        const int y = (int)(wi / out.wpr), w = (int)(wi - (int64_t)(wi / out.wpr) * out.wpr);
-        const int64_t gbase = sbase + (int64_t)y * out.W + 32 * w;
-        while (word) {
-            const int k = __ffs(word) - 1;
-            word &= word - 1;
-            idx[o++] = (int32_t)(gbase + k);
+        const uint32_t word = words[i];
+        const uint32_t gb = group_bits(word);
+        unsigned todo = __ballot_sync(0xffffffffu, gb != 0u);
+        while (todo) {  // expand lane src's word with all 32 lanes
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t wsrc = __shfl_sync(0xffffffffu, word, src);
+            const uint32_t gsrc = __shfl_sync(0xffffffffu, gb, src);
+            const int64_t osrc = __shfl_sync(0xffffffffu, o, src);
+            const int64_t wglob = __shfl_sync(0xffffffffu, w0 + i, src);
+            const int ys = (int)(wglob / out.wpr), ws = (int)(wglob - (int64_t)ys * out.wpr);
+            const int bit = lane * R;
+            if (bit < 32 && ((gsrc >> bit) & 1u)) {
+                const int64_t pos = osrc + __popc(gsrc & ((1u << bit) - 1u));
+                if (R == 1) {
+                    idx[pos] = (int32_t)(sbase + (int64_t)ys * out.W + 32 * ws + lane);
+                } else {
+                    const int64_t gid = sbase + (int64_t)ys * Gw + (32 * ws) / R + lane;
+                    idx[pos] = (int32_t)((gid << 4) | ((wsrc >> bit) & ((1u << R) - 1u)));
+                }
+            }
         }
+        o += __popc(gb);
     }
 }
 
@@ -409,21 +613,33 @@ size_t dilate_compact_workspace(const BitMask& out, int S) {
     return (size_t)round_up(tiles * 8 + 16, 256);
 }
 
-template <int WPT>
-static void launch_dc(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw, bool identity,
-                      int32_t* idx, int* total, unsigned long long* status, unsigned long long* cnt, int cstride,
-                      cudaStream_t st) {
+template <int WPT, int R>
+static void launch_dc_r(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw, bool identity,
+                        int32_t* idx, int* total, unsigned long long* status, unsigned long long* cnt, int cstride,
+                        cudaStream_t st) {
     const int64_t tiles = (int64_t)S * (out.stride / (kDcThreads * WPT));
     const size_t smem = dc_smem_bytes(in, out, identity ? 1 : kh, WPT);
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(dilate_compact_kernel<WPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dilate_compact_kernel<WPT><<<(unsigned)tiles, kDcThreads, smem, st>>>(in, out, write_out, kh, kw, ph, pw, identity,
-                                                                          idx, total, status, cnt, cstride);
+        cudaFuncSetAttribute(dilate_compact_kernel<WPT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dilate_compact_kernel<WPT, R><<<(unsigned)tiles, kDcThreads, smem, st>>>(in, out, write_out, kh, kw, ph, pw,
+                                                                             identity, idx, total, status, cnt, cstride);
+}
+
+template <int WPT>
+static void launch_dc(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw, bool identity,
+                      int32_t* idx, int* total, unsigned long long* status, unsigned long long* cnt, int cstride,
+                      cudaStream_t st, int R) {
+    if (R == 4)
+        launch_dc_r<WPT, 4>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st);
+    else if (R == 2)
+        launch_dc_r<WPT, 2>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st);
+    else
+        launch_dc_r<WPT, 1>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st);
 }
 
 void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw,
                            int32_t* idx, int* total, void* workspace, unsigned long long* cnt, int cstride,
-                           cudaStream_t st, bool ws_zeroed) {
+                           cudaStream_t st, bool ws_zeroed, int R) {
     unsigned long long* status = reinterpret_cast<unsigned long long*>(workspace);
     const bool identity = kh == 1 && kw == 1 && ph == 0 && pw == 0;
     const int64_t words = (int64_t)S * out.stride;
@@ -433,10 +649,10 @@ void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int k
     const int64_t tiles = words / (kDcThreads * wpt);
     if (!ws_zeroed) cudaMemsetAsync(workspace, 0, tiles * 8 + 16, st);
     switch (wpt) {
-        case 8: launch_dc<8>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st); break;
-        case 4: launch_dc<4>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st); break;
-        case 2: launch_dc<2>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st); break;
-        default: launch_dc<1>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st); break;
+        case 8: launch_dc<8>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st, R); break;
+        case 4: launch_dc<4>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st, R); break;
+        case 2: launch_dc<2>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st, R); break;
+        default: launch_dc<1>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st, R); break;
     }
 }
 

@@ -23,12 +23,18 @@ void launch_compact(MaskView m, int S, int32_t* idx, int* total, void* workspace
 // ---- k_bits.cu: the engine's packed-bit mask pipeline ----
 void launch_detect_bits(const float* const* cur, const float* const* prev, int S, int C, int H, int W, float tau,
                         int mode, BitMask m, unsigned long long* cnt, int cstride, cudaStream_t st);
+// 8-bit interleaved RGB frames (W % 16 == 0): detection (mode 0 threshold,
+// 1 bitwise) fused with the RGBX expansion of the current frame; mode 2 =
+// expansion only (full evaluations).
+bool rgb8_native_ok(int C, int H, int W);
+void launch_detect_rgb8(const uint8_t* const* cur, const uint8_t* const* prev, int S, int H, int W, float tau, int mode,
+                        BitMask m, unsigned long long* cnt, int cstride, Rgbx8View x, cudaStream_t st);
 size_t dilate_compact_workspace(const BitMask& out, int S);
 // ws_zeroed: the caller zeroed `workspace` (the look-back status words) in
 // the same stream, e.g. with the frame's single scratch memset.
 void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw,
                            int32_t* idx, int* total, void* workspace, unsigned long long* cnt, int cstride,
-                           cudaStream_t st, bool ws_zeroed = false);
+                           cudaStream_t st, bool ws_zeroed = false, int R = 1);
 void launch_dilate_bits(BitMask in, BitMask out, int S, int kh, int kw, int sh, int sw, int ph, int pw,
                         cudaStream_t st);
 

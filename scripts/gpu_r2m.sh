@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_u8.py tests/test_gpu_tc.py -q -x 2>&1 | tail -3
+python scripts/frame_probe.py --frames 4 --profile 2>&1 | tail -3
+python scripts/frame_probe.py --frames 4 --profile --input f32 2>&1 | tail -2

@@ -3,11 +3,13 @@ default workload) against the UNMODIFIED reference compiled from its sources
 (oracle/_ref, the bench's --impl reference arm):
 
 * paper_like.json at 1920x1080, S = 2 streams in 2 lanes, precision "f16"
-  (the bench default: layer 1 exact fp32, layer 2 kind::tf32, layer 3
-  kind::f16), base thresholds (0.04, 0.05, 0.05), the bench's sprite recipe
-  (12 sprites x 128 px, 12 px/frame) with per-stream seeds
-  (shard.stream_seed), weights generate_weights(seed 1) written by the
-  reference itself;
+  (the bench default: layer 1 kind::i8 on the 8-bit frames, layer 2
+  kind::tf32, layer 3 kind::f16), base thresholds (0.04, 0.05, 0.05), the
+  bench's sprite recipe (12 sprites x 128 px, 12 px/frame) with per-stream
+  seeds (shard.stream_seed) quantized to 8-bit camera frames exactly as the
+  bench does (bench.quantize_u8); the GPU takes the bytes (cbx_forward_u8,
+  native path), the reference read_ppm's decode of them (bench.decode_u8);
+  weights generate_weights(seed 1) written by the reference itself;
 * frame 0 (full evaluation) and two steady frames, every stream checked:
   - layer-1 detected mask and updated index list bit-exact,
   - layers 2-3: popcount(detected XOR) and |updated symdiff| <= 1 % of the
@@ -32,6 +34,7 @@ RECIPE = [(128, 12, 0.9)] * 12
 
 
 def test_bench_configuration_vs_reference(gpu):
+    import bench
     import oracle
     from paper_1704_04313_b200 import shard
     if not os.path.exists(oracle.REF_SO):
@@ -42,14 +45,15 @@ def test_bench_configuration_vs_reference(gpu):
     rnets.append(ref.load_network(spec, 1, weights_dir=rnets[0].weights_dir))
     net = gpu.Network(to_pkg_spec(gpu, spec), rnets[0].weights_dir, streams=S, precision="f16", lanes=LANES)
     assert net.num_lanes() == LANES
-    assert [net.layer_operands(k) for k in (0, 2, 4)] == ["fp32", "tf32", "f16"]
+    assert [net.layer_operands(k) for k in (0, 2, 4)] == ["i8", "tf32", "f16"]
     cfgs = [dict(channels=3, height=H, width=W, sprites=RECIPE, noise=0.0, seed=shard.stream_seed(g))
             for g in range(S)]
     nproc = os.cpu_count() or 1
     report = []
     for f in range(3):
-        frames = [ref.synth_frame(c, f) for c in cfgs]
-        got = net.forward(np.stack(frames))
+        cams = [bench.quantize_u8(ref.synth_frame(c, f)) for c in cfgs]
+        frames = [bench.decode_u8(x) for x in cams]
+        got = net.forward_u8(np.stack(cams))
         if f == 0:
             for s in range(S):  # the reference's full first frame, its ops split over all cores
                 rnets[s].warm(frames[s], nproc)

@@ -205,17 +205,22 @@ def test_tf32_mask_mismatch_counts(gpu, orc, h, w, prec):
 
 
 def test_layer_operands(gpu, orc):
-    """Operand formats reported per conv layer: layer 1 exact fp32 (planar
-    first layer), layer 2 tf32, layer 3 fp16 (fed by a MAXPOOL) under
+    """Operand formats reported per conv layer: layer 1 kind::i8 for 8-bit
+    frames (exact fp32 for planar fp32 frames), layer 2 tf32, layer 3 fp16 (fed by a MAXPOOL) under
     precision f16 and tf32 under precision tf32; the head's 1x1 convs exact;
     exact mode fp32 only."""
     spec = paper_spec(32, 48)
     w = orc.generate_weights(spec, 1)
     net = gpu.Network(to_pkg_spec(gpu, spec), w, precision="f16")
-    assert [net.layer_operands(k) for k in (0, 2, 4, 5)] == ["fp32", "tf32", "f16", "fp32"]
+    # layer 1: kind::i8 for 8-bit frames (width 48 is a multiple of 16; fp32
+    # frames take the exact path)
+    assert [net.layer_operands(k) for k in (0, 2, 4, 5)] == ["i8", "tf32", "f16", "fp32"]
     assert net.layer_operands(1) == "none"  # MAXPOOL
     net2 = gpu.Network(to_pkg_spec(gpu, spec), w, precision="tf32")
-    assert [net2.layer_operands(k) for k in (0, 2, 4, 5)] == ["fp32", "tf32", "tf32", "fp32"]
+    assert [net2.layer_operands(k) for k in (0, 2, 4, 5)] == ["i8", "tf32", "tf32", "fp32"]
+    odd = paper_spec(32, 40)  # width not a multiple of 16: no 8-bit native path
+    net3 = gpu.Network(to_pkg_spec(gpu, odd), orc.generate_weights(odd, 1), precision="tf32")
+    assert net3.layer_operands(0) == "fp32"
     ex = gpu.Network(to_pkg_spec(gpu, spec), w, precision="exact")
     assert all(ex.layer_operands(k) == "fp32" for k in (0, 2, 4))
 
@@ -447,7 +452,7 @@ def test_step_times(gpu, orc):
 @pytest.mark.parametrize("precision", ["exact", "f16"])
 def test_u8_ingest_equals_decoded_frames(gpu, orc, precision):
     """8-bit camera frames (the PPM raster, io.cpp:60-104) through
-    cbx_forward_u8 / cbx_submit_u8 give bitwise the labels, stats, traces and
+    cbx_forward_u8 / cbx_submit_u8 with CBX_OPT_U8_NATIVE = 0 give bitwise the labels, stats, traces and
     activations of cbx_forward on the planar px / 255.0f frames read_ppm would
     produce (numpy float32 division is the same IEEE-rounded division)."""
     spec = paper_spec(48, 64)
@@ -464,6 +469,10 @@ def test_u8_ingest_equals_decoded_frames(gpu, orc, precision):
     a = gpu.Network(to_pkg_spec(gpu, spec), w, streams=S, precision=precision)
     b = gpu.Network(to_pkg_spec(gpu, spec), w, streams=S, precision=precision)
     p = gpu.Network(to_pkg_spec(gpu, spec), w, streams=S, precision=precision)
+    # the decode path (bitwise the fp32 path); the native 8-bit path is
+    # covered by tests/test_gpu_u8.py
+    a.set_u8_native(False)
+    p.set_u8_native(False)
     labs = [np.zeros((S,) + tuple(p.label_hw), np.uint16) for _ in range(5)]
     tickets = [p.submit_u8(u8[f], labs[f]) for f in range(3)]
     waited = {t: p.wait(t) for t in tickets}

@@ -177,3 +177,44 @@ def test_fused_tail_equals_unfused(gpu, orc, monkeypatch, maxctas, prec):
     for engine in ("baseline",):
         a, b = fused.forward_frame(fr, engine), plain.forward_frame(fr, engine)
         assert np.array_equal(a.labels, b.labels)
+
+
+# multi-pixel-row convs (conv_mpr.cu): precision "f16" with CBX_MPR_F16=1, a <= 4-channel input;
+# groups of R adjacent output pixels per tensor-core row, fp16 operands
+# converted while gathering. Widths not divisible by R, channel padding
+# (3 -> 4 inputs, 37 -> 40 outputs), asymmetric kernels and a 1x1 kernel.
+MPR_CASES = [
+    (4, 60, 80, dict(kind="CBCONV", kernelH=7, kernelW=7, padH=3, padW=3, outChannels=52, threshold=0.0, fuseRelu=True, weightsFile="b")),
+    (3, 33, 47, dict(kind="CBCONV", kernelH=3, kernelW=3, padH=1, padW=1, outChannels=37, threshold=0.0, fuseRelu=False, weightsFile="b")),
+    (4, 29, 38, dict(kind="CBCONV", kernelH=5, kernelW=3, padH=2, padW=1, outChannels=64, threshold=0.0, fuseRelu=True, weightsFile="b")),
+    (2, 21, 30, dict(kind="CONV", kernelH=1, kernelW=1, outChannels=48, weightsFile="b")),
+]
+
+
+@pytest.mark.parametrize("R", ["1", "2", "4"])
+@pytest.mark.parametrize("maxctas", [None, "2"])
+@pytest.mark.parametrize("magnitude", ["unit", "subnormal"])
+@pytest.mark.parametrize("cin,h,w,layer", MPR_CASES)
+def test_mpr_f16_layer_vs_exact(gpu, orc, monkeypatch, cin, h, w, layer, magnitude, maxctas, R):
+    """The multi-pixel-row conv against the exact oracle under the fp16
+    operand bound, full frames and change-based frames (tau = 0) alike;
+    R = CBX_MPR_R (pixels per tensor-core row, clamped to N <= 256), maxctas
+    caps the persistent grid so every CTA walks several tiles."""
+    monkeypatch.setenv("CBX_MPR_R", R)
+    monkeypatch.setenv("CBX_MPR_F16", "1")  # (opt-in for fp32-input layers)
+    if maxctas:
+        monkeypatch.setenv("CBX_TC_MAXCTAS", maxctas)
+    spec = two_layer(cin, h, w, layer)
+    wts = orc.generate_weights(spec, 17)
+    if magnitude == "subnormal":
+        K0, b0 = wts[0]
+        wts[0] = ((K0 * 4e-5).astype(np.float32), (b0 * 4e-5).astype(np.float32))
+    onet = orc.load_network(spec, wts)
+    net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="f16")
+    assert net.layer_operands(1) == "f16"
+    cfg = dict(channels=3, height=h, width=w, sprites=[(5, 2, 0.9)], noise=0.02, seed=5)
+    _check_layer(gpu, orc, net, onet, spec, wts, cfg, 1, cin, True, frames=4)
+    if layer["kind"] == "CBCONV":  # change-based frames ran: the update lists were group lists
+        d, u = net.trace(0)
+        _, ou = onet.trace(0)
+        assert np.array_equal(u, ou)
