@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--ref-budget", type=float, default=60.0, help="seconds for --impl reference timing")
     ap.add_argument("--no-cudnn", action="store_true", help="skip the torch/cuDNN dense cross-check")
     ap.add_argument("--sweep", action="store_true", help="also report fps at every recipe")
+    ap.add_argument("--quick", action="store_true", help="tuning: time the change-based step only, print one line")
     return ap.parse_args()
 
 
@@ -449,6 +450,11 @@ def run_gpu_arm(args):
     clk["note"] = "sampled every 100 ms across warm-up, the timed region and a 0.5 s continuation of the same step"
     value = shard.aggregate_rate(ws, S * K, ms)
     log(f"[gpu] cbinfer: {ms / K:.3f} ms/step, {value:.1f} frames/s, {launches} kernels/frame")
+    if args.quick:
+        if rank == 0:
+            print(json.dumps({"quick": True, "value": value, "ms_per_step": ms / K, "streams": S,
+                              "lanes": net.num_lanes(), "clocks": clk}), flush=True)
+        return
 
     # changed fractions of exactly the timed frames: replay the clip from reset
     # (untimed, per-step readback)

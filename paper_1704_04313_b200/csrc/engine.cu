@@ -22,6 +22,7 @@
 //
 // First frame after reset and the Baseline engine run the same kernels in
 // "full" mode: no masks, every output pixel evaluated.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -487,7 +488,6 @@ void Engine::build_plan(Plan& p, bool baseline) {
             continue;
         }
         p.idx[k] = p.alloc<int32_t>((size_t)S * Ho * Wo);
-        p.cnt[k] = p.alloc<int>(1);
         const int wpr = (Wo + 31) / 32;
         ws_bytes[k] = round_up(dilate_compact_workspace(BitMask{nullptr, Ho, Wo, wpr, round_up((int64_t)Ho * wpr, 2048)}, S), 256);
         // strided geometries dilate separately, then compact the dilated mask
@@ -522,7 +522,12 @@ void Engine::build_plan(Plan& p, bool baseline) {
     p.ws_k.assign(nl, nullptr);
     p.wcount_k.assign(nl, nullptr);
     for (int k = 0; k < nl; ++k) {
-        if (ws_bytes[k]) p.ws_k[k] = p.scratch + ws_off[k];
+        if (ws_bytes[k]) {
+            p.ws_k[k] = p.scratch + ws_off[k];
+            // the compaction's list counter lives in the frame scratch: zeroed
+            // by the frame's one memset, incremented by the compaction blocks
+            p.cnt[k] = reinterpret_cast<int*>(p.ws_k[k]);
+        }
         if (wc_off[k]) p.wcount_k[k] = reinterpret_cast<int*>(p.scratch + wc_off[k]);
     }
 }
@@ -1228,6 +1233,9 @@ void Engine::get_trace(int cb, int s, uint8_t* detected, int32_t* updated, int64
     CBX_CUDA(cudaMemcpy(&total, p.cnt[k], sizeof(int), cudaMemcpyDeviceToHost));
     std::vector<int32_t> all(total);
     if (total) CBX_CUDA(cudaMemcpy(all.data(), p.idx[k], sizeof(int32_t) * total, cudaMemcpyDeviceToHost));
+    // (the compaction writes each tile's ascending run where its atomic
+    // landed: sort for the reference's extract_indexes order)
+    std::sort(all.begin(), all.end(), [](int32_t a, int32_t b) { return (uint32_t)a < (uint32_t)b; });
     const int R = list_group(k, hist_u8_);
     const int Wo = dims_[6 * k + 5], Gw = (Wo + R - 1) / R;
     const int64_t Ng = (int64_t)dims_[6 * k + 4] * Gw;

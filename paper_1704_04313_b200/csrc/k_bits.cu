@@ -15,6 +15,9 @@
 //                         layer's change detection
 //   classify_bits      <- argmax_classify  baseline.cpp:147-163
 #include <cuda_fp16.h>
+
+#include <stdexcept>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -383,38 +386,6 @@ __device__ __forceinline__ int block_scan(int my, int* s_warp, int& total) {
     return (warp ? s_warp[warp - 1] : 0) + incl - my;
 }
 
-// Decoupled look-back by warp 0; returns the exclusive global prefix of `tile`.
-__device__ __forceinline__ long long lookback(unsigned long long* status, unsigned tile, int agg) {
-    const int lane = threadIdx.x & 31;
-    long long base = 0;
-    if (tile == 0) {
-        if (lane == 0) atomicExch(status, kFlagPre | (unsigned long long)agg);
-        return 0;
-    }
-    if (lane == 0) atomicExch(status + tile, kFlagAgg | (unsigned long long)agg);
-    long long pos = (long long)tile - 1;
-    while (true) {
-        const long long j = pos - lane;
-        unsigned long long st = kFlagPre;
-        if (j >= 0) {
-            do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(st) : "l"(status + j) : "memory");
-            } while ((st >> 62) == 0);
-        }
-        const unsigned pre = __ballot_sync(0xffffffffu, (st >> 62) == 2);
-        const int stop = pre ? __ffs(pre) - 1 : 32;
-        long long val = (lane <= stop) ? (long long)(st & kValMask) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        base += val;
-        if (pre) break;
-        pos -= 32;
-    }
-    if (lane == 0) atomicExch(status + tile, kFlagPre | (unsigned long long)(base + agg));
-    return base;
-}
-
-
 // OR over a horizontal window: output bit x of the word = OR of input bits
 // x + t, t in [-pw, kw - 1 - pw], with the neighbouring words supplying the
 // bits that cross the word boundary (64-bit doubling: ~log2(kw) shift/or).
@@ -476,14 +447,11 @@ template <int WPT, int R>
 __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, BitMask out, bool write_out,
                                                                     int kh, int kw, int ph, int pw, bool identity,
                                                                     int32_t* __restrict__ idx, int* total,
-                                                                    unsigned long long* status,
                                                                     unsigned long long* cnt, int cstride) {
     extern __shared__ uint4 s_rows4[];
     uint32_t* s_rows = reinterpret_cast<uint32_t*>(s_rows4);
     __shared__ int s_warp[kDcThreads / 32];
     __shared__ long long s_base;
-    // Tile = block index: blocks are dispatched in index order, so every
-    // predecessor a tile waits on in the look-back is already resident.
     const unsigned tile = blockIdx.x;
     constexpr int kTile = kDcThreads * WPT;
     const int tps = (int)(out.stride / kTile);
@@ -561,15 +529,16 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
         const int wpx = __reduce_add_sync(0xffffffffu, mypx);
         if ((threadIdx.x & 31) == 0 && wpx) atomicAdd(cnt + (int64_t)s * cstride, (unsigned long long)wpx);
     }
+    // The block's entries go to a range claimed with ONE atomic on the list
+    // counter (zeroed by the frame's scratch memset): no tile waits for
+    // another (a decoupled look-back chains the tiles through ~tiles/32 L2
+    // round trips). Entries are ascending within a tile and the tiles land in
+    // completion order -- the convolutions do not depend on the order (every
+    // output pixel is computed from its own receptive field), traces are
+    // sorted when read back (extract_indexes order, cbconv.cpp:99-113).
     int agg;
     const int excl = block_scan(my, s_warp, agg);
-    if (threadIdx.x < 32) {
-        const long long b = lookback(status, tile, agg);
-        if (threadIdx.x == 0) {
-            s_base = b;
-            if (tile == gridDim.x - 1) *total = (int)(b + agg);  // the last tile holds the inclusive total
-        }
-    }
+    if (threadIdx.x == 0) s_base = agg ? atomicAdd(total, agg) : 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     int64_t o = s_base + excl;  // this thread's first entry
@@ -609,50 +578,50 @@ static size_t dc_smem_bytes(const BitMask& in, const BitMask& out, int kh, int w
 }
 
 size_t dilate_compact_workspace(const BitMask& out, int S) {
-    const int64_t tiles = (int64_t)S * (out.stride / kDcThreads);  // WPT = 1 upper bound
-    return (size_t)round_up(tiles * 8 + 16, 256);
+    (void)out;
+    (void)S;
+    return 256;  // the list counter (the kernel's `total`)
 }
 
 template <int WPT, int R>
 static void launch_dc_r(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw, bool identity,
-                        int32_t* idx, int* total, unsigned long long* status, unsigned long long* cnt, int cstride,
-                        cudaStream_t st) {
+                        int32_t* idx, int* total, unsigned long long* cnt, int cstride, cudaStream_t st) {
     const int64_t tiles = (int64_t)S * (out.stride / (kDcThreads * WPT));
     const size_t smem = dc_smem_bytes(in, out, identity ? 1 : kh, WPT);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(dilate_compact_kernel<WPT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dilate_compact_kernel<WPT, R><<<(unsigned)tiles, kDcThreads, smem, st>>>(in, out, write_out, kh, kw, ph, pw,
-                                                                             identity, idx, total, status, cnt, cstride);
+                                                                             identity, idx, total, cnt, cstride);
 }
 
 template <int WPT>
 static void launch_dc(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw, bool identity,
-                      int32_t* idx, int* total, unsigned long long* status, unsigned long long* cnt, int cstride,
-                      cudaStream_t st, int R) {
+                      int32_t* idx, int* total, unsigned long long* cnt, int cstride, cudaStream_t st, int R) {
     if (R == 4)
-        launch_dc_r<WPT, 4>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st);
+        launch_dc_r<WPT, 4>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, cnt, cstride, st);
     else if (R == 2)
-        launch_dc_r<WPT, 2>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st);
+        launch_dc_r<WPT, 2>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, cnt, cstride, st);
     else
-        launch_dc_r<WPT, 1>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st);
+        launch_dc_r<WPT, 1>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, cnt, cstride, st);
 }
 
 void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int kh, int kw, int ph, int pw,
                            int32_t* idx, int* total, void* workspace, unsigned long long* cnt, int cstride,
                            cudaStream_t st, bool ws_zeroed, int R) {
-    unsigned long long* status = reinterpret_cast<unsigned long long*>(workspace);
+    (void)workspace;  // (the counter `total` must be zero: ws_zeroed means the caller zeroed it in-stream)
     const bool identity = kh == 1 && kw == 1 && ph == 0 && pw == 0;
     const int64_t words = (int64_t)S * out.stride;
     // enough tiles to cover the SMs twice, at most 8 words per thread
     int wpt = 8;
     while (wpt > 1 && words / (kDcThreads * wpt) < 2 * kNumSMs) wpt /= 2;
     const int64_t tiles = words / (kDcThreads * wpt);
-    if (!ws_zeroed) cudaMemsetAsync(workspace, 0, tiles * 8 + 16, st);
+    if (!ws_zeroed) cudaMemsetAsync(total, 0, sizeof(int), st);
+    (void)tiles;
     switch (wpt) {
-        case 8: launch_dc<8>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st, R); break;
-        case 4: launch_dc<4>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st, R); break;
-        case 2: launch_dc<2>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st, R); break;
-        default: launch_dc<1>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, status, cnt, cstride, st, R); break;
+        case 8: launch_dc<8>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, cnt, cstride, st, R); break;
+        case 4: launch_dc<4>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, cnt, cstride, st, R); break;
+        case 2: launch_dc<2>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, cnt, cstride, st, R); break;
+        default: launch_dc<1>(in, out, write_out, S, kh, kw, ph, pw, identity, idx, total, cnt, cstride, st, R); break;
     }
 }
 
@@ -756,20 +725,22 @@ __device__ __forceinline__ uint32_t touched_word(const PointBitsArgs& a, int s, 
     return tw;
 }
 
-__global__ void __launch_bounds__(kPtThreads) point_scan_kernel(PointBitsArgs a) {
+// (index arithmetic: every count here is below 2^31 -- launch_point_bits
+// checks -- so divisions are multiply-shifts, FastDiv)
+__global__ void __launch_bounds__(kPtThreads) point_scan_kernel(PointBitsArgs a, FastDiv fd_plane, FastDiv fd_wpr) {
     const int Ho = a.out.H, Wo = a.out.W;
     const int wpr = (Wo + 31) / 32;
-    const int64_t nseg = (int64_t)a.S * Ho * wpr;
+    const int nseg = a.S * Ho * wpr;
     const int lane = threadIdx.x & 31;
-    for (int64_t base = (int64_t)blockIdx.x * kPtThreads; base < nseg; base += (int64_t)gridDim.x * kPtThreads) {
-        const int64_t seg = base + threadIdx.x;
+    for (int base = blockIdx.x * kPtThreads; base < nseg; base += gridDim.x * kPtThreads) {
+        const int seg = base + threadIdx.x;
         uint32_t tw = 0;
         int s = 0, y = 0, w = 0;
         if (seg < nseg) {
-            s = (int)(seg / ((int64_t)Ho * wpr));
-            const int64_t r = seg - (int64_t)s * Ho * wpr;
-            y = (int)(r / wpr);
-            w = (int)(r - (int64_t)y * wpr);
+            s = (int)fd_plane.div((uint32_t)seg);
+            const int r = seg - s * Ho * wpr;
+            y = (int)fd_wpr.div((uint32_t)r);
+            w = r - y * wpr;
             tw = touched_word(a, s, y, w);
             const int64_t wo = (int64_t)y * wpr + w;
             if (a.U_out.d) a.U_out.d[(int64_t)s * a.U_out.stride + wo] = tw;
@@ -799,28 +770,29 @@ __global__ void __launch_bounds__(kPtThreads) point_scan_kernel(PointBitsArgs a)
 }
 
 template <bool FULL>
-__global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a) {
+__global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a, FastDiv fd_c4, FastDiv fd_howo,
+                                                                FastDiv fd_wo) {
     const int Ho = a.out.H, Wo = a.out.W;
     const int wpr = (Wo + 31) / 32;
     const int c4n = a.in.Cp / 4;
-    const int64_t HoWo = (int64_t)Ho * Wo;
-    const int64_t npix = FULL ? (int64_t)a.S * HoWo : (int64_t)*a.work_count;
-    const int64_t items = npix * c4n;
+    const int HoWo = Ho * Wo;
+    const int npix = FULL ? a.S * HoWo : *a.work_count;
+    const int items = npix * c4n;
     const int rowq = a.in.Wp * c4n;
     const int lane = threadIdx.x & 31;
-    for (int64_t base = (int64_t)blockIdx.x * kPtThreads; base < items; base += (int64_t)gridDim.x * kPtThreads) {
-        const int64_t it = base + threadIdx.x;
+    for (int base = blockIdx.x * kPtThreads; base < items; base += gridDim.x * kPtThreads) {
+        const int it = base + threadIdx.x;
         const bool act = it < items;
         bool ch = false;
         uint32_t* waddr = nullptr;
         int s = 0, x = 0;
         if (act) {
-            const int64_t pi = it / c4n;
-            const int c4 = (int)(it - pi * c4n);
-            const int64_t g = FULL ? pi : (int64_t)__ldg(a.work + pi);
-            s = (int)(g / HoWo);
-            const int p = (int)(g - (int64_t)s * HoWo);
-            const int y = p / Wo;
+            const int pi = (int)fd_c4.div((uint32_t)it);
+            const int c4 = it - pi * c4n;
+            const uint32_t g = FULL ? (uint32_t)pi : __ldg(a.work + pi);
+            s = (int)fd_howo.div(g);
+            const int p = (int)(g - (uint32_t)s * (uint32_t)HoWo);
+            const int y = (int)fd_wo.div((uint32_t)p);
             x = p - y * Wo;
             const float4* src = reinterpret_cast<const float4*>(
                 a.in.d + (int64_t)s * a.in.ss + ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
@@ -882,16 +854,21 @@ void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
     const int wpr = (a.out.W + 31) / 32;
     const int64_t nseg = (int64_t)a.S * a.out.H * wpr;
     const int c4n = a.in.Cp / 4;
+    if ((int64_t)a.S * a.out.H * a.out.W * c4n >= ((int64_t)1 << 31) || nseg * 32 >= ((int64_t)1 << 31))
+        throw std::runtime_error("pooling: more than 2^31 items per frame");
+    const FastDiv fd_c4 = FastDiv::make((uint32_t)c4n), fd_howo = FastDiv::make((uint32_t)(a.out.H * a.out.W)),
+                  fd_wo = FastDiv::make((uint32_t)a.out.W), fd_plane = FastDiv::make((uint32_t)(a.out.H * wpr)),
+                  fd_wpr = FastDiv::make((uint32_t)wpr);
     if (!a.upd_in.d) {  // full frame: every pixel, no change test (the next layer evaluates in full)
         const int64_t items = (int64_t)a.S * a.out.H * a.out.W * c4n;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + kPtThreads - 1) / kPtThreads, (int64_t)kNumSMs * 16));
-        point_work_kernel<true><<<grid, kPtThreads, 0, st>>>(a);
+        point_work_kernel<true><<<grid, kPtThreads, 0, st>>>(a, fd_c4, fd_howo, fd_wo);
         return;
     }
     if (!a.count_zeroed) cudaMemsetAsync(a.work_count, 0, sizeof(int), st);
     const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>((nseg + kPtThreads - 1) / kPtThreads, (int64_t)kNumSMs * 8));
-    point_scan_kernel<<<g1, kPtThreads, 0, st>>>(a);
-    point_work_kernel<false><<<kNumSMs * 8, kPtThreads, 0, st>>>(a);
+    point_scan_kernel<<<g1, kPtThreads, 0, st>>>(a, fd_plane, fd_wpr);
+    point_work_kernel<false><<<kNumSMs * 8, kPtThreads, 0, st>>>(a, fd_c4, fd_howo, fd_wo);
 }
 
 // ---------------------------------------------------------------------------
