@@ -34,6 +34,7 @@
 // tensor keeps its previous value there, like the reference's update_output).
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -51,8 +52,9 @@ namespace {
 using namespace tc;
 
 constexpr int kABytes = kTileM * 128;
-constexpr int kEpi = 128, kProd = 128;
+constexpr int kEpi = 128, kProd = 256;  // 8 producer warps: thread = (tile row, half of its granules)
 constexpr int kThreads = kEpi + kProd + 32;
+constexpr int kMmaWarp = (kEpi + kProd) / 32;
 constexpr int kMaxSmem = 232448;
 constexpr int kMaxGran = 64;  // granule table entries (8 K-blocks)
 
@@ -121,7 +123,7 @@ __device__ __forceinline__ void group_of(const MprArgs& a, uint32_t gid, int& s,
 }
 
 template <int MODE, int R>
-__global__ void __launch_bounds__(kThreads, 2) conv_mpr_kernel(MprArgs a) {
+__global__ void __launch_bounds__(kThreads, MODE == 0 ? 2 : 1) conv_mpr_kernel(MprArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int NS = a.stages;
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 2) conv_mpr_kernel(MprArgs a) {
         mbar_init(bready, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sTmem)),
                      "r"(a.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -207,64 +209,98 @@ __global__ void __launch_bounds__(kThreads, 2) conv_mpr_kernel(MprArgs a) {
         return ((int64_t)gid << 4) | m;
     };
 
-    if (warp >= 4 && warp < 8) {
-        // ================= producers: thread = tile row =================
-        const int r = tid - kEpi;
+    if (warp >= 4 && warp < kMmaWarp) {
+        // ================= producers =================
+        // thread = (tile row r, half hf): granules 4hf .. 4hf+3 of every
+        // K-block of row r. Software-pipelined two deep: the loads of the
+        // next K-block (or of the next tile's first) are in flight while
+        // this one is converted and stored, so a producer keeps up to two
+        // K-blocks of gathers outstanding (register staging has no cp.async
+        // to run ahead with).
+        const int pt = tid - kEpi;
+        const int r = pt & (kTileM - 1), hf = pt >> 7;
         const uint32_t swz = (uint32_t)(r & 7);
-        RingPos rg;
-        int64_t enext = entry(tile_first, r);
-        for (int64_t tile = tile_first; tile < ntiles; tile += tile_step) {
-            const int64_t e = enext;
-            enext = entry(tile + tile_step, r);
-            const bool valid = e >= 0;
-            int64_t base = 0;  // input units of the window origin
-            if (valid) {
-                int s, y, x0;
-                group_of<R>(a, (uint32_t)(e >> 4), s, y, x0);
-                base = (int64_t)s * a.in_ss +
-                       ((int64_t)(y - a.ph + a.in_hh) * a.in_Wp + (x0 + a.win0 + a.in_hw)) * a.in_Cp;
-            }
-            for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
-                const uint32_t st = rg.st, ph = rg.ph;
-                uint4 g[8];
+        using Raw = typename std::conditional<MODE == 0, uint4[4], float4[4][2]>::type;
+        auto issue = [&](int64_t base, bool valid, int kb, Raw& raw) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int2 t = sGran[kb * 8 + 4 * hf + q];
                 if constexpr (MODE == 0) {
                     const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.in) + base);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int2 t = sGran[kb * 8 + j];
-                        g[j] = (valid && t.y) ? __ldg(src + (t.x >> 2)) : make_uint4(0u, 0u, 0u, 0u);
-                    }
+                    raw[q] = (valid && t.y) ? __ldg(src + (t.x >> 2)) : make_uint4(0u, 0u, 0u, 0u);
                 } else {
                     const float* src = reinterpret_cast<const float*>(a.in) + base;
-                    float4 v[8][2];
+                    raw[q][0] = (valid && t.y > 0) ? __ldg(reinterpret_cast<const float4*>(src + t.x))
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                    raw[q][1] = (valid && t.y > 1) ? __ldg(reinterpret_cast<const float4*>(src + t.x + a.in_Cp))
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+        };
+        auto row_base = [&](int64_t e, int64_t& base) -> bool {
+            if (e < 0) return false;
+            int s, y, x0;
+            group_of<R>(a, (uint32_t)(e >> 4), s, y, x0);
+            base = (int64_t)s * a.in_ss + ((int64_t)(y - a.ph + a.in_hh) * a.in_Wp + (x0 + a.win0 + a.in_hw)) * a.in_Cp;
+            return true;
+        };
+        RingPos rg;
+        int64_t tile = tile_first;
+        int64_t base = 0, nbase = 0;
+        bool valid = tile < ntiles && row_base(entry(tile, r), base);
+        int64_t enext = entry(tile + tile_step, r);
+        Raw cur, nxt;
+        if (tile < ntiles) issue(base, valid, 0, cur);
+        while (tile < ntiles) {
+            for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
+                // prefetch: the next K-block, or the next tile's first
+                const bool last = kb + 1 == a.NKB;
+                if (!last) {
+                    issue(base, valid, kb + 1, nxt);
+                } else if (tile + tile_step < ntiles) {
+                    const bool nv = row_base(enext, nbase);
+                    issue(nbase, nv, 0, nxt);
+                }
+                uint4 g[4];
+                if constexpr (MODE == 0) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int2 t = sGran[kb * 8 + j];
-                        v[j][0] = (valid && t.y > 0) ? __ldg(reinterpret_cast<const float4*>(src + t.x)) : make_float4(0.f, 0.f, 0.f, 0.f);
-                        v[j][1] = (valid && t.y > 1) ? __ldg(reinterpret_cast<const float4*>(src + t.x + a.in_Cp))
-                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
+                    for (int q = 0; q < 4; ++q) g[q] = cur[q];
+                } else {
                     bool big = false;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
+                    for (int q = 0; q < 4; ++q) {
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
-                            big |= fabsf(v[j][h].x) > 65504.0f || fabsf(v[j][h].y) > 65504.0f ||
-                                   fabsf(v[j][h].z) > 65504.0f || fabsf(v[j][h].w) > 65504.0f;
-                        g[j] = make_uint4(pack_f16x2(v[j][0].x, v[j][0].y), pack_f16x2(v[j][0].z, v[j][0].w),
-                                          pack_f16x2(v[j][1].x, v[j][1].y), pack_f16x2(v[j][1].z, v[j][1].w));
+                            big |= fabsf(cur[q][h].x) > 65504.0f || fabsf(cur[q][h].y) > 65504.0f ||
+                                   fabsf(cur[q][h].z) > 65504.0f || fabsf(cur[q][h].w) > 65504.0f;
+                        g[q] = make_uint4(pack_f16x2(cur[q][0].x, cur[q][0].y), pack_f16x2(cur[q][0].z, cur[q][0].w),
+                                          pack_f16x2(cur[q][1].x, cur[q][1].y), pack_f16x2(cur[q][1].z, cur[q][1].w));
                     }
                     if (big && a.ovf) atomicOr(a.ovf, 1);
                 }
+                const uint32_t st = rg.st, ph = rg.ph;
                 mbar_wait(&empty[st], ph ^ 1u);
                 uint4* row = reinterpret_cast<uint4*>(sA + (size_t)st * kABytes + r * 128);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) row[j ^ swz] = g[j];
+                for (int q = 0; q < 4; ++q) row[(4 * hf + q) ^ swz] = g[q];
                 fence_proxy_async();
                 mbar_arrive(&full[st]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if constexpr (MODE == 0) {
+                        cur[q] = nxt[q];
+                    } else {
+                        cur[q][0] = nxt[q][0];
+                        cur[q][1] = nxt[q][1];
+                    }
+                }
             }
+            tile += tile_step;
+            base = nbase;
+            valid = tile < ntiles && enext >= 0;
+            enext = entry(tile + tile_step, r);
         }
-    } else if (warp == 8) {
+    } else if (warp == kMmaWarp) {
         // ================= MMA issuer =================
         const uint32_t id = MODE == 0 ? idesc_i8(a.Npad) : idesc_f16(a.Npad);
         const uint64_t a_desc0 = smem_desc(smem_u32(sA)), b_desc0 = smem_desc(smem_u32(sB));
@@ -424,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 2) conv_mpr_kernel(MprArgs a) {
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols));
     }
@@ -498,7 +534,7 @@ std::unique_ptr<MprLayer, MprLayerDeleter> make_mpr_layer(const cbx_geom& g, int
     const size_t fixed = 1024 + b_bytes + kMaxGran * 8 + 2 * round_up(g.outChannels, 4) * 4 + 16 + 8 * (2 * 16 + 5) + 16;
     // CTAs per SM: two when the filters and a few stages fit twice (more
     // independent producers in flight), else one; CBX_MPR_CTAS overrides (tuning)
-    t->ctas_per_sm = fixed + 4 * (size_t)kABytes <= (size_t)kMaxSmem / 2 - 1024 ? 2 : 1;
+    t->ctas_per_sm = mode == 0 && fixed + 4 * (size_t)kABytes <= (size_t)kMaxSmem / 2 - 1024 ? 2 : 1;
     if (const char* e = std::getenv("CBX_MPR_CTAS")) t->ctas_per_sm = std::max(1, std::min(2, std::atoi(e)));
     const size_t budget = t->ctas_per_sm == 2 ? (size_t)kMaxSmem / 2 - 1024 : (size_t)kMaxSmem;
     int ns = 8;
@@ -514,11 +550,14 @@ std::unique_ptr<MprLayer, MprLayerDeleter> make_mpr_layer(const cbx_geom& g, int
         if (R == 4) set_attr<1, 4>(); else if (R == 2) set_attr<1, 2>(); else set_attr<1, 1>();
     }
     CBX_CUDA(cudaMalloc(&t->Bw, b_bytes));
-    CBX_CUDA(cudaMemset(t->Bw, 0, b_bytes));
+    CBX_CUDA(cudaMemset(t->Bw, 0, b_bytes));  // (legacy stream: synchronized below)
     if (mode == 0) {
         CBX_CUDA(cudaMalloc(&t->qsc, sizeof(float) * g.outChannels));
         CBX_CUDA(cudaMemset(t->qsc, 0, sizeof(float) * g.outChannels));
     }
+    // the zeroing ran on the legacy default stream; the weight uploads run
+    // on the engine's non-blocking stream, which is not ordered after it
+    CBX_CUDA(cudaStreamSynchronize(nullptr));
     return t;
 }
 

@@ -142,6 +142,7 @@ struct TcArgs {
     // next tile's MMAs wait only for the shared columns to be drained
     int ovl, ovl_s, ovl_b0, ovl_b1;
     int tap4x7;  // row-lane gather specialised for Cp = 4, 7x7 (NKB = 7)
+    int xrow;    // row-lane gather of 4-channel inputs as 8 rows x 4 chunks per warp instruction
     // kind::i8 (8-bit camera path, layer 1): A = RGBX bytes of the frame, one
     // 4-byte chunk per tap (32 taps per K-block); B = the filters as three
     // signed base-256 digits per weight, digit q of channel j in accumulator
@@ -393,6 +394,64 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 }
             }
         } else if constexpr (ROWLANE) {
+          if (a.xrow) {
+            // 4-channel input (one 16-byte chunk per tap), shared-memory
+            // conflict-free: a warp instruction copies 8 tile rows x 4
+            // consecutive chunks -- the 8 rows' swizzled positions
+            // (j ^ (r & 7)) are distinct, so its 32 x 16 bytes land in 4
+            // wavefronts (thread-per-row LDGSTS hit 8 bank groups 4 ways:
+            // 16 wavefronts, and the L2 conv was bound by it). Lane l: rows
+            // 32w + 8i + (l & 7), i < 4; chunks 4h + (l >> 3), h < 2.
+            const int pw = warp - 4, e = lane >> 3, rl = lane & 7;
+            Ring rg;
+            auto load_rows = [&](int64_t t, int64_t (&gr)[4]) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int64_t n = t * kRowsPerTile + row_off + 32 * pw + 8 * i + rl;
+                    gr[i] = (t < ntiles && n < total) ? (a.idx ? (int64_t)__ldg(a.idx + n) : n) : -1;
+                }
+            };
+            int64_t gnext4[4];
+            load_rows(tile_first, gnext4);
+            for (int64_t tile = tile_first; tile < ntiles; tile += tile_step) {
+                const float* base[4];
+                uint32_t vmask = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    base[i] = a.in;
+                    if (gnext4[i] >= 0) {
+                        int s, p, y, x;
+                        pixel_of(a, gnext4[i], HoWo, s, p, y, x);
+                        vmask |= 1u << i;
+                        base[i] = a.in + (int64_t)s * a.in_ss +
+                                  ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
+                    }
+                }
+                load_rows(tile + tile_step, gnext4);
+                for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
+                    const uint32_t st = rg.st, ph = rg.ph;
+                    mbar_wait(&empty[st], ph ^ 1u);
+                    if (pw == 0 && lane == 0) {
+                        mbar_arrive_expect_tx(&full[st], b_bytes);
+                        bulk_g2s(sB + (size_t)st * b_bytes, Bw + (size_t)kb * a.Brows * kKBlock, b_bytes, &full[st]);
+                    }
+                    const uint32_t stage = smem_u32(sA + (size_t)st * kABytes);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int j = 4 * h + e;
+                        const int off = sTab[kb * kChunksPerKB + j];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int r = 32 * pw + 8 * i + rl;
+                            if ((vmask >> i) & 1u)
+                                cp_async16(stage + r * 128 + ((j ^ rl) << 4), off >= 0 ? base[i] + off : a.in,
+                                           off >= 0 ? 16u : 0u);
+                        }
+                    }
+                    cp_async_arrive_noinc(&full[st]);
+                }
+            }
+          } else {
             const int r = tid - kEpiThreads;
             const uint32_t swz = (uint32_t)(r & 7);
             Ring rg;
@@ -468,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                     cp_async_arrive_noinc(&full[st]);
                 }
             }
+          }
         } else {
         // Thread pt copies chunk j = pt % 8 of rows rsub + 16*i (i < 8), so the
         // 8 lanes of a row fetch its 128 contiguous-ish bytes together and a
@@ -860,6 +920,7 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
         CBX_CUDA(cudaMemset(t->Bw, 0, (size_t)t->NKB * b_bytes));
         CBX_CUDA(cudaMalloc(&t->qsc, sizeof(float) * g.outChannels));
         CBX_CUDA(cudaMemset(t->qsc, 0, sizeof(float) * g.outChannels));
+        CBX_CUDA(cudaStreamSynchronize(nullptr));  // (legacy-stream memsets before the non-blocking uploads)
         return t;
     }
     // fp16 operands: 8 channels per 16-byte chunk; Cp stays in 4-byte units so
@@ -935,6 +996,8 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     // CBX_TC_MAXCTAS caps the persistent grid (tuning: SMs left free for the
     // other lane's kernels; tests: many tiles per CTA on small frames)
     if (const char* e = std::getenv("CBX_TC_MAXCTAS")) t->max_ctas = std::max(1, std::atoi(e));
+    if (t->Npad > 256)  // (tuning: SMs left to the other lane's kernels while the wide layer runs)
+        if (const char* e = std::getenv("CBX_TC_MAXCTAS_WIDE")) t->max_ctas = std::max(1, std::atoi(e));
     t->smem = fixed + (size_t)ns * (kABytes + b_bytes);
     set_smem_attrs<0, false>();
     set_smem_attrs<8, false>();
@@ -961,6 +1024,7 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     }
     CBX_CUDA(cudaMalloc(&t->Bw, (size_t)t->NKB * b_bytes * (t->pair ? 2 : 1)));
     CBX_CUDA(cudaMemset(t->Bw, 0, (size_t)t->NKB * b_bytes * (t->pair ? 2 : 1)));
+    CBX_CUDA(cudaStreamSynchronize(nullptr));  // (legacy-stream memset before the non-blocking uploads)
     return t;
 }
 
@@ -1132,6 +1196,8 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     }
     static const bool no_tap4x7 = std::getenv("CBX_TC_NO_TAP4X7") != nullptr;  // (tuning)
     a.tap4x7 = !no_tap4x7 && in.Cp == 4 && t.g.kernelH == 7 && t.g.kernelW == 7 && t.NKB == 7;
+    static const bool no_xrow = std::getenv("CBX_TC_NO_XROW") != nullptr;  // (tuning)
+    a.xrow = !no_xrow && in.Cp == 4 && !t.f16 && !t.pair;
     a.ovl_s = t.ovl_s;
     a.ovl_b0 = t.ovl_b0;
     a.ovl_b1 = t.ovl_b1;

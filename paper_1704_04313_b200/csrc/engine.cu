@@ -61,7 +61,11 @@ template <class T>
 T* dmalloc(size_t n) {
     void* p = nullptr;
     CBX_CUDA(cudaMalloc(&p, n * sizeof(T) + 16));
+    // cudaMemset runs on the legacy default stream, which the engine's
+    // non-blocking streams do not order against: wait for it, or a later
+    // copy into the buffer (a lazily allocated staging slot) can be zeroed
     CBX_CUDA(cudaMemset(p, 0, n * sizeof(T) + 16));
+    CBX_CUDA(cudaStreamSynchronize(nullptr));
     return static_cast<T*>(p);
 }
 
@@ -160,6 +164,8 @@ struct Engine::Plan {
     bool dirty = true;
     int fused_from = -1;            // conv layer whose epilogue runs the per-pixel tail (-1: none)
     uint32_t* work = nullptr;       // touched-pixel list shared by the MAXPOOL/RELU layers
+    TensorView rgbx_tv{};           // 8-bit path: RGBX copy of this plan's last frame (layer-1 input)
+    Rgbx8View rgbx{};
     int* ovf = nullptr;             // fp16 shadow overflow flag (sticky until a full frame)
     // Frame scratch zeroed by ONE memset at the start of a steady frame:
     // stats counters, each compaction's look-back status words, each
@@ -268,19 +274,6 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
         const uint8_t** t8 = dmalloc<const uint8_t*>(2 * (size_t)S);
         d_cur8_ = t8;
         d_prev8_ = t8 + S;
-        TensorView v{};
-        v.C = net.inputChannels;
-        v.H = net.inputHeight;
-        v.W = net.inputWidth;
-        v.Cp = 1;
-        v.hh = g.padH;
-        v.hw = (int)round_up(g.padW, 4);
-        v.Hp = v.H + 2 * v.hh;
-        v.Wp = v.W + 2 * v.hw;
-        v.ss = round_up((int64_t)v.Hp * v.Wp, 64);
-        v.d = dmalloc<float>((size_t)(v.ss * S) + 2 * (size_t)v.Wp + 64);  // zero halo, never written (+ window slack)
-        rgbx_tv_ = v;
-        rgbx_ = Rgbx8View{reinterpret_cast<uint32_t*>(v.d), v.ss, v.Wp, v.hh, v.hw};
     }
     const size_t frame = (size_t)net.inputChannels * net.inputHeight * net.inputWidth * S;
     for (auto& s : slots_) s = dmalloc<float>(frame);
@@ -308,7 +301,6 @@ Engine::~Engine() {
     mpr8_.reset();
     mpr_.clear();
     if (d_cur8_) cudaFree(d_cur8_);
-    if (rgbx_tv_.d) cudaFree(rgbx_tv_.d);
     if (prev_dec_) cudaFree(prev_dec_);
     for (auto& s : slots8_)
         if (s) cudaFree(s);
@@ -420,6 +412,27 @@ void Engine::build_plan(Plan& p, bool baseline) {
         int c, h, w;
         tensor_dims(0, c, h, w);
         p.T[0] = TensorView{nullptr, c, h, w, c, h, w, 0, 0, (int64_t)c * h * w};
+    }
+    if (tc8_) {
+        // RGBX copy of the 8-bit frame for the kind::i8 layer 1 (zero halo,
+        // never written; + slack for the last row's gather window). One per
+        // plan: a change-based frame rewrites only the pixel groups whose
+        // bytes differ from the previous frame, so the buffer must hold the
+        // change-based engine's previous frame (the dense engine has its own).
+        const cbx_geom& g = layers_[0].geom;
+        TensorView v{};
+        v.C = net_.inputChannels;
+        v.H = net_.inputHeight;
+        v.W = net_.inputWidth;
+        v.Cp = 1;
+        v.hh = g.padH;
+        v.hw = (int)round_up(g.padW, 4);
+        v.Hp = v.H + 2 * v.hh;
+        v.Wp = v.W + 2 * v.hw;
+        v.ss = round_up((int64_t)v.Hp * v.Wp, 64);
+        v.d = p.alloc<float>((size_t)(v.ss * S) + 2 * (size_t)v.Wp + 64);
+        p.rgbx_tv = v;
+        p.rgbx = Rgbx8View{reinterpret_cast<uint32_t*>(v.d), v.ss, v.Wp, v.hh, v.hw};
     }
     p.labels = p.alloc<uint16_t>((size_t)S * lh_ * lw_);
     p.stats = p.alloc<unsigned long long>(stats_words());
@@ -550,13 +563,13 @@ void Engine::record(Plan& p, bool full) {
         const auto& in = p.T[0];
         if (!full && p.chg[0].d) {
             launch_detect_rgb8(d_cur8_, d_prev8_, S, in.H, in.W, layers_[0].threshold, 0, p.chg[0], stats_of(0, 0), 2,
-                               rgbx_, st);
+                               p.rgbx, st);
             mark("detect", 0);
         } else if (!full && p.upd[0].d && p.upd_owner[0] == -1) {
-            launch_detect_rgb8(d_cur8_, d_prev8_, S, in.H, in.W, 0.0f, 1, p.upd[0], nullptr, 2, rgbx_, st);
+            launch_detect_rgb8(d_cur8_, d_prev8_, S, in.H, in.W, 0.0f, 1, p.upd[0], nullptr, 2, p.rgbx, st);
             mark("detect_bitwise", 0);
         } else {
-            launch_detect_rgb8(d_cur8_, d_cur8_, S, in.H, in.W, 0.0f, 2, BitMask{nullptr, 0, 0, 0, 0}, nullptr, 2, rgbx_, st);
+            launch_detect_rgb8(d_cur8_, d_cur8_, S, in.H, in.W, 0.0f, 2, BitMask{nullptr, 0, 0, 0, 0}, nullptr, 2, p.rgbx, st);
             mark("expand", 0);
         }
     } else if (!full) {
@@ -622,10 +635,10 @@ void Engine::record(Plan& p, bool full) {
                 const int64_t full_count = (int64_t)S * dims_[6 * k + 4] * dims_[6 * k + 5];
                 if (k == 0 && rec_u8_) {
                     if (mpr8_)
-                        launch_conv_mpr(*mpr8_, rgbx_tv_, p.T[1], dBias_[0], reinterpret_cast<const uint32_t*>(idx), count,
+                        launch_conv_mpr(*mpr8_, p.rgbx_tv, p.T[1], dBias_[0], reinterpret_cast<const uint32_t*>(idx), count,
                                         S, relu, chg_next, tau_next, cnt_next, 2, nullptr, st);
                     else
-                        launch_conv_tc(*tc8_, rgbx_tv_, p.T[1], dBias_[0], idx, count, full_count, relu, chg_next, tau_next,
+                        launch_conv_tc(*tc8_, p.rgbx_tv, p.T[1], dBias_[0], idx, count, full_count, relu, chg_next, tau_next,
                                        cnt_next, 2, S, st);
                     mark("conv_tc", 0);
                     break;

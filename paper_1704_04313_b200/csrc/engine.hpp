@@ -163,8 +163,6 @@ private:
     std::unique_ptr<MprLayer, MprLayerDeleter> mpr8_;  // the same as a multi-pixel-row conv (preferred)
     bool u8_opt_ = true;          // CBX_OPT_U8_NATIVE
     bool rec_u8_ = false;         // the frame being recorded/launched is 8-bit native
-    Rgbx8View rgbx_{};            // RGBX copy of the current frame (zero halo)
-    TensorView rgbx_tv_{};        // the same buffer as the layer-1 conv input (Cp = 1)
     const uint8_t** d_cur8_ = nullptr;
     const uint8_t** d_prev8_ = nullptr;
     std::vector<const uint8_t*> last_cb_frames8_;

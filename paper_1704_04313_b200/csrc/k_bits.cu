@@ -16,6 +16,7 @@
 //   classify_bits      <- argmax_classify  baseline.cpp:147-163
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <stdexcept>
 
 #include "common.cuh"
@@ -154,12 +155,16 @@ __global__ void __launch_bounds__(256) detect_c3_kernel(const float* const* cur,
 // K1 on 8-bit camera frames (the PPM raster read_ppm decodes, io.cpp:60-104):
 // H x W x 3 interleaved bytes per stream, W a multiple of 16. A thread owns 16
 // pixels (48 bytes = three 128-bit loads per frame). Pixel values are the
-// reference's px / 255.0f (__fdiv_rn, correctly rounded like the host
-// division), so the change test is detect_changes on read_ppm's tensors bit
-// for bit; bytes that are equal in both frames give d = 0 and are skipped
-// without decoding. The same pass writes the current frame as 4-byte RGBX
-// pixels (channel 3 = 0) into the zero-halo tensor the layer-1 tcgen05 conv
-// gathers from, one 4-byte chunk per tap.
+// reference's px / 255.0f (correctly rounded like the host division), so the
+// change test is detect_changes on read_ppm's tensors bit for bit: per
+// channel byte pair, |a - b| >= dhi is changed for every pair and < dlo for
+// none (bounds precomputed on the host for tau by brute force,
+// rgb8_tau_bounds); only differences in [dlo, dhi) -- none unless tau sits
+// within an ulp of some k / 255 -- take the exact decode + compare. The same
+// pass writes the current frame as 4-byte RGBX pixels (channel 3 = 0) into
+// the zero-halo tensor the layer-1 tcgen05 conv gathers from; a steady frame
+// rewrites only the 16-pixel groups whose bytes changed (the buffer holds the
+// previous frame's expansion).
 //   MODE 0: threshold test (CBCONV); MODE 1: any byte differs (updated
 //   pixels of a non-CB first layer); MODE 2: full frame, expansion only.
 template <int MODE>
@@ -219,11 +224,15 @@ __global__ void __launch_bounds__(256) detect_rgb8_kernel(const uint8_t* const* 
                     else if (__vcmpgeu4(ad, lo4)) amb |= 1u << p;
                 }
             }
-            uint4* xo = reinterpret_cast<uint4*>(xs + (int64_t)(y + x.hh) * x.Wp + x.hw + 16 * gx);
-            xo[0] = make_uint4(o[0], o[1], o[2], o[3]);
-            xo[1] = make_uint4(o[4], o[5], o[6], o[7]);
-            xo[2] = make_uint4(o[8], o[9], o[10], o[11]);
-            xo[3] = make_uint4(o[12], o[13], o[14], o[15]);
+            // the RGBX buffer holds the previous frame: only groups whose
+            // bytes differ are rewritten (a static camera rewrites a few %)
+            if (MODE == 2 || any) {
+                uint4* xo = reinterpret_cast<uint4*>(xs + (int64_t)(y + x.hh) * x.Wp + x.hw + 16 * gx);
+                xo[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                xo[1] = make_uint4(o[4], o[5], o[6], o[7]);
+                xo[2] = make_uint4(o[8], o[9], o[10], o[11]);
+                xo[3] = make_uint4(o[12], o[13], o[14], o[15]);
+            }
         }
         if constexpr (MODE != 2) {
             // the exact test (decode + reference compare) for pixels whose
@@ -850,6 +859,149 @@ __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a,
     }
 }
 
+// Single-pass sparse MAXPOOL / RELU: one warp per output row. The lanes form
+// the row's touched words (as point_scan), write U_out and the consumer's
+// cleared change words, then the warp walks the touched pixels of the row in
+// batches of 32 (pixel, 4-channel) items -- window max, compare-before-write,
+// store (+ fp16 shadow) -- and collects the row's change bits in registers:
+// the warp owns the row's change words, so they are written once, without
+// atomics, and counted with one atomic per row. No global work list, no
+// second launch, no dependent global round trip between the two phases.
+// Rows are processed grid-stride (rows without touched pixels cost the mask
+// loads only).
+constexpr int kPfWarps = 8;
+__global__ void __launch_bounds__(32 * kPfWarps) point_fused_kernel(PointBitsArgs a, FastDiv fd_ho, FastDiv fd_c4) {
+    __shared__ uint32_t s_tw[kPfWarps][64];   // touched words of the row (Wo <= 2048)
+    __shared__ uint32_t s_ch[kPfWarps][64];   // change bits of the row
+    __shared__ int s_pre[kPfWarps][65];       // exclusive prefix of the touched words' popcounts
+    const int Ho = a.out.H, Wo = a.out.W;
+    const int wpr = (Wo + 31) / 32;
+    const int c4n = a.in.Cp / 4;
+    const int rowq = a.in.Wp * c4n;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int nrows = a.S * Ho;
+    for (int row = blockIdx.x * kPfWarps + wl; row < nrows; row += gridDim.x * kPfWarps) {
+        const int s = (int)fd_ho.div((uint32_t)row);
+        const int y = row - s * Ho;
+        int ntouched = 0;
+        for (int w = lane; w < wpr; w += 32) {
+            const uint32_t tw = touched_word(a, s, y, w);
+            const int64_t wo = (int64_t)y * wpr + w;
+            if (a.U_out.d) a.U_out.d[(int64_t)s * a.U_out.stride + wo] = tw;
+            s_tw[wl][w] = tw;
+            s_ch[wl][w] = 0u;
+            ntouched += __popc(tw);
+        }
+        ntouched = __reduce_add_sync(0xffffffffu, ntouched);
+        __syncwarp();
+        if (ntouched) {
+            // word prefix counts (<= 64 words: two per lane, one warp scan)
+            const int p0 = lane < wpr ? __popc(s_tw[wl][lane]) : 0;
+            const int p1 = lane + 32 < wpr ? __popc(s_tw[wl][lane + 32]) : 0;
+            int v = p0 + p1, incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            // exclusive prefix of word pairs (lane, lane+32) is not contiguous:
+            // scan words 0..31 and 32..63 separately
+            int i0 = p0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, i0, o);
+                if (lane >= o) i0 += t;
+            }
+            const int tot0 = __shfl_sync(0xffffffffu, i0, 31);
+            int i1 = p1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, i1, o);
+                if (lane >= o) i1 += t;
+            }
+            s_pre[wl][lane] = i0 - p0;
+            s_pre[wl][lane + 32] = tot0 + i1 - p1;
+            if (lane == 0) s_pre[wl][64] = ntouched;
+            (void)incl;
+            __syncwarp();
+        }
+        if (ntouched) {
+            // items (pixel j of the row's touched list, channel quad c4),
+            // 32 at a time; pixel j is found by a warp-wide prefix over words
+            const int items = ntouched * c4n;
+            for (int i0 = 0; i0 < items; i0 += 32) {
+                const int it = i0 + lane;
+                bool ch = false;
+                int x = 0;
+                if (it < items) {
+                    const int j = (int)fd_c4.div((uint32_t)it);
+                    const int c4 = it - j * c4n;
+                    // the j-th set bit of the row: binary search of the word
+                    // prefix counts, then the n-th set bit of the word
+                    int lo = 0, hi = wpr - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (s_pre[wl][mid] <= j) lo = mid; else hi = mid - 1;
+                    }
+                    const int w = lo;
+                    x = 32 * w + (int)__fns(s_tw[wl][w], 0, j - s_pre[wl][w] + 1);
+                    const float4* src = reinterpret_cast<const float4*>(
+                        a.in.d + (int64_t)s * a.in.ss +
+                        ((int64_t)(y * a.stride + a.in.hh) * a.in.Wp + x * a.stride + a.in.hw) * a.in.Cp) + c4;
+                    float4* dst = reinterpret_cast<float4*>(
+                        a.out.d + (int64_t)s * a.out.ss + ((int64_t)(y + a.out.hh) * a.out.Wp + x + a.out.hw) * a.out.Cp) + c4;
+                    const float4 o = a.chg.d ? *dst : make_float4(0.f, 0.f, 0.f, 0.f);
+                    float4 m = *src;
+                    if (a.relu) {
+                        m = make_float4(ref_relu(m.x), ref_relu(m.y), ref_relu(m.z), ref_relu(m.w));
+                    } else if (a.window == 2) {
+                        const float4 v01 = src[c4n], v10 = src[rowq], v11 = src[rowq + c4n];
+                        const float4 wv[4] = {m, v01, v10, v11};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            m = make_float4(ref_max(m.x, wv[k].x), ref_max(m.y, wv[k].y), ref_max(m.z, wv[k].z),
+                                            ref_max(m.w, wv[k].w));
+                    } else {
+                        for (int kj = 0; kj < a.window; ++kj)
+                            for (int ki = 0; ki < a.window; ++ki) {
+                                const float4 v = src[kj * rowq + ki * c4n];
+                                m = make_float4(ref_max(m.x, v.x), ref_max(m.y, v.y), ref_max(m.z, v.z),
+                                                ref_max(m.w, v.w));
+                            }
+                    }
+                    if (a.chg.d)
+                        ch = ref_changed(m.x, o.x, a.tau) | ref_changed(m.y, o.y, a.tau) |
+                             ref_changed(m.z, o.z, a.tau) | ref_changed(m.w, o.w, a.tau);
+                    *dst = m;
+                    if (a.out16.d) {
+                        if (a.f16_overflow && fmaxf(fmaxf(fabsf(m.x), fabsf(m.y)), fmaxf(fabsf(m.z), fabsf(m.w))) > 65504.0f)
+                            atomicOr(a.f16_overflow, 1);
+                        const __half2 h01 = __floats2half2_rn(m.x, m.y), h23 = __floats2half2_rn(m.z, m.w);
+                        uint2 hv;
+                        hv.x = *reinterpret_cast<const uint32_t*>(&h01);
+                        hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+                        reinterpret_cast<uint2*>(a.out16.d + (int64_t)s * a.out16.ss +
+                                                 ((int64_t)(y + a.out16.hh) * a.out16.Wp + x + a.out16.hw) * a.out16.Cp)[c4] = hv;
+                    }
+                }
+                if (a.chg.d && ch) atomicOr(&s_ch[wl][x >> 5], 1u << (x & 31));  // (shared memory)
+            }
+            __syncwarp();
+        }
+        if (a.chg.d) {
+            int nch = 0;
+            for (int w = lane; w < wpr; w += 32) {
+                const uint32_t c = s_ch[wl][w];
+                a.chg.d[(int64_t)s * a.chg.stride + (int64_t)y * wpr + w] = c;
+                nch += __popc(c);
+            }
+            nch = __reduce_add_sync(0xffffffffu, nch);
+            if (lane == 0 && nch && a.chg_cnt) atomicAdd(a.chg_cnt + (int64_t)s * a.cnt_stride, (unsigned long long)nch);
+        }
+        __syncwarp();
+    }
+}
+
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
     const int wpr = (a.out.W + 31) / 32;
     const int64_t nseg = (int64_t)a.S * a.out.H * wpr;
@@ -863,6 +1015,17 @@ void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
         const int64_t items = (int64_t)a.S * a.out.H * a.out.W * c4n;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + kPtThreads - 1) / kPtThreads, (int64_t)kNumSMs * 16));
         point_work_kernel<true><<<grid, kPtThreads, 0, st>>>(a, fd_c4, fd_howo, fd_wo);
+        return;
+    }
+    static const bool two_pass = std::getenv("CBX_POOL_TWO_PASS") != nullptr;  // (tuning: the scan + work pair)
+    // (one warp walks a row's items serially, a dependent load round trip
+    // per 32 items: it wins for 4-channel rows -- pool 1: 28 -> 19 us per
+    // 8 x 1080p lane-frame -- and loses for wide ones -- pool 2's 52
+    // channels: 36 -> 92 us --, which keep the scan + flat work-list pair)
+    if (!two_pass && wpr <= 64 && c4n == 1) {
+        const int nrows = a.S * a.out.H;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nrows + kPfWarps - 1) / kPfWarps, (int64_t)kNumSMs * 16));
+        point_fused_kernel<<<grid, 32 * kPfWarps, 0, st>>>(a, FastDiv::make((uint32_t)a.out.H), fd_c4);
         return;
     }
     if (!a.count_zeroed) cudaMemsetAsync(a.work_count, 0, sizeof(int), st);

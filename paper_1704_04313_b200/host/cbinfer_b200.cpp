@@ -51,6 +51,7 @@ struct Dev {
     explicit Dev(size_t count) : n(count) {
         cuda(cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T) + 16), "cudaMalloc");
         cuda(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T) + 16), "cudaMemset");
+        cuda(cudaStreamSynchronize(nullptr), "cudaStreamSynchronize");  // legacy-stream memset vs non-blocking streams
     }
     Dev(const T* host, size_t count) : Dev(count) {
         if (count) cuda(cudaMemcpy(p, host, count * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");

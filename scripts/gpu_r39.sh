@@ -1,0 +1,1 @@
+for i in 1 2; do timeout 1800 python -m pytest tests -m gpu -q 2>&1 | grep -E "^E   |FAILED|passed|failed" | head -8; done

@@ -61,7 +61,9 @@ def test_native_u8_layer1(gpu, orc, prec, h, w, noise):
         d2, u2 = onet.trace(0)
         assert (d1 is None) == (d2 is None)
         if d1 is not None:
-            assert np.array_equal(d1, d2), f
+            rows = np.nonzero((d1 != d2).any(axis=1))[0]
+            assert np.array_equal(d1, d2), (f, rows.tolist(), int(d1.sum()), int(d2.sum()),
+                                            np.array_equal(net.layer_input(0).view(np.uint32), decode(fr).view(np.uint32)))
         assert np.array_equal(u1, u2), f
         assert np.array_equal(stats_arr(got.stats)[0], stats_arr(want["stats"])[0]), f
         # layer-1 outputs: exact integer accumulation, 2^-23 weight quantization
