@@ -1196,8 +1196,11 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     }
     static const bool no_tap4x7 = std::getenv("CBX_TC_NO_TAP4X7") != nullptr;  // (tuning)
     a.tap4x7 = !no_tap4x7 && in.Cp == 4 && t.g.kernelH == 7 && t.g.kernelW == 7 && t.NKB == 7;
-    static const bool no_xrow = std::getenv("CBX_TC_NO_XROW") != nullptr;  // (tuning)
-    a.xrow = !no_xrow && in.Cp == 4 && !t.f16 && !t.pair;
+    // (8-row x 4-chunk gather: conflict-free but measured slower than the
+    // row-lane tap4x7 gather on the paper's layer 2, 50 vs 46 us per lane-frame;
+    // CBX_TC_XROW=1 selects it, tuning)
+    static const bool xrow = std::getenv("CBX_TC_XROW") != nullptr;
+    a.xrow = xrow && in.Cp == 4 && !t.f16 && !t.pair;
     a.ovl_s = t.ovl_s;
     a.ovl_b0 = t.ovl_b0;
     a.ovl_b1 = t.ovl_b1;

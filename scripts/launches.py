@@ -11,7 +11,9 @@ per = collections.OrderedDict()
 for r in rows[hi + 1:]:
     if len(r) > vi:
         per.setdefault(r[ii], {"name": r[ki]})[r[mi]] = r[vi]
-seq = [d for d in per.values() if not d["name"].startswith("synth")]
+# the bench's own kernels only (clip synthesis and torch's elementwise/decode helpers excluded)
+seq = [d for d in per.values()
+       if not any(k in d["name"] for k in ("synth_kernel", "elementwise", "decode_u8", "vectorized", "unrolled"))]
 start = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 n = int(sys.argv[3]) if len(sys.argv) > 3 else len(seq)
 tot = 0.0

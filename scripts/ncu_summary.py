@@ -10,9 +10,12 @@ import json
 import subprocess
 import sys
 
-# launch order of a steady frame of paper_like (tf32): bench.py's kernel names
-FRAME = ["detect[0]", "dilate_compact[0]", "conv_exact[0]", "pool[1]:scan", "pool[1]:work", "dilate_compact[2]",
+# launch order of a steady frame of paper_like (f16, 8-bit frames): bench.py's kernel names
+# (FRAME_F32: the fp32-frame path of round 1)
+FRAME = ["detect[0]", "dilate_compact[0]", "conv_tc[0]", "pool[1]", "dilate_compact[2]",
          "conv_tc[2]", "pool[3]:scan", "pool[3]:work", "dilate_compact[4]", "conv_tc_tail[4]"]
+FRAME_F32 = ["detect[0]", "dilate_compact[0]", "conv_exact[0]", "pool[1]:scan", "pool[1]:work", "dilate_compact[2]",
+             "conv_tc[2]", "pool[3]:scan", "pool[3]:work", "dilate_compact[4]", "conv_tc_tail[4]"]
 METRICS = [
     ("gpu__time_duration.sum", "us", 1e-3),
     ("dram__bytes_read.sum", "MB rd", 1e-6),
