@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace cbx {
 
 constexpr int kNumSMs = 148;  // B200
@@ -51,6 +53,39 @@ struct BitMask {
 };
 
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// Programmatic dependent launch (the frame's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, see launch_k): every
+// kernel lets its successor start launching at once (pdl_trigger) and waits
+// for its predecessor's grid to complete -- memory included -- before it
+// touches anything the predecessor produced (pdl_wait). The successor's
+// CTAs are then scheduled onto the SMs the predecessor's last wave frees,
+// and can run their prologue there, instead of starting after the drain.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_entry() {
+    pdl_trigger();
+    pdl_wait();
+}
+
+// Launch with the programmatic-stream-serialization attribute when
+// CBX_PDL=1 (opt-in, see pdl_enabled in engine.cu); plain stream order else.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Division by a runtime-constant divisor as a multiply-high and a shift, for
 // numerators below 2^31 (the per-pixel index arithmetic of the hot kernels:

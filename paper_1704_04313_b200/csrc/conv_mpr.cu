@@ -124,6 +124,7 @@ __device__ __forceinline__ void group_of(const MprArgs& a, uint32_t gid, int& s,
 
 template <int MODE, int R>
 __global__ void __launch_bounds__(kThreads, MODE == 0 ? 2 : 1) conv_mpr_kernel(MprArgs a) {
+    pdl_trigger();  // (the prologue below touches only this launch's constants)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int NS = a.stages;
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, MODE == 0 ? 2 : 1) conv_mpr_kernel(M
         for (int kb = 0; kb < a.NKB; ++kb) bulk_g2s(sB + (size_t)kb * b_kb, a.Bw + (size_t)kb * b_kb, b_kb, bready);
     }
 
+    pdl_wait();  // the group list / count and the input tensor come from the previous kernels
     const int64_t total = a.list ? (int64_t)*a.count : a.full_groups;
     const int64_t ntiles = (total + kTileM - 1) / kTileM;
     const int64_t tile_first = blockIdx.x, tile_step = gridDim.x;
@@ -681,7 +683,7 @@ void launch_conv_mpr(const MprLayer& t, TensorView in, TensorView out, const flo
     const int64_t max_tiles = (a.full_groups + kTileM - 1) / kTileM;
     const int64_t cap = t.max_ctas > 0 ? t.max_ctas : (int64_t)kNumSMs * t.ctas_per_sm;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, cap));
-#define CBX_MPR(M_, R_) conv_mpr_kernel<M_, R_><<<grid, kThreads, t.smem, st>>>(a)
+#define CBX_MPR(M_, R_) launch_k(conv_mpr_kernel<M_, R_>, dim3(grid), dim3(kThreads), t.smem, st, a)
     if (t.mode == 0) {
         if (t.R == 4) CBX_MPR(0, 4); else if (t.R == 2) CBX_MPR(0, 2); else CBX_MPR(0, 1);
     } else {

@@ -249,6 +249,7 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, float (&v)[32], int c
 // accumulator rows of its own 128 pixels, so the epilogue is unchanged.
 template <bool ROWLANE, int TC, bool PAIR, bool I8 = false>
 __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs a) {
+    pdl_trigger();  // (the prologue below touches only this launch's constants)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // align by offsetting the shared array itself (not via an integer round
     // trip), so the compiler keeps emitting LDS/STS for the smem tables below
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
     tc_fence_after();
     const uint32_t tmem_base = *sTmem;
 
+    pdl_wait();  // the index list / count and the input tensor come from the previous kernels
     const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
     const int64_t ntiles = (total + kRowsPerTile - 1) / kRowsPerTile;
     const int64_t HoWo = (int64_t)a.Ho * a.Wo;
@@ -1251,10 +1253,10 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     const int64_t cap = t.max_ctas > 0 ? t.max_ctas : (int64_t)kNumSMs * t.ctas_per_sm;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_tiles, cap));
     if (t.i8) {
-        conv_tc_kernel<true, 0, false, true><<<grid, kThreads, t.smem, st>>>(a);
+        launch_k(conv_tc_kernel<true, 0, false, true>, dim3(grid), dim3(kThreads), t.smem, st, a);
         return;
     }
-#define CBX_TC_LAUNCH(R, T) conv_tc_kernel<R, T, false><<<grid, kThreads, t.smem, st>>>(a)
+#define CBX_TC_LAUNCH(R, T) launch_k(conv_tc_kernel<R, T, false>, dim3(grid), dim3(kThreads), t.smem, st, a)
     if (tc == 0) {
         if (rowlane) CBX_TC_LAUNCH(true, 0); else CBX_TC_LAUNCH(false, 0);
     } else if (tc == 8) {

@@ -24,6 +24,7 @@
 // "full" mode: no masks, every output pixel evaluated.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -33,6 +34,14 @@
 #include "conv_tc.hpp"
 
 namespace cbx {
+
+// Programmatic dependent launch is opt-in (CBX_PDL=1): with two lanes the
+// early-launched successors sit on SM slots the other lane's kernels would
+// use, and the step measured slower (27.8k vs 30.6k frames/s, 16 x 1080p).
+bool pdl_enabled() {
+    static const bool on = std::getenv("CBX_PDL") && std::atoi(std::getenv("CBX_PDL")) == 1;
+    return on;
+}
 
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) {

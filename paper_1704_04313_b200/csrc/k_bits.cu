@@ -31,6 +31,7 @@ template <int MODE, bool VEC>
 __global__ void __launch_bounds__(256) detect_bits_kernel(const float* const* cur, const float* const* prev, int C,
                                                           int H, int W, float tau, BitMask m,
                                                           unsigned long long* cnt, int cstride) {
+    pdl_entry();
     const int s = blockIdx.y;
     const float* a = cur[s];
     const float* b = prev[s];
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(256) detect_bits_kernel(const float* const* cu
 template <int QPT>
 __global__ void __launch_bounds__(256) detect_c3_kernel(const float* const* cur, const float* const* prev, int H, int W,
                                                         float tau, BitMask m, unsigned long long* cnt, int cstride) {
+    pdl_entry();
     const int s = blockIdx.y;
     const float* a = cur[s];
     const float* b = prev[s];
@@ -171,6 +173,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) detect_rgb8_kernel(const uint8_t* const* cur, const uint8_t* const* prev, int H,
                                                           int W, float tau, int dlo, int dhi, BitMask m,
                                                           unsigned long long* cnt, int cstride, Rgbx8View x) {
+    pdl_entry();
     // px / 255.0f of every byte value: the reference's read_ppm decode
     // (correctly rounded division, like the host's)
     __shared__ float lut[256];
@@ -319,11 +322,11 @@ void launch_detect_rgb8(const uint8_t* const* cur, const uint8_t* const* prev, i
     int dlo = 256, dhi = 256;
     if (mode != 2) rgb8_tau_bounds(tau, mode, dlo, dhi);
     if (mode == 0)
-        detect_rgb8_kernel<0><<<grid, 256, 0, st>>>(cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
+        launch_k(detect_rgb8_kernel<0>, grid, dim3(256), 0, st, cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
     else if (mode == 1)
-        detect_rgb8_kernel<1><<<grid, 256, 0, st>>>(cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
+        launch_k(detect_rgb8_kernel<1>, grid, dim3(256), 0, st, cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
     else
-        detect_rgb8_kernel<2><<<grid, 256, 0, st>>>(cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
+        launch_k(detect_rgb8_kernel<2>, grid, dim3(256), 0, st, cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
 }
 
 void launch_detect_bits(const float* const* cur, const float* const* prev, int S, int C, int H, int W, float tau,
@@ -340,17 +343,17 @@ void launch_detect_bits(const float* const* cur, const float* const* prev, int S
         int g3 = (int)((nq + 256 * QPT - 1) / (256 * QPT));
         const int cap3 = (kNumSMs * 8 + S - 1) / S;
         if (g3 > cap3) g3 = cap3 < 1 ? 1 : cap3;
-        detect_c3_kernel<QPT><<<dim3(g3, S), 256, 0, st>>>(cur, prev, H, W, tau, m, cnt, cstride);
+        launch_k(detect_c3_kernel<QPT>, dim3(g3, S), dim3(256), 0, st, cur, prev, H, W, tau, m, cnt, cstride);
         return;
     }
     if (mode == 0 && vec)
-        detect_bits_kernel<0, true><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
+        launch_k(detect_bits_kernel<0, true>, grid, dim3(256), 0, st, cur, prev, C, H, W, tau, m, cnt, cstride);
     else if (mode == 0)
-        detect_bits_kernel<0, false><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
+        launch_k(detect_bits_kernel<0, false>, grid, dim3(256), 0, st, cur, prev, C, H, W, tau, m, cnt, cstride);
     else if (vec)
-        detect_bits_kernel<1, true><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
+        launch_k(detect_bits_kernel<1, true>, grid, dim3(256), 0, st, cur, prev, C, H, W, tau, m, cnt, cstride);
     else
-        detect_bits_kernel<1, false><<<grid, 256, 0, st>>>(cur, prev, C, H, W, tau, m, cnt, cstride);
+        launch_k(detect_bits_kernel<1, false>, grid, dim3(256), 0, st, cur, prev, C, H, W, tau, m, cnt, cstride);
 }
 
 // ---------------------------------------------------------------------------
@@ -457,6 +460,7 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
                                                                     int kh, int kw, int ph, int pw, bool identity,
                                                                     int32_t* __restrict__ idx, int* total,
                                                                     unsigned long long* cnt, int cstride) {
+    pdl_entry();
     extern __shared__ uint4 s_rows4[];
     uint32_t* s_rows = reinterpret_cast<uint32_t*>(s_rows4);
     __shared__ int s_warp[kDcThreads / 32];
@@ -599,8 +603,8 @@ static void launch_dc_r(BitMask in, BitMask out, bool write_out, int S, int kh, 
     const size_t smem = dc_smem_bytes(in, out, identity ? 1 : kh, WPT);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(dilate_compact_kernel<WPT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dilate_compact_kernel<WPT, R><<<(unsigned)tiles, kDcThreads, smem, st>>>(in, out, write_out, kh, kw, ph, pw,
-                                                                             identity, idx, total, cnt, cstride);
+    launch_k(dilate_compact_kernel<WPT, R>, dim3((unsigned)tiles), dim3(kDcThreads), smem, st, in, out, write_out, kh, kw,
+             ph, pw, identity, idx, total, cnt, cstride);
 }
 
 template <int WPT>
@@ -638,6 +642,7 @@ void launch_dilate_compact(BitMask in, BitMask out, bool write_out, int S, int k
 // Generic dilation (any stride): one thread per output word; every output
 // pixel ORs its zero-padded receptive field via bit tests.
 __global__ void dilate_bits_kernel(BitMask in, BitMask out, int kh, int kw, int sh, int sw, int ph, int pw) {
+    pdl_entry();
     const int s = blockIdx.y;
     const int64_t nw = (int64_t)out.H * out.wpr;
     for (int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += (int64_t)gridDim.x * blockDim.x) {
@@ -668,7 +673,7 @@ void launch_dilate_bits(BitMask in, BitMask out, int S, int kh, int kw, int sh, 
                         cudaStream_t st) {
     const int64_t nw = (int64_t)out.H * out.wpr;
     int gx = (int)std::min<int64_t>((nw + 127) / 128, 4096);
-    dilate_bits_kernel<<<dim3(gx < 1 ? 1 : gx, S), 128, 0, st>>>(in, out, kh, kw, sh, sw, ph, pw);
+    launch_k(dilate_bits_kernel, dim3(gx < 1 ? 1 : gx, S), dim3(128), 0, st, in, out, kh, kw, sh, sw, ph, pw);
 }
 
 // ---------------------------------------------------------------------------
@@ -737,6 +742,7 @@ __device__ __forceinline__ uint32_t touched_word(const PointBitsArgs& a, int s, 
 // (index arithmetic: every count here is below 2^31 -- launch_point_bits
 // checks -- so divisions are multiply-shifts, FastDiv)
 __global__ void __launch_bounds__(kPtThreads) point_scan_kernel(PointBitsArgs a, FastDiv fd_plane, FastDiv fd_wpr) {
+    pdl_entry();
     const int Ho = a.out.H, Wo = a.out.W;
     const int wpr = (Wo + 31) / 32;
     const int nseg = a.S * Ho * wpr;
@@ -781,6 +787,7 @@ __global__ void __launch_bounds__(kPtThreads) point_scan_kernel(PointBitsArgs a,
 template <bool FULL>
 __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a, FastDiv fd_c4, FastDiv fd_howo,
                                                                 FastDiv fd_wo) {
+    pdl_entry();
     const int Ho = a.out.H, Wo = a.out.W;
     const int wpr = (Wo + 31) / 32;
     const int c4n = a.in.Cp / 4;
@@ -871,6 +878,7 @@ __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a,
 // loads only).
 constexpr int kPfWarps = 8;
 __global__ void __launch_bounds__(32 * kPfWarps) point_fused_kernel(PointBitsArgs a, FastDiv fd_ho, FastDiv fd_c4) {
+    pdl_entry();
     __shared__ uint32_t s_tw[kPfWarps][64];   // touched words of the row (Wo <= 2048)
     __shared__ uint32_t s_ch[kPfWarps][64];   // change bits of the row
     __shared__ int s_pre[kPfWarps][65];       // exclusive prefix of the touched words' popcounts
@@ -1014,7 +1022,7 @@ void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
     if (!a.upd_in.d) {  // full frame: every pixel, no change test (the next layer evaluates in full)
         const int64_t items = (int64_t)a.S * a.out.H * a.out.W * c4n;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + kPtThreads - 1) / kPtThreads, (int64_t)kNumSMs * 16));
-        point_work_kernel<true><<<grid, kPtThreads, 0, st>>>(a, fd_c4, fd_howo, fd_wo);
+        launch_k(point_work_kernel<true>, dim3(grid), dim3(kPtThreads), 0, st, a, fd_c4, fd_howo, fd_wo);
         return;
     }
     static const bool two_pass = std::getenv("CBX_POOL_TWO_PASS") != nullptr;  // (tuning: the scan + work pair)
@@ -1025,17 +1033,18 @@ void launch_point_bits(const PointBitsArgs& a, cudaStream_t st) {
     if (!two_pass && wpr <= 64 && c4n == 1) {
         const int nrows = a.S * a.out.H;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nrows + kPfWarps - 1) / kPfWarps, (int64_t)kNumSMs * 16));
-        point_fused_kernel<<<grid, 32 * kPfWarps, 0, st>>>(a, FastDiv::make((uint32_t)a.out.H), fd_c4);
+        launch_k(point_fused_kernel, dim3(grid), dim3(32 * kPfWarps), 0, st, a, FastDiv::make((uint32_t)a.out.H), fd_c4);
         return;
     }
     if (!a.count_zeroed) cudaMemsetAsync(a.work_count, 0, sizeof(int), st);
     const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>((nseg + kPtThreads - 1) / kPtThreads, (int64_t)kNumSMs * 8));
-    point_scan_kernel<<<g1, kPtThreads, 0, st>>>(a, fd_plane, fd_wpr);
-    point_work_kernel<false><<<kNumSMs * 8, kPtThreads, 0, st>>>(a, fd_c4, fd_howo, fd_wo);
+    launch_k(point_scan_kernel, dim3(g1), dim3(kPtThreads), 0, st, a, fd_plane, fd_wpr);
+    launch_k(point_work_kernel<false>, dim3(kNumSMs * 8), dim3(kPtThreads), 0, st, a, fd_c4, fd_howo, fd_wo);
 }
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) classify_bits_kernel(TensorView in, BitMask upd, uint16_t* labels, int S) {
+    pdl_entry();
     const int H = in.H, W = in.W;
     const int64_t HW = (int64_t)H * W, total = HW * S;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1060,7 +1069,7 @@ __global__ void __launch_bounds__(256) classify_bits_kernel(TensorView in, BitMa
 void launch_classify_bits(TensorView in, BitMask upd, uint16_t* labels, int S, cudaStream_t st) {
     const int64_t total = (int64_t)in.H * in.W * S;
     int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
-    classify_bits_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(in, upd, labels, S);
+    launch_k(classify_bits_kernel, dim3(grid < 1 ? 1 : grid), dim3(256), 0, st, in, upd, labels, S);
 }
 
 // Per-stream number of set bits of a mask (analyze-prop worst-case counts).

@@ -27,6 +27,7 @@ constexpr int kConvThreads = 128, kConvKC = 256;
 // 8 or 16 otherwise, so no accumulator is wasted on padding.
 template <bool PLANAR, int kConvOC>
 __global__ void __launch_bounds__(kConvThreads) conv_exact_kernel(ConvArgs a) {
+    pdl_entry();
     __shared__ __align__(16) float sW[kConvKC][kConvOC];  // r-major: the OC weights of one tap are one 16B-vector load
     const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
     const int64_t ntiles = (total + kConvThreads - 1) / kConvThreads;
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(kConvThreads) conv_exact_kernel(ConvArgs a) {
 // 8 in flight) before they are accumulated in reference order.
 template <int OC>
 __global__ void __launch_bounds__(kConvThreads) conv_planar_kernel(ConvArgs a) {
+    pdl_entry();
     extern __shared__ float4 sWv[];  // [Kdim][OC/4]
     const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
     const int64_t ntiles = (total + kConvThreads - 1) / kConvThreads;
@@ -252,6 +254,7 @@ struct PlanarFilters {
 template <int C, int KH, int KW, int OC>
 __global__ void __launch_bounds__(kConvThreads, 8) conv_planar_fixed_kernel(ConvArgs a,
                                                                             const __grid_constant__ PlanarFilters<C, KH, KW, OC> f) {
+    pdl_entry();
     const int64_t total = a.idx ? (int64_t)*a.count : a.full_count;
     const int Wo = a.out.W, H = a.in.H, W = a.in.W;
     const int64_t HoWo = (int64_t)a.out.H * Wo, HW = (int64_t)H * W;
@@ -365,11 +368,11 @@ template <int OC>
 static void launch_conv_exact_oc(const ConvArgs& a, int grid, cudaStream_t st) {
     const size_t smem = (size_t)a.in.C * a.kh * a.kw * OC * sizeof(float);
     if (a.in_ptrs && smem <= 48 * 1024)
-        conv_planar_kernel<OC><<<grid, kConvThreads, smem, st>>>(a);
+        launch_k(conv_planar_kernel<OC>, dim3(grid), dim3(kConvThreads), smem, st, a);
     else if (a.in_ptrs)
-        conv_exact_kernel<true, OC><<<grid, kConvThreads, 0, st>>>(a);
+        launch_k(conv_exact_kernel<true, OC>, dim3(grid), dim3(kConvThreads), 0, st, a);
     else
-        conv_exact_kernel<false, OC><<<grid, kConvThreads, 0, st>>>(a);
+        launch_k(conv_exact_kernel<false, OC>, dim3(grid), dim3(kConvThreads), 0, st, a);
 }
 
 void launch_conv_exact(const ConvArgs& a, cudaStream_t st) {
@@ -385,7 +388,7 @@ void launch_conv_exact(const ConvArgs& a, cudaStream_t st) {
         for (int j = 0; j < 4; ++j) f.b[j] = a.hB[j];
         f.one = 1.0f;
         f.nzero = -0.0f;
-        conv_planar_fixed_kernel<3, 7, 7, 4><<<grid, kConvThreads, 0, st>>>(a, f);
+        launch_k(conv_planar_fixed_kernel<3, 7, 7, 4>, dim3(grid), dim3(kConvThreads), 0, st, a, f);
         return;
     }
     if (a.out.C <= 4)
@@ -584,6 +587,7 @@ void launch_synth_frame(float* out, int C, int H, int W, const SpriteRect* rects
 namespace cbx {
 
 __global__ void ingest_kernel(const float* const* frames, TensorView t) {
+    pdl_entry();
     const int s = blockIdx.y;
     const float* src = frames[s];
     const int64_t HW = (int64_t)t.H * t.W, n = HW * t.C;
@@ -598,7 +602,7 @@ __global__ void ingest_kernel(const float* const* frames, TensorView t) {
 void launch_ingest(const float* const* frames, TensorView t, int S, cudaStream_t st) {
     const int64_t n = (int64_t)t.C * t.H * t.W;
     int gx = (int)std::min<int64_t>((n + 255) / 256, 1024);
-    ingest_kernel<<<dim3(gx < 1 ? 1 : gx, S), 256, 0, st>>>(frames, t);
+    launch_k(ingest_kernel, dim3(gx < 1 ? 1 : gx, S), dim3(256), 0, st, frames, t);
 }
 
 }  // namespace cbx

@@ -1,0 +1,6 @@
+timeout 1500 python -m pytest tests/test_gpu_network.py tests/test_gpu_u8.py tests/test_gpu_tc.py tests/test_gpu_benchconfig.py -q -x 2>&1 | tail -2
+q() { echo -n "$* : "; env "$@" timeout 300 python bench.py --quick --steps 30 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['ms_per_step'],4), d['clocks']['sm_mhz'])"; }
+q CBX_PDL=1
+q CBX_PDL=0
+q CBX_PDL=1
+q CBX_PDL=0
