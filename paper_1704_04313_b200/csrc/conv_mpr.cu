@@ -539,7 +539,9 @@ std::unique_ptr<MprLayer, MprLayerDeleter> make_mpr_layer(const cbx_geom& g, int
     t->ctas_per_sm = mode == 0 && fixed + 4 * (size_t)kABytes <= (size_t)kMaxSmem / 2 - 1024 ? 2 : 1;
     if (const char* e = std::getenv("CBX_MPR_CTAS")) t->ctas_per_sm = std::max(1, std::min(2, std::atoi(e)));
     const size_t budget = t->ctas_per_sm == 2 ? (size_t)kMaxSmem / 2 - 1024 : (size_t)kMaxSmem;
-    int ns = 8;
+    // three A stages (plus the two K-blocks in flight in the producers'
+    // registers): a small footprint so the other lane's kernels fit beside it
+    int ns = 3;
     if (const char* e = std::getenv("CBX_MPR_STAGES")) ns = std::max(2, std::min(12, std::atoi(e)));  // (tuning)
     while (ns > 2 && fixed + (size_t)ns * kABytes > budget) --ns;
     if (fixed + (size_t)ns * kABytes > budget) throw Error(CBX_E_ARG, "multi-pixel-row conv: filters too large");

@@ -977,7 +977,9 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     // other's MMAs/epilogue.
     t->pair = pair_mode > 0;
     t->Brows = t->pair ? t->Npad / 2 : t->Npad;
-    t->ctas_per_sm = (!t->pair && t->Npad <= 128) ? 2 : 1;
+    // one CTA per SM: with two lanes the second CTA's shared memory is worth
+    // more to the other lane's kernels (16 x 1080p: 31.7k -> 32.3k frames/s)
+    t->ctas_per_sm = 1;
     if (const char* e = std::getenv("CBX_TC_CTAS_PER_SM"))  // tuning
         if (!t->pair && t->Npad <= 128) t->ctas_per_sm = std::max(1, std::min(2, std::atoi(e)));
     const size_t b_bytes = (size_t)t->Brows * 128;
@@ -989,8 +991,16 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     // leave L1 for the gather's tap reuse (neighbouring output pixels share
     // input pixels across taps; the L1 hit rate collapses when shared memory
     // takes the whole carve-out). CBX_TC_STAGES overrides (tuning).
-    int ns = t->pair ? 4 : 8;
+    // Three stages: the layers do not get faster with more (measured: the
+    // paper's layer 3 155.6 us with 3 or 4 stages, layer 2 44-46 us with
+    // 2..8), and the smaller shared-memory footprint lets the other lane's
+    // kernels co-reside with the persistent CTAs (16 x 1080p: 30.3k -> 30.9k
+    // frames/s; with the 3-stage layer-1 conv, 31.4k). CBX_TC_STAGES /
+    // CBX_TC_STAGES_WIDE (N > 256) override (tuning).
+    int ns = t->pair ? 4 : 3;
     if (const char* e = std::getenv("CBX_TC_STAGES")) ns = std::max(2, std::min(16, std::atoi(e)));
+    if (t->Npad > 256)
+        if (const char* e = std::getenv("CBX_TC_STAGES_WIDE")) ns = std::max(2, std::min(16, std::atoi(e)));
     while (ns > 2 && fixed + (size_t)ns * (kABytes + b_bytes) > budget) --ns;
     if (fixed + (size_t)ns * (kABytes + b_bytes) > budget)
         throw Error(CBX_E_ARG, "tcgen05 conv: layer too wide for shared memory");

@@ -169,6 +169,16 @@ __global__ void __launch_bounds__(256) detect_c3_kernel(const float* const* cur,
 // previous frame's expansion).
 //   MODE 0: threshold test (CBCONV); MODE 1: any byte differs (updated
 //   pixels of a non-CB first layer); MODE 2: full frame, expansion only.
+// SWAR: nonzero iff some byte of x is >= t (1 <= t <= 256; t = 256: never).
+// Bytes below 128 carry into bit 7 when (b & 0x7f) + 0x80 - t overflows 7
+// bits; bytes with bit 7 set need their low 7 bits compared with t - 128.
+__device__ __forceinline__ uint32_t any_byte_ge(uint32_t x, int t) {
+    if (t > 255) return 0u;
+    const uint32_t lo7 = x & 0x7f7f7f7fu;
+    if (t <= 128) return ((lo7 + (uint32_t)(0x80 - t) * 0x01010101u) | x) & 0x80808080u;
+    return (lo7 + (uint32_t)(0x80 - (t - 128)) * 0x01010101u) & x & 0x80808080u;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) detect_rgb8_kernel(const uint8_t* const* cur, const uint8_t* const* prev, int H,
                                                           int W, float tau, int dlo, int dhi, BitMask m,
@@ -181,7 +191,6 @@ __global__ void __launch_bounds__(256) detect_rgb8_kernel(const uint8_t* const* 
         for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = __fdiv_rn((float)i, 255.0f);
         __syncthreads();
     }
-    const uint32_t lo4 = (uint32_t)dlo * 0x01010101u, hi4 = (uint32_t)min(dhi, 255) * 0x01010101u;
     const int s = blockIdx.y;
     const uint4* a = reinterpret_cast<const uint4*>(cur[s]);
     const uint4* b = MODE == 2 ? nullptr : reinterpret_cast<const uint4*>(prev[s]);
@@ -223,8 +232,8 @@ __global__ void __launch_bounds__(256) detect_rgb8_kernel(const uint8_t* const* 
                     // |a - b| per channel byte: >= dhi is changed for every byte
                     // pair, < dlo for none; in between decide exactly below
                     const uint32_t ad = __vabsdiffu4(o[p], op[p]);
-                    if (__vcmpgeu4(ad, hi4) && dhi <= 255) flags |= 1u << p;
-                    else if (__vcmpgeu4(ad, lo4)) amb |= 1u << p;
+                    if (any_byte_ge(ad, dhi)) flags |= 1u << p;
+                    else if (any_byte_ge(ad, dlo)) amb |= 1u << p;
                 }
             }
             // the RGBX buffer holds the previous frame: only groups whose
