@@ -75,6 +75,30 @@ __device__ __forceinline__ void pixel_of(const A& a, int64_t g, int64_t HoWo, in
     }
 }
 
+// List entry n of a launch: the list's value, or in full mode the pixel index
+// n / the group entry (n << 4 | mask of the group's pixels inside the row).
+template <class A>
+__device__ __forceinline__ int64_t entry_at(const A& a, int64_t n) {
+    if (a.idx) return (int64_t)__ldg(a.idx + n);
+    if (a.grp_R <= 1) return n;
+    const uint32_t gid = (uint32_t)n;
+    const uint32_t rem = gid - a.fd_gplane.div(gid) * (uint32_t)(a.Ho * a.Gw);
+    const int x0 = (int)(rem - a.fd_gw.div(rem) * (uint32_t)a.Gw) * a.grp_R;
+    return (n << 4) | ((1 << min(a.grp_R, a.Wo - x0)) - 1);
+}
+
+// Group entry -> stream, output row, first output column.
+template <class A>
+__device__ __forceinline__ void group_of_tc(const A& a, int64_t e, int& s, int& y, int& x0) {
+    const uint32_t gid = (uint32_t)(e >> 4);
+    const uint32_t ss = a.fd_gplane.div(gid);
+    const uint32_t rem = gid - ss * (uint32_t)(a.Ho * a.Gw);
+    const uint32_t yy = a.fd_gw.div(rem);
+    s = (int)ss;
+    y = (int)yy;
+    x0 = (int)(rem - yy * (uint32_t)a.Gw) * a.grp_R;
+}
+
 // Remaining per-pixel ops of a fused tail (after the first 1x1 CONV, whose
 // outputs arrive in `cur`): RELU (ref_relu), 1x1 CONV (bias-first, ascending
 // channel order, one rounding per multiply and add -- the reference gemm
@@ -152,6 +176,12 @@ struct TcArgs {
     // pixel index -> (stream, y, x) by multiply-shift when S*Ho*Wo < 2^31
     int fast;
     FastDiv fd_howo, fd_wo;
+    // pixel groups (grp_R > 1, stride-1 layers with a 4-channel input): an A
+    // row is R horizontally adjacent output pixels, K its union window
+    // (kh x (kw + R - 1) taps), N = R x grp_N (sub-pixel j's channels at
+    // columns j * grp_N); list entries (gid << 4 | mask), gid over Ho x Gw
+    int grp_R, grp_N, Gw;
+    FastDiv fd_gplane, fd_gw;
     int f16;     // operands are fp16 (kind::f16): the input is an fp16 shadow tensor
                  // addressed in 4-byte units (in_Cp = fp16 channels / 2)
     int relu;
@@ -290,6 +320,13 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         int off = -1;
         if (I8) {
             // (unused: the register-staged gather computes its offsets)
+        } else if (a.grp_R > 1) {
+            const int span = a.kw + a.grp_R - 1;  // window columns per kernel row
+            if (j < a.kh * span * C4) {
+                const int tap = j / C4, c4 = j - tap * C4;
+                const int kj = tap / span, w = tap - kj * span;
+                off = (kj * a.in_Wp + w) * a.in_Cp + c4 * 4;
+            }
         } else if (j < nchunks) {
             const int tap = j / C4, c4 = j - tap * C4;
             const int kj = tap / a.kw, ki = tap - kj * a.kw;
@@ -461,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             // gathered, so a tile never starts with a dependent index load
             auto row_index = [&](int64_t t) -> int64_t {
                 const int64_t n = t * kRowsPerTile + row_off + r;
-                return (t < ntiles && n < total) ? (a.idx ? (int64_t)__ldg(a.idx + n) : n) : -1;
+                return (t < ntiles && n < total) ? entry_at(a, n) : -1;
             };
             int64_t gnext = row_index(tile_first);
             for (int64_t tile = tile_first; tile < ntiles; tile += tile_step) {
@@ -471,7 +508,11 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 const float* base = a.in;
                 if (valid) {
                     int s, p, y, x;
-                    pixel_of(a, g, HoWo, s, p, y, x);
+                    if (a.grp_R > 1) {  // the group's window: stride 1, columns from x0 - pw
+                        group_of_tc(a, g, s, y, x);
+                    } else {
+                        pixel_of(a, g, HoWo, s, p, y, x);
+                    }
                     base = a.in + (int64_t)s * a.in_ss +
                            ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
                 }
@@ -680,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         // bound by that latency)
         auto row_index = [&](int64_t t) -> int64_t {
             const int64_t n = t * kRowsPerTile + row_off + r;
-            return (t < ntiles && n < total) ? (a.idx ? (int64_t)__ldg(a.idx + n) : n) : -1;
+            return (t < ntiles && n < total) ? entry_at(a, n) : -1;
         };
         int64_t gnext = row_index(tile_first);
         for (int64_t tile = tile_first; tile < ntiles; tile += tile_step, ++acc_it) {
@@ -692,7 +733,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             const int64_t g = valid ? gi : 0;
             int s = 0, p = 0, y = 0, x = 0;
             float* dst = nullptr;
-            if (valid) {
+            if (valid && a.grp_R <= 1) {
                 pixel_of(a, g, HoWo, s, p, y, x);
                 dst = a.out + (int64_t)s * a.out_ss + ((int64_t)(y + a.out_hh) * a.out_Wp + (x + a.out_hw)) * a.out_Cp;
                 // the values this pixel overwrites (compare-before-write) are
@@ -752,6 +793,53 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                 if (a.chg.d) {
                     if (valid && changed) bit_set(a.chg, s, y, x);
                     if (a.chg_cnt) warp_count_add(a.chg_cnt, a.cnt_stride, s, changed, valid);
+                }
+                continue;
+            }
+            if (a.grp_R > 1) {
+                // pixel group: sub-pixel j's channels at columns j * grp_N;
+                // each live sub-pixel (mask bit) gets the per-pixel epilogue
+                int gs = 0, gy = 0, gx0 = 0;
+                const uint32_t gm = valid ? (uint32_t)(gi & 15) : 0u;
+                if (valid) group_of_tc(a, gi, gs, gy, gx0);
+                const uint32_t tb = trow + as * a.acc_cols;
+                TailAcc<TC> t1g;
+                uint32_t chb = 0;
+                for (int j = 0; j < a.grp_R; ++j) {
+                    const bool live = (gm >> j) & 1u;
+                    float* dj = a.out + (int64_t)gs * a.out_ss +
+                                ((int64_t)(gy + a.out_hh) * a.out_Wp + (gx0 + j + a.out_hw)) * a.out_Cp;
+                    bool chj = false;
+                    for (int c0 = 0; c0 < a.O; c0 += 32) {
+                        float v[32];
+                        tmem_ld32(tb + (uint32_t)(j * a.grp_N + c0), v);
+                        if (!live) continue;
+                        if (c0 + 32 <= a.O)
+                            epi_chunk<TC, true>(a, v, c0, 32, sBias, sTailW, t1g, dj, chj);
+                        else
+                            epi_chunk<TC, false>(a, v, c0, a.O - c0, sBias, sTailW, t1g, dj, chj);
+                    }
+                    if (live && chj) chb |= 1u << j;
+                }
+                tc_fence_before();
+                mbar_arrive(&tempty[as]);
+                if (a.chg.d) {
+                    for (int j = 0; j < a.grp_R; ++j)
+                        if ((chb >> j) & 1u) bit_set(a.chg, gs, gy, gx0 + j);
+                    if (a.chg_cnt) {
+                        const unsigned act = __ballot_sync(0xffffffffu, valid);
+                        const int n = __popc(chb);
+                        if (valid) {
+                            const unsigned same = __match_any_sync(act, gs);
+                            if (same == act) {
+                                const int sum = __reduce_add_sync(act, n);
+                                if (lane == __ffs(act) - 1 && sum)
+                                    atomicAdd(a.chg_cnt + (int64_t)gs * a.cnt_stride, (unsigned long long)sum);
+                            } else if (n) {
+                                atomicAdd(a.chg_cnt + (int64_t)gs * a.cnt_stride, (unsigned long long)n);
+                            }
+                        }
+                    }
                 }
                 continue;
             }
@@ -845,6 +933,7 @@ struct TcLayer {
     bool f16 = false;    // fp16 operands (kind::f16): Cp counts 4-byte units of the fp16 shadow input
     bool i8 = false;     // kind::i8 over RGBX camera bytes (Cp = 1 unit per pixel), digit filters
     int Opad = 0;        // i8: output channels padded to 4 (digit column stride)
+    int grpR = 1, grpN = 0;  // pixel groups: R adjacent output pixels per row, column stride per sub-pixel
     float* qsc = nullptr;   // i8: per-channel scale / 255
     int ovl_s = 0, ovl_b0 = 0, ovl_b1 = 0;
     int max_ctas = 0;    // persistent grid cap (0: one per SM x ctas_per_sm)
@@ -885,8 +974,15 @@ void set_smem_attrs() {
 }
 }  // namespace
 
+int tc_group_width(const TcLayer& t) { return t.grpR; }
+
+bool tc_group_supported(const cbx_geom& g, int R) {
+    return R > 1 && R <= 4 && g.strideH == 1 && g.strideW == 1 && g.inChannels <= 4 &&
+           R * round_up(g.outChannels, 32) <= 256 && g.kernelH * (g.kernelW + R - 1) <= 8 * 64;
+}
+
 std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats, int pair_mode, bool f16,
-                                                       bool i8) {
+                                                       bool i8, int grpR) {
     std::unique_ptr<TcLayer, TcLayerDeleter> t(new TcLayer);
     t->g = g;
     if (i8) {
@@ -929,9 +1025,15 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     // the gather's address arithmetic is the same for both operand types
     t->f16 = f16;
     t->Cp = f16 ? (int)round_up(g.inChannels, 8) / 2 : (int)round_up(g.inChannels, 4);
-    const int nchunks = g.kernelH * g.kernelW * (t->Cp / 4);
+    if (grpR > 1 && (f16 || pair_mode > 0 || tail_floats > 0 || !tc_group_supported(g, grpR))) grpR = 1;
+    t->grpR = grpR;
+    // pixel groups: K = kh x (kw + R - 1) window taps; sub-pixel j's outputs in
+    // columns [j * grpN, j * grpN + O), grpN = O rounded up to 32 (the
+    // epilogue's tcgen05.ld granularity)
+    const int nchunks = g.kernelH * (g.kernelW + grpR - 1) * (t->Cp / 4);
     t->NKB = (nchunks + kChunksPerKB - 1) / kChunksPerKB;
-    t->Npad = (int)round_up(g.outChannels, 16);
+    t->grpN = grpR > 1 ? (int)round_up(g.outChannels, 32) : 0;
+    t->Npad = grpR > 1 ? grpR * t->grpN : (int)round_up(g.outChannels, 16);
     // N > 256 needs two MMAs per K-step; split evenly (304 = 160 + 144, not
     // 256 + 48): a narrow instruction re-reads the whole A slice for few
     // columns and is shared-memory-bound, a balanced pair is not.
@@ -1134,6 +1236,29 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
         CBX_CUDA(cudaStreamSynchronize(st));
         return;
     }
+    if (t.grpR > 1) {
+        // pixel groups (tf32, 4-channel input, C4 = 1): chunk J = kj * span + w
+        // holds the 4 channels of window column w; B row j * grpN + o carries
+        // filter o shifted by j: K[o][c][kj][w - j] for 0 <= w - j < kw
+        const int span = g.kernelW + t.grpR - 1;
+        std::vector<float> img((size_t)t.NKB * t.Brows * kKBlock, 0.0f);
+        for (int j = 0; j < t.grpR; ++j)
+            for (int o = 0; o < g.outChannels; ++o) {
+                const int row = j * t.grpN + o;
+                for (int kj = 0; kj < g.kernelH; ++kj)
+                    for (int w = 0; w < span; ++w) {
+                        const int ki = w - j;
+                        if (ki < 0 || ki >= g.kernelW) continue;
+                        const int J = kj * span + w, kb = J / kChunksPerKB, jj = J % kChunksPerKB;
+                        for (int c = 0; c < g.inChannels; ++c)
+                            img[(size_t)kb * t.Brows * kKBlock + (size_t)row * kKBlock + ((jj ^ (row & 7)) * 4) + c] =
+                                round_tf32(K[(size_t)o * Kref + ((size_t)c * g.kernelH + kj) * g.kernelW + ki]);
+                    }
+            }
+        CBX_CUDA(cudaMemcpyAsync(t.Bw, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+        CBX_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
     std::vector<float> img((size_t)ranks * t.NKB * t.Brows * kKBlock, 0.0f);
     for (int n = 0; n < g.outChannels; ++n) {
         int rank, row;
@@ -1158,7 +1283,6 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
 void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float* bias, const int32_t* idx,
                     const int* count, int64_t full_count, bool relu, BitMask chg, float tau,
                     unsigned long long* cnt, int cstride, int S, cudaStream_t st, const TcTail* tail) {
-    (void)S;
     if (in.Cp != t.Cp) throw Error(CBX_E_SHAPE, "tcgen05 conv: input channel stride mismatch");
     TcArgs a{};
     a.in = in.d;
@@ -1206,13 +1330,24 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
         a.fd_howo = FastDiv::make((uint32_t)std::min<int64_t>(HoWo, 0x7fffffff));
         a.fd_wo = FastDiv::make((uint32_t)out.W);
     }
+    a.grp_R = t.grpR;
+    a.grp_N = t.grpN;
+    if (t.grpR > 1) {
+        // full mode walks every group; entries carry gid << 4 (below 2^31)
+        a.Gw = (out.W + t.grpR - 1) / t.grpR;
+        a.fd_gplane = FastDiv::make((uint32_t)(out.H * a.Gw));
+        a.fd_gw = FastDiv::make((uint32_t)a.Gw);
+        a.full_count = full_count = (int64_t)S * out.H * a.Gw;
+        if (full_count >= ((int64_t)1 << 27)) throw Error(CBX_E_ARG, "tcgen05 conv: too many pixel groups");
+        if (in.Cp != 4) throw Error(CBX_E_SHAPE, "tcgen05 conv: pixel groups need a 4-channel input");
+    }
     static const bool no_tap4x7 = std::getenv("CBX_TC_NO_TAP4X7") != nullptr;  // (tuning)
-    a.tap4x7 = !no_tap4x7 && in.Cp == 4 && t.g.kernelH == 7 && t.g.kernelW == 7 && t.NKB == 7;
+    a.tap4x7 = !no_tap4x7 && in.Cp == 4 && t.g.kernelH == 7 && t.g.kernelW == 7 && t.NKB == 7 && t.grpR == 1;
     // (8-row x 4-chunk gather: conflict-free but measured slower than the
     // row-lane tap4x7 gather on the paper's layer 2, 50 vs 46 us per lane-frame;
     // CBX_TC_XROW=1 selects it, tuning)
     static const bool xrow = std::getenv("CBX_TC_XROW") != nullptr;
-    a.xrow = xrow && in.Cp == 4 && !t.f16 && !t.pair;
+    a.xrow = xrow && in.Cp == 4 && !t.f16 && !t.pair && t.grpR == 1;
     a.ovl_s = t.ovl_s;
     a.ovl_b0 = t.ovl_b0;
     a.ovl_b1 = t.ovl_b1;
@@ -1230,7 +1365,7 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     if (tail) a.tail = *tail;
     const int tc = (tail && tail->n) ? (tail->cout[0] <= 8 ? 8 : 16) : 0;
     static const int rowlane_env = std::getenv("CBX_TC_ROWLANE") ? std::atoi(std::getenv("CBX_TC_ROWLANE")) : -1;
-    const bool rowlane = rowlane_env >= 0 ? rowlane_env != 0 : in.Cp <= 4;  // (env: tuning)
+    const bool rowlane = t.grpR > 1 || (rowlane_env >= 0 ? rowlane_env != 0 : in.Cp <= 4);  // (env: tuning)
     if (t.pair) {
         const int64_t max_tiles = (full_count + 2 * tc::kTileM - 1) / (2 * tc::kTileM);
         int64_t ccap = t.max_clusters;

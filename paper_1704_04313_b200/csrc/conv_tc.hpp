@@ -44,8 +44,14 @@ bool tc_supported(const cbx_geom& g);
 // frame (TensorView with Cp = 1: one 4-byte unit per pixel), filters as three
 // signed base-256 digits of a 22-bit fixed-point weight (relative weight
 // error <= 2^-23 of the channel's largest weight, exact integer accumulation).
+// grpR > 1: pixel groups -- each tensor-core row is grpR horizontally
+// adjacent output pixels (stride-1 layers with a <= 4-channel fp32 input,
+// tf32, no fused tail); the update lists hold group entries (gid << 4 | mask)
+// from dilate_compact with R = grpR. Falls back to 1 when unsupported.
 std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats = 0, int pair_mode = -1,
-                                                       bool f16 = false, bool i8 = false);
+                                                       bool f16 = false, bool i8 = false, int grpR = 1);
+int tc_group_width(const TcLayer& t);
+bool tc_group_supported(const cbx_geom& g, int R);
 bool tc_is_f16(const TcLayer& t);
 bool tc_is_i8(const TcLayer& t);
 bool tc_i8_supported(const cbx_geom& g);

@@ -245,7 +245,7 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
                 const bool f16 = precision_ == CBX_PREC_F16 && g.outChannels > 128 &&
                                  layers_[k - 1].kind == CBX_MAXPOOL;
                 if (f16) f16_layers_.push_back(k);
-                tc_[k] = make_tc_layer(g, tail_floats, -1, f16);
+                tc_[k] = make_tc_layer(g, tail_floats, -1, f16, false, group_width_for(g));
                 // narrow layer on a 4-channel input (paper layer 2): groups of
                 // R adjacent output pixels per tensor-core row, fp16 operands
                 // converted while gathering. Opt-in (CBX_MPR_F16=1): on the
@@ -329,7 +329,23 @@ Engine::~Engine() {
 int Engine::list_group(int k, bool u8) const {
     if (k == 0 && u8 && mpr8_) return mpr_group_width(*mpr8_);
     if (mpr_[k]) return mpr_group_width(*mpr_[k]);
+    if (tc_[k]) return tc_group_width(*tc_[k]);
     return 1;
+}
+
+// Pixel groups for a narrow tcgen05 layer on a 4-channel input (the paper's
+// layer 2): R adjacent output pixels per tensor-core row share their window
+// (R = 4: K = 7 x 10 taps instead of 4 x 7 x 7, N = 4 x 64) -- 2.8x fewer
+// gathered bytes and 1.7x fewer MMA cycles per pixel. Opt-in (CBX_TC_GROUP =
+// 2 or 4): on the paper's layer 2 the kernel time did not follow (8-stream
+// lane-frame: 49 / 47 / 53 us for R = 4 / 2 / 1) and the two-lane step was
+// best with R = 1 (31.7k vs 31.0k frames/s). make_tc_layer falls back to 1
+// where unsupported.
+int Engine::group_width_for(const cbx_geom& g) const {
+    int R = 1;
+    if (const char* e = std::getenv("CBX_TC_GROUP")) R = std::max(1, std::min(4, std::atoi(e)));
+    while (R > 1 && !tc_group_supported(g, R)) R /= 2;
+    return R;
 }
 
 int Engine::layer_operands(int layer) const {
@@ -504,7 +520,8 @@ void Engine::build_plan(Plan& p, bool baseline) {
         if (!is_conv(l.kind)) continue;
         const int Ho = dims_[6 * k + 4], Wo = dims_[6 * k + 5];
         if (l.kind == CBX_CONV && identity_geom(l.geom) && p.upd_owner[k] >= 0 &&
-            is_conv(layers_[p.upd_owner[k]].kind) && !mpr_[p.upd_owner[k]] && !(p.upd_owner[k] == 0 && mpr8_)) {
+            is_conv(layers_[p.upd_owner[k]].kind) && list_group(p.upd_owner[k], true) == 1 &&
+            list_group(p.upd_owner[k], false) == 1) {  // (a pixel-group list cannot be reused as a pixel list)
             const int j = p.upd_owner[k];
             p.idx_src[k] = p.idx_src[j] >= 0 ? p.idx_src[j] : j;
             continue;
@@ -1492,7 +1509,8 @@ void Engine::set_option(int option, int value) {
             const int tail_floats = te > 0 ? (c1 <= 8 ? 8 : 16) * g.outChannels : 0;
             std::vector<float> K((size_t)g.outChannels * g.inChannels * g.kernelH * g.kernelW);
             CBX_CUDA(cudaMemcpy(K.data(), dK_[k], K.size() * sizeof(float), cudaMemcpyDeviceToHost));
-            tc_[k] = make_tc_layer(g, tail_floats, value, tc_is_f16(*tc_[k]));
+            tc_[k] = make_tc_layer(g, tail_floats, value, tc_is_f16(*tc_[k]), false,
+                                   tail_floats ? 1 : group_width_for(g));
             tc_load_weights(*tc_[k], K.data(), stream_);
         }
     } else if (option == CBX_OPT_FUSE_TAIL) {

@@ -218,3 +218,30 @@ def test_mpr_f16_layer_vs_exact(gpu, orc, monkeypatch, cin, h, w, layer, magnitu
         d, u = net.trace(0)
         _, ou = onet.trace(0)
         assert np.array_equal(u, ou)
+
+
+GROUP_CASES = [c for c in MPR_CASES if c[3].get("strideH", 1) == 1]
+
+
+@pytest.mark.parametrize("R", ["2", "4"])
+@pytest.mark.parametrize("maxctas", [None, "2"])
+@pytest.mark.parametrize("cin,h,w,layer", GROUP_CASES)
+def test_tc_pixel_groups_vs_exact(gpu, orc, monkeypatch, cin, h, w, layer, maxctas, R):
+    """conv_tc with pixel groups (CBX_TC_GROUP: R adjacent output pixels per
+    tensor-core row, kind::tf32) within the tf32 bound of the exact result,
+    full and change-based frames; the change-based update lists are group
+    lists, their traces equal the oracle's."""
+    monkeypatch.setenv("CBX_TC_GROUP", R)
+    if maxctas:
+        monkeypatch.setenv("CBX_TC_MAXCTAS", maxctas)
+    spec = two_layer(cin, h, w, layer)
+    wts = orc.generate_weights(spec, 19)
+    onet = orc.load_network(spec, wts)
+    net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="tf32")
+    assert net.layer_operands(1) == "tf32"
+    cfg = dict(channels=3, height=h, width=w, sprites=[(5, 2, 0.9)], noise=0.02, seed=6)
+    _check_layer(gpu, orc, net, onet, spec, wts, cfg, 1, cin, False, frames=4)
+    if layer["kind"] == "CBCONV":
+        _, u = net.trace(0)
+        _, ou = onet.trace(0)
+        assert np.array_equal(u, ou)
