@@ -516,6 +516,7 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
         return (t | (t >> 2)) & 0x11111111u;
     };
     const int y0 = (int)(w0 / out.wpr), wr0 = (int)(w0 - (int64_t)y0 * out.wpr);
+    int wy[WPT], ww[WPT];  // row / word of each of the thread's words (kept for the list writes)
 #pragma unroll
     for (int i = 0; i < WPT; ++i) {
         int y = y0, w = wr0 + i;
@@ -523,6 +524,8 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
             y += w / out.wpr;
             w -= (w / out.wpr) * out.wpr;
         }
+        wy[i] = y;
+        ww[i] = w;
         uint32_t word = 0;
         if (y < out.H && w < in.wpr) {
             if (identity) {
@@ -577,8 +580,7 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
             const uint32_t wsrc = __shfl_sync(0xffffffffu, word, src);
             const uint32_t gsrc = __shfl_sync(0xffffffffu, gb, src);
             const int64_t osrc = __shfl_sync(0xffffffffu, o, src);
-            const int64_t wglob = __shfl_sync(0xffffffffu, w0 + i, src);
-            const int ys = (int)(wglob / out.wpr), ws = (int)(wglob - (int64_t)ys * out.wpr);
+            const int ys = __shfl_sync(0xffffffffu, wy[i], src), ws = __shfl_sync(0xffffffffu, ww[i], src);
             const int bit = lane * R;
             if (bit < 32 && ((gsrc >> bit) & 1u)) {
                 const int64_t pos = osrc + __popc(gsrc & ((1u << bit) - 1u));
