@@ -169,19 +169,34 @@ __global__ void __launch_bounds__(256) detect_c3_kernel(const float* const* cur,
 // previous frame's expansion).
 //   MODE 0: threshold test (CBCONV); MODE 1: any byte differs (updated
 //   pixels of a non-CB first layer); MODE 2: full frame, expansion only.
-// SWAR: nonzero iff some byte of x is >= t (1 <= t <= 256; t = 256: never).
-// Bytes below 128 carry into bit 7 when (b & 0x7f) + 0x80 - t overflows 7
-// bits; bytes with bit 7 set need their low 7 bits compared with t - 128.
-__device__ __forceinline__ uint32_t any_byte_ge(uint32_t x, int t) {
-    if (t > 255) return 0u;
-    const uint32_t lo7 = x & 0x7f7f7f7fu;
-    if (t <= 128) return ((lo7 + (uint32_t)(0x80 - t) * 0x01010101u) | x) & 0x80808080u;
-    return (lo7 + (uint32_t)(0x80 - (t - 128)) * 0x01010101u) & x & 0x80808080u;
-}
+// SWAR "some byte of x is >= t" (1 <= t <= 256; t = 256: never), branch
+// free with per-launch constants (ByteGe::make on the host): bytes below 128
+// carry into bit 7 when (b & 0x7f) + 0x80 - t overflows 7 bits (t <= 128:
+// OR with x's own bit 7); for t > 128 a byte needs bit 7 set AND its low 7
+// bits >= t - 128 (AND with x).
+struct ByteGe {
+    uint32_t add, and_sel, mask;  // and_sel: ~0 selects the AND form
+    static ByteGe make(int t) {
+        ByteGe b{0u, 0u, 0x80808080u};
+        if (t > 255) {
+            b.mask = 0u;
+        } else if (t <= 128) {
+            b.add = (uint32_t)(0x80 - t) * 0x01010101u;
+        } else {
+            b.add = (uint32_t)(0x80 - (t - 128)) * 0x01010101u;
+            b.and_sel = 0xffffffffu;
+        }
+        return b;
+    }
+    __device__ __forceinline__ uint32_t test(uint32_t x) const {
+        const uint32_t r = (x & 0x7f7f7f7fu) + add;
+        return ((r & x) | ((r | x) & ~and_sel)) & mask;
+    }
+};
 
 template <int MODE>
 __global__ void __launch_bounds__(256) detect_rgb8_kernel(const uint8_t* const* cur, const uint8_t* const* prev, int H,
-                                                          int W, float tau, int dlo, int dhi, BitMask m,
+                                                          int W, float tau, ByteGe ge_lo, ByteGe ge_hi, BitMask m,
                                                           unsigned long long* cnt, int cstride, Rgbx8View x) {
     pdl_entry();
     // px / 255.0f of every byte value: the reference's read_ppm decode
@@ -215,30 +230,36 @@ __global__ void __launch_bounds__(256) detect_rgb8_kernel(const uint8_t* const* 
                 cw[4] = c1.x; cw[5] = c1.y; cw[6] = c1.z; cw[7] = c1.w;
                 cw[8] = c2.x; cw[9] = c2.y; cw[10] = c2.z; cw[11] = c2.w;
             }
+            uint32_t anyd = 1u;  // full frames: every group is expanded
             if constexpr (MODE != 2) {
                 const uint4 p0 = __ldcs(b + q), p1 = __ldcs(b + q + 1), p2 = __ldcs(b + q + 2);
                 pw[0] = p0.x; pw[1] = p0.y; pw[2] = p0.z; pw[3] = p0.w;
                 pw[4] = p1.x; pw[5] = p1.y; pw[6] = p1.z; pw[7] = p1.w;
                 pw[8] = p2.x; pw[9] = p2.y; pw[10] = p2.z; pw[11] = p2.w;
-            }
-            // RGBX expansion: pixel p = bytes 3p..3p+2 of the group
+                anyd = 0u;
 #pragma unroll
-            for (int p = 0; p < 16; ++p) {
-                const int bi = 3 * p, wi = bi >> 2, r = bi & 3;
-                const uint32_t sel = (uint32_t)(r | ((r + 1) << 4) | ((r + 2) << 8));
-                o[p] = __byte_perm(cw[wi], wi + 1 < 12 ? cw[wi + 1] : 0u, sel) & 0x00ffffffu;
-                if constexpr (MODE != 2) {
-                    op[p] = __byte_perm(pw[wi], wi + 1 < 12 ? pw[wi + 1] : 0u, sel) & 0x00ffffffu;
-                    // |a - b| per channel byte: >= dhi is changed for every byte
-                    // pair, < dlo for none; in between decide exactly below
-                    const uint32_t ad = __vabsdiffu4(o[p], op[p]);
-                    if (any_byte_ge(ad, dhi)) flags |= 1u << p;
-                    else if (any_byte_ge(ad, dlo)) amb |= 1u << p;
-                }
+                for (int i = 0; i < 12; ++i) anyd |= cw[i] ^ pw[i];
             }
-            // the RGBX buffer holds the previous frame: only groups whose
-            // bytes differ are rewritten (a static camera rewrites a few %)
-            if (MODE == 2 || any) {
+            // A group whose 48 bytes equal the previous frame's has no change
+            // and its RGBX pixels (the buffer holds the previous frame's
+            // expansion) are already right: only changed groups are expanded,
+            // tested and rewritten (a static camera changes a few %).
+            if (anyd) {
+                // RGBX expansion: pixel p = bytes 3p..3p+2 of the group
+#pragma unroll
+                for (int p = 0; p < 16; ++p) {
+                    const int bi = 3 * p, wi = bi >> 2, r = bi & 3;
+                    const uint32_t sel = (uint32_t)(r | ((r + 1) << 4) | ((r + 2) << 8));
+                    o[p] = __byte_perm(cw[wi], wi + 1 < 12 ? cw[wi + 1] : 0u, sel) & 0x00ffffffu;
+                    if constexpr (MODE != 2) {
+                        op[p] = __byte_perm(pw[wi], wi + 1 < 12 ? pw[wi + 1] : 0u, sel) & 0x00ffffffu;
+                        // |a - b| per channel byte: >= dhi is changed for every
+                        // byte pair, < dlo for none; in between decide exactly below
+                        const uint32_t ad = __vabsdiffu4(o[p], op[p]);
+                        if (ge_hi.test(ad)) flags |= 1u << p;
+                        else if (ge_lo.test(ad)) amb |= 1u << p;
+                    }
+                }
                 uint4* xo = reinterpret_cast<uint4*>(xs + (int64_t)(y + x.hh) * x.Wp + x.hw + 16 * gx);
                 xo[0] = make_uint4(o[0], o[1], o[2], o[3]);
                 xo[1] = make_uint4(o[4], o[5], o[6], o[7]);
@@ -331,11 +352,11 @@ void launch_detect_rgb8(const uint8_t* const* cur, const uint8_t* const* prev, i
     int dlo = 256, dhi = 256;
     if (mode != 2) rgb8_tau_bounds(tau, mode, dlo, dhi);
     if (mode == 0)
-        launch_k(detect_rgb8_kernel<0>, grid, dim3(256), 0, st, cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
+        launch_k(detect_rgb8_kernel<0>, grid, dim3(256), 0, st, cur, prev, H, W, tau, ByteGe::make(dlo), ByteGe::make(dhi), m, cnt, cstride, x);
     else if (mode == 1)
-        launch_k(detect_rgb8_kernel<1>, grid, dim3(256), 0, st, cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
+        launch_k(detect_rgb8_kernel<1>, grid, dim3(256), 0, st, cur, prev, H, W, tau, ByteGe::make(dlo), ByteGe::make(dhi), m, cnt, cstride, x);
     else
-        launch_k(detect_rgb8_kernel<2>, grid, dim3(256), 0, st, cur, prev, H, W, tau, dlo, dhi, m, cnt, cstride, x);
+        launch_k(detect_rgb8_kernel<2>, grid, dim3(256), 0, st, cur, prev, H, W, tau, ByteGe::make(dlo), ByteGe::make(dhi), m, cnt, cstride, x);
 }
 
 void launch_detect_bits(const float* const* cur, const float* const* prev, int S, int C, int H, int W, float tau,
