@@ -523,7 +523,8 @@ __global__ void __launch_bounds__(kDcThreads) dilate_compact_kernel(BitMask in, 
             const int w = i % in.wpr;
             const uint32_t prev = w > 0 ? rows[i - 1] : 0u;
             const uint32_t next = w + 1 < in.wpr ? rows[i + 1] : 0u;
-            hrows[i] = hdilate(prev, rows[i], next, kw, pw);
+            const uint32_t cur = rows[i];
+            hrows[i] = (prev | cur | next) ? hdilate(prev, cur, next, kw, pw) : 0u;  // (most words are empty)
         }
         __syncthreads();
     }
