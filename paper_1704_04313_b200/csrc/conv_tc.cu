@@ -182,6 +182,13 @@ struct TcArgs {
     // columns j * grp_N); list entries (gid << 4 | mask), gid over Ho x Gw
     int grp_R, grp_N, Gw;
     FastDiv fd_gplane, fd_gw;
+    // packed fp16 input (pack_cpr > 0): channels not padded, each kernel row's
+    // kw x C halves gathered as pack_cpr contiguous 16-byte chunks (the last
+    // may run into the next pixel: zero weights there); `in2` is the same
+    // shadow shifted by 8 bytes, used for windows that start 8-byte aligned
+    int pack_cpr;
+    const float* in2;
+    int kinst_last;  // MMA instructions of the last K-block (its 32-byte K steps that hold data)
     int f16;     // operands are fp16 (kind::f16): the input is an fp16 shadow tensor
                  // addressed in 4-byte units (in_Cp = fp16 channels / 2)
     int relu;
@@ -320,6 +327,11 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
         int off = -1;
         if (I8) {
             // (unused: the register-staged gather computes its offsets)
+        } else if (a.pack_cpr > 0) {
+            if (j < a.kh * a.pack_cpr) {
+                const int kj = j / a.pack_cpr, i = j - kj * a.pack_cpr;
+                off = kj * a.in_Wp * a.in_Cp + 4 * i;  // 4-byte units from the window origin
+            }
         } else if (a.grp_R > 1) {
             const int span = a.kw + a.grp_R - 1;  // window columns per kernel row
             if (j < a.kh * span * C4) {
@@ -605,8 +617,11 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                     const int64_t g = gcur[i];
                     int s, p, y, x;
                     pixel_of(a, g, HoWo, s, p, y, x);
-                    base[i] = a.in + (int64_t)s * a.in_ss +
-                              ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
+                    const int64_t u = (int64_t)s * a.in_ss +
+                                      ((int64_t)(y * a.sh - a.ph + a.in_hh) * a.in_Wp + (x * a.sw - a.pw + a.in_hw)) * a.in_Cp;
+                    // packed: a window origin on an odd 8-byte boundary reads
+                    // the 8-byte-shifted copy, where it is 16-byte aligned
+                    base[i] = (a.pack_cpr > 0 && (u & 2)) ? a.in2 + u + 2 : a.in + u;
                 }
             }
             for (int kb = 0; kb < a.NKB; ++kb, rg.next(NS)) {
@@ -678,9 +693,11 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                     // consumer_wait, then the MMAs); the fence cost 1-2 % of L3
                     tc_fence_after();
                     const uint64_t ad = a_desc0 + st * a_st, bd = b_desc0 + st * b_st;
+                    const int nk = kb + 1 == a.NKB ? a.kinst_last : kKBlock / 8;
                     if (elect_one()) {
 #pragma unroll
                         for (int k = 0; k < kKBlock / 8; ++k) {
+                            if (k >= nk) break;
                             const uint32_t accum = (kb | k) ? 1u : 0u;
                             if constexpr (I8) {
                                 mma_i8(d, ad + 2 * k, bd + 2 * k, id0, accum);
@@ -934,6 +951,8 @@ struct TcLayer {
     bool i8 = false;     // kind::i8 over RGBX camera bytes (Cp = 1 unit per pixel), digit filters
     int Opad = 0;        // i8: output channels padded to 4 (digit column stride)
     int grpR = 1, grpN = 0;  // pixel groups: R adjacent output pixels per row, column stride per sub-pixel
+    int pack_cpr = 0;        // packed fp16 input: 16-byte chunks per kernel row (0: channels padded to 8)
+    int kinst_last = 4;
     float* qsc = nullptr;   // i8: per-channel scale / 255
     int ovl_s = 0, ovl_b0 = 0, ovl_b1 = 0;
     int max_ctas = 0;    // persistent grid cap (0: one per SM x ctas_per_sm)
@@ -975,6 +994,7 @@ void set_smem_attrs() {
 }  // namespace
 
 int tc_group_width(const TcLayer& t) { return t.grpR; }
+int tc_input_cp(const TcLayer& t) { return t.Cp; }
 
 bool tc_group_supported(const cbx_geom& g, int R) {
     return R > 1 && R <= 4 && g.strideH == 1 && g.strideW == 1 && g.inChannels <= 4 &&
@@ -982,7 +1002,7 @@ bool tc_group_supported(const cbx_geom& g, int R) {
 }
 
 std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats, int pair_mode, bool f16,
-                                                       bool i8, int grpR) {
+                                                       bool i8, int grpR, bool pack) {
     std::unique_ptr<TcLayer, TcLayerDeleter> t(new TcLayer);
     t->g = g;
     if (i8) {
@@ -1030,8 +1050,17 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     // pixel groups: K = kh x (kw + R - 1) window taps; sub-pixel j's outputs in
     // columns [j * grpN, j * grpN + O), grpN = O rounded up to 32 (the
     // epilogue's tcgen05.ld granularity)
-    const int nchunks = g.kernelH * (g.kernelW + grpR - 1) * (t->Cp / 4);
+    int nchunks = g.kernelH * (g.kernelW + grpR - 1) * (t->Cp / 4);
+    if (f16 && pack && g.inChannels % 2 == 0 && pair_mode <= 0 && grpR == 1) {
+        // packed fp16 operands: a kernel row's kw x C halves are contiguous in
+        // the unpadded shadow (Cp = C/2 units) -> ceil(kw C 2 / 16) chunks per
+        // kernel row instead of kw ceil(C / 8) (paper layer 3: 46 vs 49)
+        t->Cp = g.inChannels / 2;
+        t->pack_cpr = (g.kernelW * g.inChannels * 2 + 15) / 16;
+        nchunks = g.kernelH * t->pack_cpr;
+    }
     t->NKB = (nchunks + kChunksPerKB - 1) / kChunksPerKB;
+    t->kinst_last = (nchunks - kChunksPerKB * (t->NKB - 1) + 1) / 2;  // 2 chunks (32 B of K) per instruction
     t->grpN = grpR > 1 ? (int)round_up(g.outChannels, 32) : 0;
     t->Npad = grpR > 1 ? grpR * t->grpN : (int)round_up(g.outChannels, 16);
     // N > 256 needs two MMAs per K-step; split evenly (304 = 160 + 144, not
@@ -1205,6 +1234,29 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
         CBX_CUDA(cudaStreamSynchronize(st));
         return;
     }
+    if (t.f16 && t.pack_cpr > 0) {
+        for (size_t i = 0; i < (size_t)g.outChannels * Kref; ++i)
+            if (std::fabs(K[i]) > 65504.0f)
+                throw Error(CBX_E_ARG, "a filter weight of a kind::f16 layer exceeds the fp16 range (|w| > 65504); "
+                                       "create the context with CBX_PREC_TF32");
+        // packed fp16 image: chunk J = kj * pack_cpr + i holds halves
+        // h = 8 i + e of kernel row kj's window (tap ki = h / C, channel
+        // c = h % C; h >= kw C: next pixel, zero weight)
+        const int C = g.inChannels;
+        std::vector<__half> img((size_t)t.NKB * t.Brows * 64, __float2half_rn(0.0f));
+        for (int n = 0; n < g.outChannels; ++n)
+            for (int kj = 0; kj < g.kernelH; ++kj)
+                for (int h = 0; h < g.kernelW * C; ++h) {
+                    const int ki = h / C, c = h % C;
+                    const int J = kj * t.pack_cpr + h / 8, e = h % 8;
+                    const int kb = J / kChunksPerKB, jj = J % kChunksPerKB;
+                    img[(size_t)kb * t.Brows * 64 + (size_t)n * 64 + ((jj ^ (n & 7)) * 8) + e] =
+                        __float2half_rn(K[(size_t)n * Kref + ((size_t)c * g.kernelH + kj) * g.kernelW + ki]);
+                }
+        CBX_CUDA(cudaMemcpyAsync(t.Bw, img.data(), img.size() * sizeof(__half), cudaMemcpyHostToDevice, st));
+        CBX_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
     if (t.f16) {
         // fp16 image (round to nearest even): chunk J = tap * C4 + c4 holds
         // channels 8*c4 .. 8*c4+7 of that tap; half (row, kb*64 + j*8 + e) at
@@ -1282,7 +1334,8 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
 
 void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float* bias, const int32_t* idx,
                     const int* count, int64_t full_count, bool relu, BitMask chg, float tau,
-                    unsigned long long* cnt, int cstride, int S, cudaStream_t st, const TcTail* tail) {
+                    unsigned long long* cnt, int cstride, int S, cudaStream_t st, const TcTail* tail,
+                    const float* in_shifted) {
     if (in.Cp != t.Cp) throw Error(CBX_E_SHAPE, "tcgen05 conv: input channel stride mismatch");
     TcArgs a{};
     a.in = in.d;
@@ -1332,6 +1385,11 @@ void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float
     }
     a.grp_R = t.grpR;
     a.grp_N = t.grpN;
+    a.pack_cpr = t.pack_cpr;
+    a.in2 = in_shifted;
+    a.kinst_last = t.kinst_last;
+    if (t.pack_cpr > 0 && (!in_shifted || (in.Wp & 1) || (in.ss & 3)))
+        throw Error(CBX_E_ARG, "tcgen05 conv: packed fp16 input needs the shifted copy, an even row pitch and 16-byte streams");
     if (t.grpR > 1) {
         // full mode walks every group; entries carry gid << 4 (below 2^31)
         a.Gw = (out.W + t.grpR - 1) / t.grpR;

@@ -48,8 +48,12 @@ bool tc_supported(const cbx_geom& g);
 // adjacent output pixels (stride-1 layers with a <= 4-channel fp32 input,
 // tf32, no fused tail); the update lists hold group entries (gid << 4 | mask)
 // from dilate_compact with R = grpR. Falls back to 1 when unsupported.
+// pack: fp16 operands from an UNPADDED shadow (Cp = C/2 4-byte units, C even)
+// plus the same shadow shifted by 8 bytes (in_shifted of launch_conv_tc):
+// each kernel row's kw x C halves are gathered as contiguous 16-byte chunks.
 std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int tail_floats = 0, int pair_mode = -1,
-                                                       bool f16 = false, bool i8 = false, int grpR = 1);
+                                                       bool f16 = false, bool i8 = false, int grpR = 1, bool pack = false);
+int tc_input_cp(const TcLayer& t);
 int tc_group_width(const TcLayer& t);
 bool tc_group_supported(const cbx_geom& g, int R);
 bool tc_is_f16(const TcLayer& t);
@@ -60,6 +64,6 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st);
 void launch_conv_tc(const TcLayer& t, TensorView in, TensorView out, const float* bias,
                     const int32_t* idx, const int* count, int64_t full_count, bool relu,
                     BitMask chg, float tau, unsigned long long* cnt, int cstride, int S,
-                    cudaStream_t st, const TcTail* tail = nullptr);
+                    cudaStream_t st, const TcTail* tail = nullptr, const float* in_shifted = nullptr);
 
 }  // namespace cbx

@@ -149,6 +149,7 @@ struct Engine::Plan {
     bool baseline = false;
     std::vector<TensorView> T;      // nl+1; T[0] = frame (planar) unless ingested
     std::vector<TensorView> T16;    // nl+1; fp16 shadows (4-byte channel units) of kind::f16 conv inputs
+    std::vector<TensorView> T16b;   // packed shadows: the same shifted by 8 bytes (d[v + 2] = T16.d[v])
     bool ingest = false;            // first layer is not a conv: frame copied to HWC T[0]
     std::vector<BitMask> chg;       // nl+1
     std::vector<bool> chg_by_conv;  // chg written with 1s only -> cleared per frame
@@ -245,7 +246,7 @@ Engine::Engine(const cbx_net_desc& net, int device, int S, int precision)
                 const bool f16 = precision_ == CBX_PREC_F16 && g.outChannels > 128 &&
                                  layers_[k - 1].kind == CBX_MAXPOOL;
                 if (f16) f16_layers_.push_back(k);
-                tc_[k] = make_tc_layer(g, tail_floats, -1, f16, false, group_width_for(g));
+                tc_[k] = make_tc_layer(g, tail_floats, -1, f16, false, group_width_for(g), pack_f16(k));
                 // narrow layer on a 4-channel input (paper layer 2): groups of
                 // R adjacent output pixels per tensor-core row, fp16 operands
                 // converted while gathering. Opt-in (CBX_MPR_F16=1): on the
@@ -341,6 +342,17 @@ int Engine::list_group(int k, bool u8) const {
 // lane-frame: 49 / 47 / 53 us for R = 4 / 2 / 1) and the two-lane step was
 // best with R = 1 (31.7k vs 31.0k frames/s). make_tc_layer falls back to 1
 // where unsupported.
+// fp16 operands from the unpadded shadow (packed kernel rows) when the
+// input's padded row pitch is even (CBX_TC_PACK=0 keeps the padded layout;
+// tuning): the paper's layer 3 gathers 46 instead of 49 chunks per kernel
+// row, 41 instead of 43 K-blocks.
+bool Engine::pack_f16(int k) const {
+    const char* e = std::getenv("CBX_TC_PACK");
+    if (e && std::atoi(e) == 0) return false;
+    const int W = dims_[6 * k + 2];
+    return ((W + 2 * layers_[k].geom.padW) & 1) == 0;
+}
+
 int Engine::group_width_for(const cbx_geom& g) const {
     int R = 1;
     if (const char* e = std::getenv("CBX_TC_GROUP")) R = std::max(1, std::min(4, std::atoi(e)));
@@ -426,12 +438,20 @@ void Engine::build_plan(Plan& p, bool baseline) {
         alloc_tensor(k + 1);
     }
     p.T16.assign(nl + 1, TensorView{});
+    p.T16b.assign(nl + 1, TensorView{});
     for (int k : f16_layers_) {
+        // the layer's fp16 shadow: channels padded to 8, or packed (Cp = C/2
+        // units) plus a copy shifted by 8 bytes (T16b, element v + 2 = T16's v)
         TensorView v = p.T[k];
-        v.Cp = (int)round_up(v.C, 8) / 2;
+        v.Cp = tc_input_cp(*tc_[k]);
         v.ss = round_up((int64_t)v.Hp * v.Wp * v.Cp, 64);
-        v.d = p.alloc<float>((size_t)(v.ss * S));
+        v.d = p.alloc<float>((size_t)(v.ss * S) + 64);
         p.T16[k] = v;
+        if (v.Cp * 2 == v.C) {
+            TensorView b = v;
+            b.d = p.alloc<float>((size_t)(v.ss * S) + 64);
+            p.T16b[k] = b;
+        }
     }
     if (p.T[0].d == nullptr) {
         int c, h, w;
@@ -703,13 +723,13 @@ void Engine::record(Plan& p, bool full) {
                     t.labels = p.labels;
                     t.l_ss = (int64_t)lh_ * lw_;
                     launch_conv_tc(*tc_[k], p.T16[k].d ? p.T16[k] : p.T[k], p.T[k + 1], dBias_[k], idx, count, full_count, relu,
-                                   chg_next, tau_next, cnt_next, 2, S, st, &t);
+                                   chg_next, tau_next, cnt_next, 2, S, st, &t, p.T16b[k].d);
                     mark("conv_tc_tail", k);
                     p.fused_from = k;
                     break;
                 } else if (tc_[k] && !planar_in) {
                     launch_conv_tc(*tc_[k], p.T16[k].d ? p.T16[k] : p.T[k], p.T[k + 1], dBias_[k], idx, count, full_count, relu,
-                                   chg_next, tau_next, cnt_next, 2, S, st);
+                                   chg_next, tau_next, cnt_next, 2, S, st, nullptr, p.T16b[k].d);
                     mark("conv_tc", k);
                 } else {
                     ConvArgs a{};
@@ -759,6 +779,7 @@ void Engine::record(Plan& p, bool full) {
                 a.work_count = p.wcount_k.empty() ? nullptr : p.wcount_k[k];  // (sparse frames only)
                 a.count_zeroed = 1;
                 a.out16 = p.T16[k + 1];
+                a.out16b = p.T16b[k + 1];
                 a.f16_overflow = p.T16[k + 1].d ? p.ovf : nullptr;
                 launch_point_bits(a, st);
                 mark(a.relu ? "relu" : "pool", k);
@@ -1499,6 +1520,7 @@ void Engine::set_option(int option, int value) {
     }
     if (option == CBX_OPT_TC_PAIR) {
         if (value < -1 || value > 1) throw Error(CBX_E_ARG, "CBX_OPT_TC_PAIR takes -1, 0 or 1");
+        bool relayout = false;
         // rebuild every tcgen05 layer with the requested CTA grouping; the
         // filters come back from the device copy in the reference layout
         for (int k = 0; k < (int)layers_.size(); ++k) {
@@ -1509,9 +1531,20 @@ void Engine::set_option(int option, int value) {
             const int tail_floats = te > 0 ? (c1 <= 8 ? 8 : 16) * g.outChannels : 0;
             std::vector<float> K((size_t)g.outChannels * g.inChannels * g.kernelH * g.kernelW);
             CBX_CUDA(cudaMemcpy(K.data(), dK_[k], K.size() * sizeof(float), cudaMemcpyDeviceToHost));
+            const int cp_before = tc_input_cp(*tc_[k]);
             tc_[k] = make_tc_layer(g, tail_floats, value, tc_is_f16(*tc_[k]), false,
-                                   tail_floats ? 1 : group_width_for(g));
+                                   tail_floats ? 1 : group_width_for(g), pack_f16(k));
             tc_load_weights(*tc_[k], K.data(), stream_);
+            if (tc_input_cp(*tc_[k]) != cp_before) relayout = true;
+        }
+        if (relayout) {
+            // the fp16 shadow layout changed (CTA pairs read the padded one):
+            // new plans, and the next frame is a full evaluation
+            CBX_CUDA(cudaStreamSynchronize(stream_));
+            cb_.reset(new Plan);
+            build_plan(*cb_, false);
+            base_.reset();
+            has_history_ = false;
         }
     } else if (option == CBX_OPT_FUSE_TAIL) {
         fuse_tail_ = value != 0;

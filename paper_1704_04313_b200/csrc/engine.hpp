@@ -139,6 +139,7 @@ private:
     bool any_f16_ = false;  // some layer has fp16 operands: the plan keeps an overflow flag
     int list_group(int k, bool u8) const;  // group width of layer k's update list (1 = pixel indices)
     int group_width_for(const cbx_geom& g) const;
+    bool pack_f16(int k) const;
     void check_f16_overflow(const unsigned long long* hs, int engine);
     bool last_ovf_[2] = {false, false};
     // device counters of one frame: [nl][S][2] + the fp16 overflow flag

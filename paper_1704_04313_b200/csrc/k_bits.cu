@@ -882,8 +882,9 @@ __global__ void __launch_bounds__(kPtThreads) point_work_kernel(PointBitsArgs a,
                 uint2 hv;
                 hv.x = *reinterpret_cast<const uint32_t*>(&h01);
                 hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-                reinterpret_cast<uint2*>(a.out16.d + (int64_t)s * a.out16.ss +
-                                         ((int64_t)(y + a.out16.hh) * a.out16.Wp + x + a.out16.hw) * a.out16.Cp)[c4] = hv;
+                const int64_t u16 = (int64_t)s * a.out16.ss + ((int64_t)(y + a.out16.hh) * a.out16.Wp + x + a.out16.hw) * a.out16.Cp;
+                reinterpret_cast<uint2*>(a.out16.d + u16)[c4] = hv;
+                if (a.out16b.d) reinterpret_cast<uint2*>(a.out16b.d + u16 + 2)[c4] = hv;
             }
         }
         if (!FULL && a.chg.d) {
@@ -1021,8 +1022,10 @@ __global__ void __launch_bounds__(32 * kPfWarps) point_fused_kernel(PointBitsArg
                         uint2 hv;
                         hv.x = *reinterpret_cast<const uint32_t*>(&h01);
                         hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-                        reinterpret_cast<uint2*>(a.out16.d + (int64_t)s * a.out16.ss +
-                                                 ((int64_t)(y + a.out16.hh) * a.out16.Wp + x + a.out16.hw) * a.out16.Cp)[c4] = hv;
+                        const int64_t u16 = (int64_t)s * a.out16.ss +
+                                            ((int64_t)(y + a.out16.hh) * a.out16.Wp + x + a.out16.hw) * a.out16.Cp;
+                        reinterpret_cast<uint2*>(a.out16.d + u16)[c4] = hv;
+                        if (a.out16b.d) reinterpret_cast<uint2*>(a.out16b.d + u16 + 2)[c4] = hv;
                     }
                 }
                 if (a.chg.d && ch) atomicOr(&s_ch[wl][x >> 5], 1u << (x & 31));  // (shared memory)

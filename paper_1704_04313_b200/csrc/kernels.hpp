@@ -54,6 +54,7 @@ struct PointBitsArgs {  // MAXPOOL (window/stride) or RELU (relu=1, window=strid
     // optional fp16 shadow of `out` (round to nearest even) for a kind::f16
     // consumer; channels counted in 4-byte units (Cp = fp16 channels / 2)
     TensorView out16;
+    TensorView out16b;  // packed shadows: the same written again 8 bytes further (conv_tc packed gather)
     int* f16_overflow;  // set to 1 when a value written to out16 exceeds the fp16 range
 };
 void launch_point_bits(const PointBitsArgs& a, cudaStream_t st);
