@@ -1051,7 +1051,7 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     // columns [j * grpN, j * grpN + O), grpN = O rounded up to 32 (the
     // epilogue's tcgen05.ld granularity)
     int nchunks = g.kernelH * (g.kernelW + grpR - 1) * (t->Cp / 4);
-    if (f16 && pack && g.inChannels % 2 == 0 && pair_mode <= 0 && grpR == 1) {
+    if (f16 && pack && g.inChannels % 2 == 0 && grpR == 1) {
         // packed fp16 operands: a kernel row's kw x C halves are contiguous in
         // the unpadded shadow (Cp = C/2 units) -> ceil(kw C 2 / 16) chunks per
         // kernel row instead of kw ceil(C / 8) (paper layer 3: 46 vs 49)
@@ -1243,16 +1243,20 @@ void tc_load_weights(TcLayer& t, const float* K, cudaStream_t st) {
         // h = 8 i + e of kernel row kj's window (tap ki = h / C, channel
         // c = h % C; h >= kw C: next pixel, zero weight)
         const int C = g.inChannels;
-        std::vector<__half> img((size_t)t.NKB * t.Brows * 64, __float2half_rn(0.0f));
-        for (int n = 0; n < g.outChannels; ++n)
+        std::vector<__half> img((size_t)ranks * t.NKB * t.Brows * 64, __float2half_rn(0.0f));
+        for (int n = 0; n < g.outChannels; ++n) {
+            int rank, row;
+            place(n, rank, row);
+            __half* base = img.data() + (size_t)rank * t.NKB * t.Brows * 64;
             for (int kj = 0; kj < g.kernelH; ++kj)
                 for (int h = 0; h < g.kernelW * C; ++h) {
                     const int ki = h / C, c = h % C;
                     const int J = kj * t.pack_cpr + h / 8, e = h % 8;
                     const int kb = J / kChunksPerKB, jj = J % kChunksPerKB;
-                    img[(size_t)kb * t.Brows * 64 + (size_t)n * 64 + ((jj ^ (n & 7)) * 8) + e] =
+                    base[(size_t)kb * t.Brows * 64 + (size_t)row * 64 + ((jj ^ (row & 7)) * 8) + e] =
                         __float2half_rn(K[(size_t)n * Kref + ((size_t)c * g.kernelH + kj) * g.kernelW + ki]);
                 }
+        }
         CBX_CUDA(cudaMemcpyAsync(t.Bw, img.data(), img.size() * sizeof(__half), cudaMemcpyHostToDevice, st));
         CBX_CUDA(cudaStreamSynchronize(st));
         return;

@@ -1538,7 +1538,7 @@ void Engine::set_option(int option, int value) {
             if (tc_input_cp(*tc_[k]) != cp_before) relayout = true;
         }
         if (relayout) {
-            // the fp16 shadow layout changed (CTA pairs read the padded one):
+            // the fp16 shadow layout changed (packing depends on the layer shape):
             // new plans, and the next frame is a full evaluation
             CBX_CUDA(cudaStreamSynchronize(stream_));
             cb_.reset(new Plan);
