@@ -1,0 +1,2 @@
+# lean MMA issue loop for the tf32 single-instruction layer (L2): timing builds
+bash scripts/ab_libs.sh "timeout 300 python scripts/frame_probe.py --profile | tail -3 | head -1 | grep -o 'conv_tc.2.=[0-9.]*us\|conv_tc_tail.4.=[0-9.]*us' | tr '\n' ' '; echo" base.so lean.so l2all.so l2alllean.so
