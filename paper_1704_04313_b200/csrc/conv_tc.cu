@@ -672,6 +672,14 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
             const uint64_t a_desc0 = smem_desc(smem_u32(sA)), b_desc0 = smem_desc(smem_u32(sB));
             // descriptor start-address field is in 16-byte units
             const uint64_t a_st = kABytes >> 4, b_st = b_bytes >> 4, b1_d = b1_off >> 4;
+#ifdef CBX_EXP_SOLO
+#define MMA_ELECT true
+#define MMA_SYNCWARP (void)0
+            if (lane == 0) {
+#else
+#define MMA_ELECT elect_one()
+#define MMA_SYNCWARP __syncwarp()
+#endif
             Ring rg;
             uint32_t acc_it = 0;
             for (int64_t tile = tile_first; tile < ntiles; tile += tile_step, ++acc_it) {
@@ -694,7 +702,7 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                     tc_fence_after();
                     const uint64_t ad = a_desc0 + st * a_st, bd = b_desc0 + st * b_st;
                     const int nk = kb + 1 == a.NKB ? a.kinst_last : kKBlock / 8;
-                    if (elect_one()) {
+                    if (MMA_ELECT) {
 #pragma unroll
                         for (int k = 0; k < kKBlock / 8; ++k) {
                             if (k >= nk) break;
@@ -719,13 +727,18 @@ __global__ void __launch_bounds__(kThreads, PAIR ? 1 : 2) conv_tc_kernel(TcArgs 
                         }
                         if constexpr (PAIR) mma_commit_pair(&empty[st]); else mma_commit(&empty[st]);
                     }
-                    __syncwarp();
+                    MMA_SYNCWARP;
                 }
-                if (elect_one()) {
+                if (MMA_ELECT) {
                     if constexpr (PAIR) mma_commit_pair(&tfull[as]); else mma_commit(&tfull[as]);
                 }
-                __syncwarp();
+                MMA_SYNCWARP;
             }
+#ifdef CBX_EXP_SOLO
+            }
+#endif
+#undef MMA_ELECT
+#undef MMA_SYNCWARP
         }
         __syncwarp();
     } else {
