@@ -1064,10 +1064,12 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     // columns [j * grpN, j * grpN + O), grpN = O rounded up to 32 (the
     // epilogue's tcgen05.ld granularity)
     int nchunks = g.kernelH * (g.kernelW + grpR - 1) * (t->Cp / 4);
-    if (f16 && pack && g.inChannels % 2 == 0 && grpR == 1) {
+    if (f16 && pack && g.inChannels % 4 == 0 && grpR == 1) {
         // packed fp16 operands: a kernel row's kw x C halves are contiguous in
         // the unpadded shadow (Cp = C/2 units) -> ceil(kw C 2 / 16) chunks per
-        // kernel row instead of kw ceil(C / 8) (paper layer 3: 46 vs 49)
+        // kernel row instead of kw ceil(C / 8) (paper layer 3: 46 vs 49).
+        // C % 4 == 0 keeps every window origin 8-byte aligned (even Cp), so it
+        // is 16-byte aligned in the shadow or in its 8-byte-shifted copy
         t->Cp = g.inChannels / 2;
         t->pack_cpr = (g.kernelW * g.inChannels * 2 + 15) / 16;
         nchunks = g.kernelH * t->pack_cpr;

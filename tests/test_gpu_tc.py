@@ -49,6 +49,14 @@ F16_CASES = [
     (13, 34, 38, dict(kind="CBCONV", kernelH=3, kernelW=3, padH=1, padW=1, outChannels=300, threshold=0.0, fuseRelu=True, weightsFile="b")),
     (20, 40, 50, dict(kind="CBCONV", kernelH=5, kernelW=3, strideH=2, strideW=1, padH=2, padW=1, outChannels=160, threshold=0.0, fuseRelu=False, weightsFile="b")),
     (6, 26, 30, dict(kind="CONV", kernelH=1, kernelW=1, outChannels=136, weightsFile="b")),
+    # packed fp16 gather (channels a multiple of 4, even padded row): 3 x 12
+    # halves = 72 B per kernel row, the 5th chunk runs 8 B into the next
+    # pixel, windows start on both 8-byte parities (24-byte pixels); 5 x 20
+    # halves = 200 B (13 chunks) with stride 2; and 10 channels (20-byte
+    # pixels: not 8-byte aligned, so the padded layout is kept)
+    (12, 36, 44, dict(kind="CBCONV", kernelH=3, kernelW=3, padH=1, padW=1, outChannels=144, threshold=0.0, fuseRelu=True, weightsFile="b")),
+    (20, 44, 52, dict(kind="CBCONV", kernelH=5, kernelW=5, strideH=2, strideW=2, padH=2, padW=2, outChannels=160, threshold=0.0, fuseRelu=False, weightsFile="b")),
+    (10, 36, 44, dict(kind="CBCONV", kernelH=3, kernelW=3, padH=1, padW=1, outChannels=144, threshold=0.0, fuseRelu=True, weightsFile="b")),
 ]
 
 
@@ -149,6 +157,23 @@ def test_f16_layer_vs_exact(gpu, orc, monkeypatch, cin, h, w, layer, maxctas, pa
         x = onet.layer_output(1)
         assert 0 < np.abs(x).max() < 6.1e-5 * 4  # mostly below the fp16 normal range
         onet.reset_state()
+    _check_layer(gpu, orc, net, onet, spec, wts, cfg, 2, cin, True)
+
+
+@pytest.mark.parametrize("pack", ["0", "1"])
+def test_f16_packed_and_padded_gather(gpu, orc, monkeypatch, pack):
+    """The paper's layer 3 (52 -> 304, 7x7) with the packed fp16 gather
+    (52 channels unpadded, 46 chunks per kernel row, odd-parity windows from
+    the 8-byte-shifted shadow) and with CBX_TC_PACK=0 (channels padded to 56,
+    49 chunks): both within the kind::f16 bound of the exact oracle."""
+    monkeypatch.setenv("CBX_TC_PACK", pack)
+    cin, h, w, layer = F16_CASES[0]
+    spec = pooled_layer(cin, h, w, layer)
+    wts = orc.generate_weights(spec, 17)
+    onet = orc.load_network(spec, wts)
+    net = gpu.Network(to_pkg_spec(gpu, spec), wts, precision="f16")
+    assert net.layer_operands(2) == "f16"
+    cfg = dict(channels=3, height=h, width=w, sprites=[(6, 3, 0.9)], noise=0.02, seed=9)
     _check_layer(gpu, orc, net, onet, spec, wts, cfg, 2, cin, True)
 
 
