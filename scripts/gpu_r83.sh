@@ -1,0 +1,3 @@
+# smaller footprints for the narrow tensor-core convs (stages), whole step
+q() { echo -n "$QE : "; timeout 300 env $QE python bench.py --quick --steps 30 --streams 16 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['ms_per_step'],4), d['clocks']['sm_mhz'])"; }
+for i in 1 2; do QE="CBX_X=0" q; QE="CBX_TC_STAGES=2 CBX_TC_STAGES_WIDE=3" q; QE="CBX_MPR_STAGES=2" q; QE="CBX_TC_STAGES=4 CBX_TC_STAGES_WIDE=3" q; done
