@@ -515,6 +515,15 @@ def run_gpu_arm(args):
     except (OSError, ValueError):
         pass
     roof["kernel"] = f"{kname}[layer {klayer}]"
+    if bound == "tensor" and kname == "conv_tc_tail":
+        # the instruction-shape ceiling of the paper's layer 3: N = 304 output
+        # channels exceed one tcgen05.mma (N <= 256), so every 32-byte K step is
+        # two instructions (N = 160 + 144); measured issue cost 101 + 95 clk
+        # against 136.7 clk for a full-rate N = 256 instruction
+        # (profiles/r2_mma_shape.log): at most (304 / 256) * 136.7 / 196 of the peak
+        ceil_ = (304.0 / 256.0) * 136.7 / 196.0
+        roof["mma_shape_ceiling_frac"] = round(ceil_, 3)
+        roof["frac_of_shape_ceiling"] = roof["frac"] / ceil_
     # share of the serial sum of the frame's kernel times (graph-free pass,
     # lanes one after the other); the graph-timed step overlaps the lanes
     roof["kernel_share_of_kernel_sum"] = kms / step_ms if step_ms else None
