@@ -212,7 +212,7 @@ int run3(int N, unsigned long long* clk) {
     return 0;
 }
 
-int main() {
+int main(int argc, char**) {
     unsigned long long* clk;
     CK(cudaMalloc(&clk, 148 * sizeof(unsigned long long)));
     const int iters = 4096;
@@ -222,6 +222,11 @@ int main() {
     const C cs[] = {{1, 64, 0, 1}, {1, 64, 0, 2}, {1, 64, 0, 4}, {1, 64, 0, 8}, {0, 64, 0, 1}, {0, 64, 0, 4},
                     {0, 128, 0, 1}, {0, 128, 0, 2}, {0, 128, 0, 4}, {0, 256, 0, 1}, {0, 256, 0, 2},
                     {0, 160, 144, 1}, {0, 128, 176, 1}, {0, 256, 48, 1}, {0, 192, 112, 1}};
+    if (argc > 1) {  // f16 cost per N (rotating stages), then exit
+        for (int N = 16; N <= 256; N += 16) run3<0, 3, 1>(N, clk);
+        for (int N = 16; N <= 256; N += 16) run2<0, 1, 1>(N, clk);
+        return 0;
+    }
     run3<1, 3, 0>(64, clk); run3<1, 3, 1>(64, clk); run3<0, 3, 0>(256, clk); run3<0, 3, 1>(256, clk); run3<0, 3, 1>(160, clk); run3<0, 3, 1>(128, clk);
     run2<1, 1, 1>(64, clk); run2<1, 1, 0>(64, clk); run2<1, 2, 1>(64, clk); run2<1, 4, 1>(64, clk);
     run2<0, 1, 1>(128, clk); run2<0, 2, 1>(128, clk); run2<0, 1, 1>(256, clk); run2<0, 2, 1>(256, clk);
