@@ -1143,7 +1143,9 @@ std::unique_ptr<TcLayer, TcLayerDeleter> make_tc_layer(const cbx_geom& g, int ta
     // kernels co-reside with the persistent CTAs (16 x 1080p: 30.3k -> 30.9k
     // frames/s; with the 3-stage layer-1 conv, 31.4k). CBX_TC_STAGES /
     // CBX_TC_STAGES_WIDE (N > 256) override (tuning).
-    int ns = t->pair ? 4 : 3;
+    // grouped layers: two stages keep the footprint of the wider N (the
+    // other lane's kernels run beside it) at the one-pixel layer's size
+    int ns = t->pair ? 4 : t->grpR > 1 ? 2 : 3;
     if (const char* e = std::getenv("CBX_TC_STAGES")) ns = std::max(2, std::min(16, std::atoi(e)));
     if (t->Npad > 256)
         if (const char* e = std::getenv("CBX_TC_STAGES_WIDE")) ns = std::max(2, std::min(16, std::atoi(e)));

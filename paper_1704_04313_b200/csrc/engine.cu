@@ -353,8 +353,13 @@ bool Engine::pack_f16(int k) const {
     return ((W + 2 * layers_[k].geom.padW) & 1) == 0;
 }
 
+// Pixel groups of R = 2 for narrow tcgen05 layers on a 4-channel input (the
+// paper's layer 2): one tensor-core row carries two adjacent output pixels
+// (N = 2 x 64 costs what N = 64 does: profiles/r2_mma_cost_by_n.log), 56 K
+// taps for two pixels instead of 49 for one. CBX_TC_GROUP overrides (1 = one
+// pixel per row).
 int Engine::group_width_for(const cbx_geom& g) const {
-    int R = 1;
+    int R = 2;
     if (const char* e = std::getenv("CBX_TC_GROUP")) R = std::max(1, std::min(4, std::atoi(e)));
     while (R > 1 && !tc_group_supported(g, R)) R /= 2;
     return R;
